@@ -1,0 +1,180 @@
+/*
+ * lic.h -- C ABI of the B200 learned-image-codec hot path (arXiv 2208.01641).
+ *
+ * The paper states the problem as "encode an image" into strings and "decode strings"
+ * into an image (§III.A-B, Fig. 1); its encoder GPU workload is g_a, h_a, the
+ * quantisation of z and h_s, its decoder GPU workloads are h_s (GPU1) and
+ * g_s (GPU2) of the 4-stage CPU1-GPU1-CPU2-GPU2 pipeline, and the entropy
+ * coder is a CPU workload.  This library therefore exports:
+ *   - GPU: lic_encode      frame(s)  -> y symbols (+ y CDF indexes, z symbols)
+ *          lic_hyper_indexes z symbols -> y CDF indexes         (decoder GPU1)
+ *          lic_decode      y symbols -> frame(s)                (decoder GPU2)
+ *   - HOST: CDF tables and the rANS coder (lic_cdf*, lic_rans_*), reentrant, no GPU.
+ * Every step of the GPU path runs in this library's sm_100a kernels; there is no CPU
+ * fallback.  Names follow the paper's notation (x, y, z, y-hat, z-hat, sigma).
+ *
+ * Conventions
+ *   - Frames: f32 planar [batch][3][H][W] with values in [0,1] (lic_encode / lic_decode),
+ *     or u8 interleaved [batch][H][W][3] (lic_*_u8; x = u8/255 on input, out =
+ *     round_half_away(255 * x-hat) on output).  H x W is the geometry given to lic_open;
+ *     the library pads it centred with zeros to a multiple of 16 (factorized) or 64
+ *     (hyperprior) and crops after decode.
+ *   - Symbol planes: int8 [batch][C][Hl][Wl] in channel-major raster order, values in
+ *     [-L, L]; y CDF indexes uint8 with the same shape ("scales information
+ *     deduced from z"; SPEC.md:135-139 SymbolPlane).  Shapes from lic_shapes.
+ *   - Pointers may be device pointers, pinned host pointers (cudaHostAlloc /
+ *     lic_buf_acquire: kernels read/write them in place, the paper's zero-copy,
+ *     PAPER.md:84), or ordinary host pointers (staged through library-owned pinned
+ *     buffers).  The caller owns every array it passes.
+ *   - `stream` is a cudaStream_t passed as void*.  NULL: the library uses its own stream
+ *     and returns after the work (and any host copy) is complete.  Non-NULL: work is
+ *     enqueued and the call returns; outputs are valid after the caller synchronises
+ *     the stream.
+ *   - Device memory is allocated once in lic_open and freed only in lic_close (PAPER.md:105
+ *     "we carefully control dynamic memory allocation/deallocation and pool the
+ *     allocated memory"); no call allocates or frees device memory in steady state.
+ *   - Errors: every call returns lic_status; nothing aborts or throws across the ABI
+ *     ("never a panic").  A CUDA failure is sticky for the codec (LIC_ECUDA).
+ *   - Concurrency: one lic_codec is driven by one thread at a time; the host coder
+ *     functions are reentrant and may run on any number of threads.
+ */
+#ifndef LIC_H
+#define LIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lic_codec lic_codec;
+
+typedef enum {
+    LIC_OK = 0,
+    LIC_EINVAL = 1,     /* bad argument or invalid weights (beta <= 0, gamma < 0: SPEC.md:102) */
+    LIC_ESHAPE = 2,     /* geometry / batch mismatch */
+    LIC_ECORRUPT = 3,   /* corrupt or truncated bitstream */
+    LIC_EDIGEST = 4,    /* weights container failed validation */
+    LIC_ENOMEM = 5,     /* allocation failed (only in lic_open / pool growth) */
+    LIC_ECUDA = 6,      /* CUDA error (sticky) or no sm_100 device */
+    LIC_EFOREIGN = 7,   /* buffer not owned by this pool */
+    LIC_ENOSPACE = 8    /* output capacity too small */
+} lic_status;
+
+typedef struct { uint32_t c, h, w; } lic_shape;
+
+typedef enum {
+    LIC_PREC_SPLIT = 0, /* activations as fp16 hi + lo planes, fp32 accumulation (graded) */
+    LIC_PREC_F16 = 1    /* single fp16 activation plane (the paper's TensorRT FP16) */
+} lic_precision;
+
+/* ---------------------------------------------------------------- codec lifetime */
+
+/* Parse and validate an LICW weights container (layout in DESIGN.md §4),
+ * upload the weights to `device`, plan every layer for frames of height x width and up
+ * to max_batch frames per call, allocate all device memory.  `licw` is only read during
+ * the call.  Errors: LIC_EDIGEST (malformed container), LIC_EINVAL (beta <= 0, gamma < 0,
+ * unsupported N/M), LIC_ESHAPE (zero geometry), LIC_ECUDA (no sm_100 device), LIC_ENOMEM. */
+lic_status lic_open(const uint8_t* licw, size_t len, int device, uint32_t height, uint32_t width,
+                    uint32_t max_batch, int precision, lic_codec** out);
+void lic_close(lic_codec* codec);
+
+/* Latent shapes per frame: y = M x Hp/16 x Wp/16; z = N x Hp/64 x Wp/64 (z = {0,0,0}
+ * for the factorized codec).  `kind` receives 0 (factorized) or 1 (hyperprior). */
+lic_status lic_shapes(const lic_codec* codec, lic_shape* y, lic_shape* z, int* kind);
+
+/* Message for the last error on this codec (owned by the codec). */
+const char* lic_last_error(const lic_codec* codec);
+
+/* ---------------------------------------------------------------- pooled pinned buffers */
+
+/* Pinned, device-mapped host buffers from an exact-size free-list pool (
+ * PAPER.md:84 zero-copy, :105 pooling).  Kernels write symbol planes straight into them.
+ * acquire reuses a released buffer of the same size before allocating.  release of a
+ * pointer not from this pool returns LIC_EFOREIGN. */
+lic_status lic_buf_acquire(lic_codec* codec, size_t bytes, void** host_ptr);
+lic_status lic_buf_release(lic_codec* codec, void* host_ptr);
+/* counters: allocations, reuses (SPEC.md:359 pool_allocations / pool_reuses) */
+lic_status lic_buf_stats(const lic_codec* codec, uint64_t* allocations, uint64_t* reuses);
+
+/* ---------------------------------------------------------------- GPU entry points */
+
+/* Encode (PAPER.md:68 factorized, :74 hyperprior GPU workload):
+ *   x -> g_a -> y; factorized: y_sym = clamp(round_half_away(y - mu_c), -L, L);
+ *   hyperprior: z = h_a(|y|), z_sym = clamp(round(z - mu_z)), z-hat = z_sym + mu_z,
+ *   sigma = h_s(z-hat), y_idx = #{j <= 62 : table_j < max(sigma, 0.11)},
+ *   y_sym = clamp(round(y)).
+ * y_idx and z_sym must be NULL for the factorized codec and non-NULL for the hyperprior.
+ * n_saturated (nullable) receives the number of clamped symbols.  batch <= max_batch. */
+lic_status lic_encode(lic_codec* codec, const float* frames, uint32_t batch,
+                      int8_t* y_sym, uint8_t* y_idx, int8_t* z_sym, uint64_t* n_saturated,
+                      void* stream);
+lic_status lic_encode_u8(lic_codec* codec, const uint8_t* frames_hwc, uint32_t batch,
+                         int8_t* y_sym, uint8_t* y_idx, int8_t* z_sym, uint64_t* n_saturated,
+                         void* stream);
+
+/* Hyperprior decoder stage GPU1: z_sym -> z-hat -> h_s -> y CDF indexes.
+ * Bit-identical to the y_idx lic_encode produced from the same z symbols. */
+lic_status lic_hyper_indexes(lic_codec* codec, const int8_t* z_sym, uint32_t batch,
+                             uint8_t* y_idx, void* stream);
+
+/* Decoder stage GPU2: y-hat = y_sym + mu_c (hyperprior: mu = 0),
+ * x-hat = clamp(g_s(y-hat), 0, 1) cropped to H x W. */
+lic_status lic_decode(lic_codec* codec, const int8_t* y_sym, uint32_t batch, float* frames,
+                      void* stream);
+lic_status lic_decode_u8(lic_codec* codec, const int8_t* y_sym, uint32_t batch,
+                         uint8_t* frames_hwc, void* stream);
+
+/* ---------------------------------------------------------------- test-only exports
+ * Same device code as the hot path, exposed for per-layer parity tests. */
+
+/* Layer ids: 0-3 g_a L1-L4, 4-7 g_s L1-L4, 8-10 h_a L1-L3, 11-13 h_s L1-L3.
+ * in: f32 [batch][Cin][Hin][Win] (the layer's input in padded coordinates; for g_a L1 the
+ * padded frame); out: f32 [batch][Cout][Hout][Wout] = the layer's output after its fused
+ * activation (g_a L4: y; h_a L3: z; h_s L3: sigma after ReLU; g_s L4: clamp to [0,1]). */
+lic_status lic_test_layer(lic_codec* codec, int layer_id, const float* in, uint32_t batch,
+                          float* out, void* stream);
+/* Shapes of a layer: input (c,h,w) and output (c,h,w). */
+lic_status lic_layer_shapes(const lic_codec* codec, int layer_id, lic_shape* in, lic_shape* out);
+/* sigma -> index exactly as the h_s L3 epilogue computes it, on a given sigma array. */
+lic_status lic_test_sigma_to_index(lic_codec* codec, const float* sigma, size_t n, uint8_t* idx);
+/* When enabled, lic_encode also keeps y (and z, sigma) as f32 for lic_debug_latents. */
+lic_status lic_set_debug(lic_codec* codec, int on);
+lic_status lic_debug_latents(lic_codec* codec, uint32_t batch, float* y, float* z, float* sigma);
+
+/* ---------------------------------------------------------------- HOST entropy coder */
+
+/* CDF tables of this codec: which = 0 factorized y rows (one per
+ * channel, from sigma_c), 1 z rows (one per channel, sigma_z), 2 Gaussian rows (one per
+ * scale-table entry).  Rows are row_len = 2L+2 uint32 cumulative frequencies 0..65536.
+ * The table is owned by the codec.  LIC_EINVAL if the codec has no such table. */
+lic_status lic_cdf(const lic_codec* codec, int which, const uint32_t** rows, uint32_t* n_rows,
+                   uint32_t* row_len);
+
+/* Build one CDF row per sigma (zero-mean discretised Gaussian over [-L, L], tails folded,
+ * 16-bit quantised, every frequency >= 1).  out: n x (2L+2) uint32. */
+lic_status lic_cdf_build(const float* sigmas, uint32_t n, uint32_t L, uint32_t* out);
+
+/* rANS: 32-bit state, L = 2^23, byte-wise
+ * renormalisation, 16-bit precision, symbols coded in reverse raster order, 4-byte
+ * big-endian final state at the front.  Symbol s uses CDF row `row[i]` (uint8, per symbol)
+ * or, if row == NULL, row = channel index of the C x H x W plane.  Symbol s occupies CDF
+ * entries [s - sym_min, s - sym_min + 1].  out: capacity `cap` bytes, written length in
+ * *out_len.  Errors: LIC_EINVAL (symbol out of range / bad row), LIC_ENOSPACE (cap). */
+lic_status lic_rans_encode(const int8_t* sym, const uint8_t* row, lic_shape plane,
+                           const uint32_t* cdf, uint32_t n_rows, uint32_t row_len, int sym_min,
+                           uint8_t* out, size_t cap, size_t* out_len);
+/* Inverse of lic_rans_encode.  LIC_ECORRUPT if the stream is exhausted early, a slot is
+ * outside the table, or the final state is not 2^23 with every byte consumed. */
+lic_status lic_rans_decode(const uint8_t* in, size_t len, const uint8_t* row, lic_shape plane,
+                           const uint32_t* cdf, uint32_t n_rows, uint32_t row_len, int sym_min,
+                           int8_t* sym_out);
+
+/* Library version string. */
+const char* lic_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIC_H */

@@ -1,0 +1,870 @@
+// codec.cu -- the lic_codec runtime behind include/lic.h.
+//
+//  * parses + validates the LICW container and repacks the
+//    weights into the GEMM engine's layout (fp16 W[tap][co][ci]);
+//  * plans every transform layer once per (geometry, max_batch): GEMM grid, tile shape,
+//    tap lists (conv / sub-pixel deconv phases), pipeline depth, TMEM budget, TMA maps;
+//  * owns all device memory, allocated once in lic_open, freed in lic_close;
+//  * owns a pinned, device-mapped host buffer pool (PAPER.md:84 zero-copy, :105 pooling);
+//  * runs encode, hyper_indexes (decoder GPU1, :76) and decode (GPU2).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/lic.h"
+#include "layer.h"
+
+namespace lic {
+cudaError_t launch_conv_umma(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const ConvParams&, int,
+                             cudaStream_t);
+cudaError_t launch_ingest(const void*, int, int, int, int, int, int, int, int, __half*, size_t, int, cudaStream_t);
+cudaError_t launch_sym_ingest(const int8_t*, const float*, int, int, int, int, __half*, size_t, int, cudaStream_t);
+cudaError_t launch_pack_chw(const float*, int, int, int, int, __half*, size_t, int, cudaStream_t);
+cudaError_t launch_sigma_index(const float*, size_t, const float*, uint8_t*, cudaStream_t);
+}  // namespace lic
+
+using namespace lic;
+
+// ------------------------------------------------------------------ tensor-map encoder
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+
+// TMA box semantics for strided traversal: boxDim counts elements of the *unstrided*
+// footprint; the unit loads ceil(boxDim / elementStride) of them (CUDA driver API,
+// cuTensorMapEncodeTiled "elementStrides").
+#ifndef LIC_TMA_BOX_SCALED
+#define LIC_TMA_BOX_SCALED 1
+#endif
+
+// ------------------------------------------------------------------ LICW format
+namespace {
+
+enum Role { R_CONV, R_DECONV, R_BIAS, R_BETA, R_GAMMA, R_PARAM };
+struct BlockSpec { int tag; std::string name; Role role; std::vector<int> shape; bool hyper_only; };
+
+std::vector<BlockSpec> licw_blocks(int N, int M) {
+    std::vector<BlockSpec> b;
+    int tag = 0;
+    auto add = [&](const std::string& n, Role r, std::vector<int> s, bool h) { b.push_back({++tag, n, r, s, h}); };
+    for (int i = 1; i <= 3; ++i) {
+        int cin = i == 1 ? 3 : N;
+        add("ga" + std::to_string(i) + ".w", R_CONV, {N, cin, 5, 5}, false);
+        add("ga" + std::to_string(i) + ".b", R_BIAS, {N}, false);
+        add("ga" + std::to_string(i) + ".beta", R_BETA, {N}, false);
+        add("ga" + std::to_string(i) + ".gamma", R_GAMMA, {N, N}, false);
+    }
+    add("ga4.w", R_CONV, {M, N, 5, 5}, false);
+    add("ga4.b", R_BIAS, {M}, false);
+    for (int i = 1; i <= 3; ++i) {
+        int cin = i == 1 ? M : N;
+        add("gs" + std::to_string(i) + ".w", R_DECONV, {N, cin, 5, 5}, false);
+        add("gs" + std::to_string(i) + ".b", R_BIAS, {N}, false);
+        add("gs" + std::to_string(i) + ".beta", R_BETA, {N}, false);
+        add("gs" + std::to_string(i) + ".gamma", R_GAMMA, {N, N}, false);
+    }
+    add("gs4.w", R_DECONV, {3, N, 5, 5}, false);
+    add("gs4.b", R_BIAS, {3}, false);
+    add("ha1.w", R_CONV, {N, M, 3, 3}, true);
+    add("ha1.b", R_BIAS, {N}, true);
+    add("ha2.w", R_CONV, {N, N, 5, 5}, true);
+    add("ha2.b", R_BIAS, {N}, true);
+    add("ha3.w", R_CONV, {N, N, 5, 5}, true);
+    add("ha3.b", R_BIAS, {N}, true);
+    add("hs1.w", R_DECONV, {N, N, 5, 5}, true);
+    add("hs1.b", R_BIAS, {N}, true);
+    add("hs2.w", R_DECONV, {N, N, 5, 5}, true);
+    add("hs2.b", R_BIAS, {N}, true);
+    add("hs3.w", R_CONV, {M, N, 3, 3}, true);
+    add("hs3.b", R_BIAS, {M}, true);
+    add("mu_y", R_PARAM, {M}, false);
+    add("sigma_y", R_PARAM, {M}, false);
+    add("mu_z", R_PARAM, {N}, true);
+    add("sigma_z", R_PARAM, {N}, true);
+    add("scale_table", R_PARAM, {64}, false);
+    return b;
+}
+
+template <typename T>
+T rd(const uint8_t* p) { T v; std::memcpy(&v, p, sizeof(T)); return v; }  // little-endian host
+
+}  // namespace
+
+// ------------------------------------------------------------------ codec state
+enum LayerId { GA1 = 0, GA2, GA3, GA4, GS1, GS2, GS3, GS4, HA1, HA2, HA3, HS1, HS2, HS3, NLAYER };
+static const char* kLayerW[NLAYER] = {"ga1", "ga2", "ga3", "ga4", "gs1", "gs2", "gs3", "gs4",
+                                      "ha1", "ha2", "ha3", "hs1", "hs2", "hs3"};
+
+struct Layer {
+    bool present = false;
+    bool deconv = false;
+    int k = 5, s = 2, p = 2;
+    int Cin = 0, Cin_eff = 0, Cout = 0;
+    int Hin = 0, Win = 0, Hout = 0, Wout = 0;
+    EpKind ep = EP_F32;
+    __half* w = nullptr;      // [ntaps_w][Cout_pad][Cin_eff]
+    float* bias = nullptr;
+    float* beta = nullptr;
+    __half* gamma = nullptr;  // [Cout][Cout]
+    __half* in_buf = nullptr;
+    size_t in_plane = 0;
+    __half* out_buf = nullptr;
+    size_t out_plane = 0;
+    ConvParams prm{};
+    CUtensorMap mapA{}, mapB{}, mapG{};
+};
+
+struct lic_codec {
+    int device = 0, num_sms = 148;
+    int kind = 0, act = 0, N = 0, M = 0, L = 32;
+    int H = 0, W = 0, Hp = 0, Wp = 0, top = 0, left = 0;
+    int max_batch = 1, split = 2;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    bool sticky = false;
+    Layer layers[NLAYER];
+    // device buffers
+    __half *bufI = nullptr, *bufA = nullptr, *bufB = nullptr, *bufY = nullptr, *bufZ = nullptr;
+    size_t planeI = 0, planeA = 0, planeY = 0, planeZ = 0;
+    float *mu_y = nullptr, *mu_z = nullptr, *table = nullptr;
+    unsigned long long* d_sat = nullptr;
+    void* d_frames = nullptr;           // staging for host frames (f32 CHW size)
+    int8_t* d_ysym = nullptr;
+    uint8_t* d_yidx = nullptr;
+    int8_t* d_zsym = nullptr;
+    float* d_dbg = nullptr;             // test-layer / debug scratch
+    size_t dbg_elems = 0;
+    float *dbg_y = nullptr, *dbg_z = nullptr, *dbg_s = nullptr;
+    int debug = 0;
+    std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
+    std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
+    std::vector<void*> allocs;          // device allocations to free
+    // pinned pool
+    std::mutex pool_mu;
+    std::map<size_t, std::vector<void*>> free_lists;
+    std::map<void*, size_t> owned;
+    uint64_t pool_allocs = 0, pool_reuses = 0;
+};
+
+static lic_status fail(lic_codec* c, lic_status st, const char* fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+        if (st == LIC_ECUDA) c->sticky = true;
+    }
+    return st;
+}
+
+#define CK(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) return fail(c, LIC_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename T>
+static lic_status dalloc(lic_codec* c, T** p, size_t bytes) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, bytes ? bytes : 16) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, LIC_ENOMEM, "cudaMalloc(%zu) failed", bytes);
+    }
+    c->allocs.push_back(q);
+    *p = (T*)q;
+    return LIC_OK;
+}
+
+// ------------------------------------------------------------------ planning helpers
+// plane_elems: distance between the hi and lo planes of the buffer (its full plane size,
+// which exceeds B*H*W*C when a large buffer is reused by a smaller layer)
+static bool encode_act_map(CUtensorMap* m, const __half* base, int C, int W, int H, int B, int planes,
+                           size_t plane_elems, int box_w, int box_h, int es) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B, (cuuint64_t)planes};
+    cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2,
+                         (cuuint64_t)plane_elems * 2};
+#if LIC_TMA_BOX_SCALED
+    cuuint32_t box[5] = {64, (cuuint32_t)(box_w * es), (cuuint32_t)(box_h * es), 1, 1};
+#else
+    cuuint32_t box[5] = {64, (cuuint32_t)box_w, (cuuint32_t)box_h, 1, 1};
+#endif
+    cuuint32_t es5[5] = {1, (cuuint32_t)es, (cuuint32_t)es, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, (void*)base, dims, str, box, es5, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool encode_w_map(CUtensorMap* m, const __half* base, int K, int rows, int depth, int box_rows) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)depth};
+    cuuint64_t str[2] = {(cuuint64_t)K * 2, (cuuint64_t)rows * K * 2};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, (void*)base, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// choose Wt x Ht = 128 minimising padded tiles over the grid
+static void choose_tile(int Hg, int Wg, int* Wt, int* Ht) {
+    static const int opts[5][2] = {{16, 8}, {32, 4}, {8, 16}, {64, 2}, {128, 1}};
+    long best = -1;
+    for (auto& o : opts) {
+        long tiles = (long)((Wg + o[0] - 1) / o[0]) * ((Hg + o[1] - 1) / o[1]);
+        if (best < 0 || tiles < best) { best = tiles; *Wt = o[0]; *Ht = o[1]; }
+    }
+}
+
+static int pow2_cols(int n) {
+    int c = 32;
+    while (c < n) c <<= 1;
+    return c;
+}
+
+// build the GEMM-side plan of one layer (everything except epilogue output pointers)
+static lic_status plan_layer(lic_codec* c, Layer& Ly) {
+    ConvParams& P = Ly.prm;
+    std::memset(&P, 0, sizeof P);
+    const bool gemm_l1 = (&Ly == &c->layers[GA1]);
+    P.Cin = Ly.Cin_eff;
+    P.kchunks = Ly.Cin_eff / 64;
+    P.Cout = Ly.Cout;
+    if (Ly.Cout <= 256) { P.BN = (Ly.Cout + 15) / 16 * 16; P.n_ntiles = 1; }
+    else { P.n_ntiles = (Ly.Cout + 255) / 256; P.BN = ((Ly.Cout + P.n_ntiles - 1) / P.n_ntiles + 15) / 16 * 16; }
+    const bool gdn = (Ly.ep == EP_GDN || Ly.ep == EP_IGDN);
+    if (gdn && (P.n_ntiles != 1 || P.BN != Ly.Cout || Ly.Cout % 64))
+        return fail(c, LIC_EINVAL, "GDN layer needs Cout %% 64 == 0 and Cout <= 256");
+    P.split = c->split;
+    int ntap = 0;
+    if (gemm_l1) {
+        P.Hg = Ly.Hout; P.Wg = Ly.Wout; P.stride = 1; P.out_s = 1; P.nphase = 1;
+        P.tap0[0] = 0; P.ntaps[0] = 1; P.tap_dy[0] = 0; P.tap_dx[0] = 0; P.tap_w[0] = 0;
+        ntap = 1;
+    } else if (!Ly.deconv) {
+        P.Hg = Ly.Hout; P.Wg = Ly.Wout; P.stride = Ly.s; P.out_s = 1; P.nphase = 1;
+        P.tap0[0] = 0;
+        for (int ky = 0; ky < Ly.k; ++ky)
+            for (int kx = 0; kx < Ly.k; ++kx) {
+                P.tap_dy[ntap] = ky - Ly.p; P.tap_dx[ntap] = kx - Ly.p; P.tap_w[ntap] = ky * Ly.k + kx; ++ntap;
+            }
+        P.ntaps[0] = ntap;
+    } else {
+        // stride-2 5x5 transposed conv, p = 2, output_padding 1: output (2qy+py, 2qx+px) takes
+        // taps ky = py (mod 2) from input row qy + (py + 2 - ky)/2 (same for x).
+        P.Hg = Ly.Hin; P.Wg = Ly.Win; P.stride = 1; P.out_s = 2; P.nphase = 4;
+        for (int ph = 0; ph < 4; ++ph) {
+            const int py = ph >> 1, px = ph & 1;
+            P.tap0[ph] = ntap;
+            for (int ky = py; ky < 5; ky += 2)
+                for (int kx = px; kx < 5; kx += 2) {
+                    P.tap_dy[ntap] = (py + 2 - ky) / 2; P.tap_dx[ntap] = (px + 2 - kx) / 2;
+                    P.tap_w[ntap] = ky * 5 + kx; ++ntap;
+                }
+            P.ntaps[ph] = ntap - P.tap0[ph];
+        }
+    }
+    choose_tile(P.Hg, P.Wg, &P.Wt, &P.Ht);
+    P.tiles_x = (P.Wg + P.Wt - 1) / P.Wt;
+    P.tiles_y = (P.Hg + P.Ht - 1) / P.Ht;
+    // shared memory plan
+    const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)P.BN * 64 * 2;
+    P.stage_bytes = a_bytes * P.split + b_bytes;
+    uint32_t extras = gdn ? (uint32_t)(P.BN / 64) * b_bytes + 2 * a_bytes : 0;
+    const uint32_t budget = 227 * 1024 - 1024 - 256;
+    int stages = (int)((budget - extras) / P.stage_bytes);
+    stages = std::min(stages, 8);
+    if (stages < 2) return fail(c, LIC_EINVAL, "layer does not fit shared memory");
+    P.stages = stages;
+    P.off_gamma = stages * P.stage_bytes;
+    P.off_xsq = P.off_gamma + (gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0);
+    P.off_bar = P.off_xsq + (gdn ? 2 * a_bytes : 0);
+    P.smem_bytes = P.off_bar + (2 * stages + 8) * 8 + 1024;
+    if (P.smem_bytes < 120 * 1024) P.smem_bytes = 120 * 1024;     // one CTA per SM (TMEM)
+    // TMEM plan: accumulator (+ GDN norm) per buffer, double-buffered when it fits
+    int per = std::max(32, P.BN) + (gdn ? P.BN : 0);
+    P.n_accbuf = (2 * per <= 512) ? 2 : 1;
+    P.acc_stride = per;
+    P.tmem_cols = pow2_cols(P.n_accbuf * per);
+    P.L = c->L;
+    // tensor maps
+    const int ntaps_w = gemm_l1 ? 1 : Ly.k * Ly.k;
+    const int cout_pad = P.BN * P.n_ntiles;
+    if (!encode_act_map(&Ly.mapA, Ly.in_buf, P.Cin, Ly.deconv ? Ly.Win : (gemm_l1 ? Ly.Wout : Ly.Win),
+                        Ly.deconv ? Ly.Hin : (gemm_l1 ? Ly.Hout : Ly.Hin), c->max_batch, P.split, Ly.in_plane,
+                        P.Wt, P.Ht, P.stride))
+        return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (activations) failed");
+    if (!encode_w_map(&Ly.mapB, Ly.w, P.Cin, cout_pad, ntaps_w, P.BN))
+        return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (weights) failed");
+    if (gdn) {
+        if (!encode_w_map(&Ly.mapG, Ly.gamma, Ly.Cout, Ly.Cout, 1, Ly.Cout))
+            return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (gamma) failed");
+    } else {
+        Ly.mapG = Ly.mapB;
+    }
+    // epilogue constants
+    P.ep = Ly.ep;
+    P.Hout = Ly.Hout;
+    P.Wout = Ly.Wout;
+    P.bias = Ly.bias;
+    P.beta = Ly.beta;
+    P.table = c->table;
+    P.out_act = Ly.out_buf;
+    P.act_plane = Ly.out_plane;
+    P.crop_top = 0; P.crop_left = 0; P.crop_H = Ly.Hout; P.crop_W = Ly.Wout;
+    return LIC_OK;
+}
+
+static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int batch, cudaStream_t st) {
+    ConvParams P = P0;
+    P.batch = batch;
+    P.total_tiles = batch * P.nphase * P.tiles_y * P.tiles_x * P.n_ntiles;
+    const int grid = std::min(P.total_tiles, c->num_sms);
+    CK(launch_conv_umma(Ly.mapA, Ly.mapB, Ly.mapG, P, grid, st));
+    return LIC_OK;
+}
+
+// ------------------------------------------------------------------ pointer handling
+// Returns a device-accessible alias of p (device memory or pinned/mapped host memory),
+// or nullptr if p is pageable host memory that must be staged.
+static void* device_alias(const void* p) {
+    if (!p) return nullptr;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return const_cast<void*>(p);
+    if (a.type == cudaMemoryTypeHost && a.devicePointer) return a.devicePointer;
+    return nullptr;
+}
+
+// ------------------------------------------------------------------ ABI
+extern "C" const char* lic_version(void) { return "lic-b200 0.1 (sm_100a tcgen05)"; }
+
+extern "C" const char* lic_last_error(const lic_codec* c) { return c ? c->err.c_str() : "null codec"; }
+
+extern "C" void lic_close(lic_codec* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (void* p : c->allocs) cudaFree(p);
+    {
+        std::lock_guard<std::mutex> g(c->pool_mu);
+        for (auto& kv : c->owned) cudaFreeHost(kv.first);
+    }
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+static lic_status upload(lic_codec* c, void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint32_t height, uint32_t width,
+                               uint32_t max_batch, int precision, lic_codec** out) {
+    if (!licw || !out || max_batch == 0) return LIC_EINVAL;
+    *out = nullptr;
+    if (height == 0 || width == 0 || height > 8192 || width > 8192) return LIC_ESHAPE;
+    if (precision != LIC_PREC_SPLIT && precision != LIC_PREC_F16) return LIC_EINVAL;
+    if (len < 13 || std::memcmp(licw, "LICW", 4) != 0 || licw[4] != 1) return LIC_EDIGEST;
+    lic_codec* c = new lic_codec();
+    auto bail = [&](lic_status st) { lic_close(c); return st; };
+    c->kind = licw[5];
+    c->act = licw[6];
+    c->N = rd<uint16_t>(licw + 7);
+    c->M = rd<uint16_t>(licw + 9);
+    c->L = rd<uint16_t>(licw + 11);
+    if (c->kind > 1 || c->act != 0) return bail(LIC_EINVAL);      // 1DN: NEXT-1
+    if (c->N % 64 || c->M % 64 || c->N < 64 || c->N > 256 || c->M < 64 || c->M > 512 || c->L < 1 || c->L > 127)
+        return bail(LIC_EINVAL);
+    // ---- parse blocks
+    std::map<std::string, std::vector<float>> blk;
+    size_t off = 13;
+    for (const BlockSpec& b : licw_blocks(c->N, c->M)) {
+        if (b.hyper_only && c->kind != 1) continue;
+        size_t cnt = 1;
+        for (int d : b.shape) cnt *= (size_t)d;
+        if (off + 5 > len || licw[off] != b.tag || rd<uint32_t>(licw + off + 1) != cnt) return bail(LIC_EDIGEST);
+        off += 5;
+        if (off + 4 * cnt > len) return bail(LIC_EDIGEST);
+        std::vector<float> v(cnt);
+        std::memcpy(v.data(), licw + off, 4 * cnt);
+        off += 4 * cnt;
+        for (float f : v)
+            if (!std::isfinite(f)) return bail(LIC_EINVAL);
+        if (b.role == R_BETA)
+            for (float f : v) if (!(f > 0.0f)) return bail(LIC_EINVAL);
+        if (b.role == R_GAMMA)
+            for (float f : v) if (!(f >= 0.0f)) return bail(LIC_EINVAL);
+        blk[b.name] = std::move(v);
+    }
+    if (off != len) return bail(LIC_EDIGEST);
+    const std::vector<float>& tab = blk["scale_table"];
+    for (int i = 1; i < 64; ++i) if (!(tab[i] > tab[i - 1]) || !(tab[0] > 0)) return bail(LIC_EINVAL);
+
+    // ---- device
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return bail(LIC_ECUDA);
+    }
+    cudaDeviceProp prop;
+    if (cudaSetDevice(device) != cudaSuccess || cudaGetDeviceProperties(&prop, device) != cudaSuccess ||
+        prop.major != 10) {
+        cudaGetLastError();
+        return bail(LIC_ECUDA);
+    }
+    if (!get_encode_fn()) return bail(LIC_ECUDA);
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(LIC_ECUDA);
+    c->split = precision == LIC_PREC_SPLIT ? 2 : 1;
+    c->max_batch = (int)max_batch;
+    c->H = (int)height; c->W = (int)width;
+    const int P = c->kind == 1 ? 64 : 16;
+    c->Hp = (c->H + P - 1) / P * P; c->Wp = (c->W + P - 1) / P * P;
+    c->top = (c->Hp - c->H) / 2; c->left = (c->Wp - c->W) / 2;
+    const int N = c->N, M = c->M, B = c->max_batch, S = c->split;
+    const int H2 = c->Hp / 2, W2 = c->Wp / 2, Hy = c->Hp / 16, Wy = c->Wp / 16, Hz = c->Hp / 64, Wz = c->Wp / 64;
+
+    // ---- host tables (CDF build)
+    c->h_table = tab;
+    c->h_mu_y = blk["mu_y"];
+    c->h_sigma_y = blk["sigma_y"];
+    const uint32_t rl = 2 * c->L + 2;
+    if (c->kind == 0) {
+        c->cdf_fact.resize((size_t)M * rl);
+        if (lic_cdf_build(c->h_sigma_y.data(), M, c->L, c->cdf_fact.data()) != LIC_OK) return bail(LIC_EINVAL);
+    } else {
+        c->h_mu_z = blk["mu_z"];
+        c->h_sigma_z = blk["sigma_z"];
+        c->cdf_z.resize((size_t)N * rl);
+        c->cdf_gauss.resize((size_t)64 * rl);
+        if (lic_cdf_build(c->h_sigma_z.data(), N, c->L, c->cdf_z.data()) != LIC_OK ||
+            lic_cdf_build(tab.data(), 64, c->L, c->cdf_gauss.data()) != LIC_OK)
+            return bail(LIC_EINVAL);
+    }
+
+    // ---- activation buffers (planes of fp16 NHWC)
+    c->planeI = (size_t)B * H2 * W2 * 128;
+    c->planeA = (size_t)B * H2 * W2 * N;
+    c->planeY = (size_t)B * Hy * Wy * M;
+    c->planeZ = (size_t)B * std::max(1, Hz) * std::max(1, Wz) * N;
+    lic_status st;
+    if ((st = dalloc(c, &c->bufI, c->planeI * S * 2)) || (st = dalloc(c, &c->bufA, c->planeA * S * 2)) ||
+        (st = dalloc(c, &c->bufB, c->planeA * S * 2)) || (st = dalloc(c, &c->bufY, c->planeY * S * 2)) ||
+        (st = dalloc(c, &c->bufZ, c->planeZ * S * 2)) || (st = dalloc(c, &c->table, 64 * 4)) ||
+        (st = dalloc(c, &c->mu_y, (size_t)M * 4)) || (st = dalloc(c, &c->mu_z, (size_t)N * 4)) ||
+        (st = dalloc(c, &c->d_sat, 8)) || (st = dalloc(c, &c->d_frames, (size_t)B * 3 * c->H * c->W * 4)) ||
+        (st = dalloc(c, &c->d_ysym, (size_t)B * M * Hy * Wy)) || (st = dalloc(c, &c->d_yidx, (size_t)B * M * Hy * Wy)) ||
+        (st = dalloc(c, &c->d_zsym, (size_t)B * N * std::max(1, Hz) * std::max(1, Wz))))
+        return bail(st);
+    if ((st = upload(c, c->table, tab.data(), 256)) || (st = upload(c, c->mu_y, c->h_mu_y.data(), (size_t)M * 4)))
+        return bail(st);
+    if (c->kind == 1 && (st = upload(c, c->mu_z, c->h_mu_z.data(), (size_t)N * 4))) return bail(st);
+
+    // ---- layers
+    struct Def { int id; bool deconv; int k, s, p, cin, cout, hin, win, hout, wout; EpKind ep; __half* in; size_t inpl;
+                 __half* out; size_t outpl; };
+    std::vector<Def> defs = {
+        {GA1, false, 5, 2, 2, 3, N, c->Hp, c->Wp, H2, W2, EP_GDN, c->bufI, c->planeI, c->bufA, c->planeA},
+        {GA2, false, 5, 2, 2, N, N, H2, W2, H2 / 2, W2 / 2, EP_GDN, c->bufA, c->planeA, c->bufB, c->planeA},
+        {GA3, false, 5, 2, 2, N, N, H2 / 2, W2 / 2, H2 / 4, W2 / 4, EP_GDN, c->bufB, c->planeA, c->bufA, c->planeA},
+        {GA4, false, 5, 2, 2, N, M, H2 / 4, W2 / 4, Hy, Wy, EP_YQUANT, c->bufA, c->planeA, c->bufY, c->planeY},
+        {GS1, true, 5, 2, 2, M, N, Hy, Wy, Hy * 2, Wy * 2, EP_IGDN, c->bufY, c->planeY, c->bufA, c->planeA},
+        {GS2, true, 5, 2, 2, N, N, Hy * 2, Wy * 2, Hy * 4, Wy * 4, EP_IGDN, c->bufA, c->planeA, c->bufB, c->planeA},
+        {GS3, true, 5, 2, 2, N, N, Hy * 4, Wy * 4, H2, W2, EP_IGDN, c->bufB, c->planeA, c->bufA, c->planeA},
+        {GS4, true, 5, 2, 2, N, 3, H2, W2, c->Hp, c->Wp, EP_FINAL, c->bufA, c->planeA, nullptr, 0},
+    };
+    if (c->kind == 1) {
+        defs.push_back({HA1, false, 3, 1, 1, M, N, Hy, Wy, Hy, Wy, EP_RELU, c->bufY, c->planeY, c->bufA, c->planeA});
+        defs.push_back({HA2, false, 5, 2, 2, N, N, Hy, Wy, Hy / 2, Wy / 2, EP_RELU, c->bufA, c->planeA, c->bufB, c->planeA});
+        defs.push_back({HA3, false, 5, 2, 2, N, N, Hy / 2, Wy / 2, Hz, Wz, EP_ZQUANT, c->bufB, c->planeA, c->bufZ, c->planeZ});
+        defs.push_back({HS1, true, 5, 2, 2, N, N, Hz, Wz, Hz * 2, Wz * 2, EP_RELU, c->bufZ, c->planeZ, c->bufA, c->planeA});
+        defs.push_back({HS2, true, 5, 2, 2, N, N, Hz * 2, Wz * 2, Hy, Wy, EP_RELU, c->bufA, c->planeA, c->bufB, c->planeA});
+        defs.push_back({HS3, false, 3, 1, 1, N, M, Hy, Wy, Hy, Wy, EP_SIGMA, c->bufB, c->planeA, nullptr, 0});
+    }
+    size_t dbg = 0;
+    for (const Def& d : defs) {
+        Layer& Ly = c->layers[d.id];
+        Ly.present = true;
+        Ly.deconv = d.deconv; Ly.k = d.k; Ly.s = d.s; Ly.p = d.p;
+        Ly.Cin = d.cin; Ly.Cout = d.cout;
+        Ly.Cin_eff = d.id == GA1 ? 128 : d.cin;
+        Ly.Hin = d.hin; Ly.Win = d.win; Ly.Hout = d.hout; Ly.Wout = d.wout;
+        Ly.ep = d.ep;
+        Ly.in_buf = d.in; Ly.in_plane = d.inpl; Ly.out_buf = d.out; Ly.out_plane = d.outpl;
+        dbg = std::max(dbg, (size_t)B * d.cout * d.hout * d.wout);
+        dbg = std::max(dbg, (size_t)B * d.cin * d.hin * d.win);
+        // weights: LICW out x in x k x k (fp32, fp16-exact) -> fp16 [tap][co_pad][ci_eff]
+        const std::string wn = std::string(kLayerW[d.id]);
+        const std::vector<float>& w = blk[wn + ".w"];
+        int bn = d.cout <= 256 ? (d.cout + 15) / 16 * 16 : 0;
+        if (!bn) { int nt = (d.cout + 255) / 256; bn = ((d.cout + nt - 1) / nt + 15) / 16 * 16 * nt; }
+        const int cout_pad = bn;
+        const int taps = d.id == GA1 ? 1 : d.k * d.k;
+        std::vector<__half> wp((size_t)taps * cout_pad * Ly.Cin_eff, __float2half(0.0f));
+        for (int co = 0; co < d.cout; ++co)
+            for (int ci = 0; ci < d.cin; ++ci)
+                for (int ky = 0; ky < d.k; ++ky)
+                    for (int kx = 0; kx < d.k; ++kx) {
+                        const float v = w[(((size_t)co * d.cin + ci) * d.k + ky) * d.k + kx];
+                        size_t o;
+                        if (d.id == GA1) o = (size_t)co * 128 + (ky * 5 + kx) * 3 + ci;     // im2col K order
+                        else o = ((size_t)(ky * d.k + kx) * cout_pad + co) * Ly.Cin_eff + ci;
+                        wp[o] = __float2half_rn(v);
+                    }
+        if ((st = dalloc(c, &Ly.w, wp.size() * 2)) || (st = upload(c, Ly.w, wp.data(), wp.size() * 2))) return bail(st);
+        const std::vector<float>& bb = blk[wn + ".b"];
+        if ((st = dalloc(c, &Ly.bias, bb.size() * 4)) || (st = upload(c, Ly.bias, bb.data(), bb.size() * 4)))
+            return bail(st);
+        if (d.ep == EP_GDN || d.ep == EP_IGDN) {
+            const std::vector<float>& be = blk[wn + ".beta"];
+            const std::vector<float>& ga = blk[wn + ".gamma"];
+            std::vector<__half> gh(ga.size());
+            for (size_t i = 0; i < ga.size(); ++i) gh[i] = __float2half_rn(ga[i]);
+            if ((st = dalloc(c, &Ly.beta, be.size() * 4)) || (st = upload(c, Ly.beta, be.data(), be.size() * 4)) ||
+                (st = dalloc(c, &Ly.gamma, gh.size() * 2)) || (st = upload(c, Ly.gamma, gh.data(), gh.size() * 2)))
+                return bail(st);
+        }
+        if ((st = plan_layer(c, Ly))) return bail(st);
+    }
+    c->layers[GA4].prm.mu = c->kind == 0 ? c->mu_y : nullptr;
+    c->layers[GA4].prm.abs_out = c->kind == 1;
+    if (c->kind == 1) c->layers[HA3].prm.mu = c->mu_z;
+    c->layers[GS4].prm.crop_top = c->top;
+    c->layers[GS4].prm.crop_left = c->left;
+    c->layers[GS4].prm.crop_H = c->H;
+    c->layers[GS4].prm.crop_W = c->W;
+    c->dbg_elems = dbg;
+    *out = c;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_shapes(const lic_codec* c, lic_shape* y, lic_shape* z, int* kind) {
+    if (!c) return LIC_EINVAL;
+    if (y) *y = {(uint32_t)c->M, (uint32_t)(c->Hp / 16), (uint32_t)(c->Wp / 16)};
+    if (z) *z = c->kind == 1 ? lic_shape{(uint32_t)c->N, (uint32_t)(c->Hp / 64), (uint32_t)(c->Wp / 64)}
+                             : lic_shape{0, 0, 0};
+    if (kind) *kind = c->kind;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_layer_shapes(const lic_codec* c, int id, lic_shape* in, lic_shape* out) {
+    if (!c || id < 0 || id >= NLAYER || !c->layers[id].present) return LIC_EINVAL;
+    const Layer& L = c->layers[id];
+    if (in) *in = {(uint32_t)L.Cin, (uint32_t)L.Hin, (uint32_t)L.Win};
+    if (out) *out = {(uint32_t)L.Cout, (uint32_t)L.Hout, (uint32_t)L.Wout};
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_cdf(const lic_codec* c, int which, const uint32_t** rows, uint32_t* n_rows,
+                              uint32_t* row_len) {
+    if (!c || !rows || !n_rows || !row_len) return LIC_EINVAL;
+    const std::vector<uint32_t>* t = which == 0 ? &c->cdf_fact : which == 1 ? &c->cdf_z : which == 2 ? &c->cdf_gauss : nullptr;
+    if (!t || t->empty()) return LIC_EINVAL;
+    *row_len = 2 * c->L + 2;
+    *n_rows = (uint32_t)(t->size() / *row_len);
+    *rows = t->data();
+    return LIC_OK;
+}
+
+// ------------------------------------------------------------------ pool
+extern "C" lic_status lic_buf_acquire(lic_codec* c, size_t bytes, void** host_ptr) {
+    if (!c || !host_ptr || bytes == 0) return LIC_EINVAL;
+    std::lock_guard<std::mutex> g(c->pool_mu);
+    auto& fl = c->free_lists[bytes];
+    if (!fl.empty()) {
+        *host_ptr = fl.back();
+        fl.pop_back();
+        ++c->pool_reuses;
+        return LIC_OK;
+    }
+    void* p = nullptr;
+    cudaSetDevice(c->device);
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, LIC_ENOMEM, "cudaHostAlloc(%zu)", bytes);
+    }
+    c->owned[p] = bytes;
+    ++c->pool_allocs;
+    *host_ptr = p;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_buf_release(lic_codec* c, void* host_ptr) {
+    if (!c || !host_ptr) return LIC_EINVAL;
+    std::lock_guard<std::mutex> g(c->pool_mu);
+    auto it = c->owned.find(host_ptr);
+    if (it == c->owned.end()) return LIC_EFOREIGN;
+    c->free_lists[it->second].push_back(host_ptr);
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_buf_stats(const lic_codec* c, uint64_t* allocations, uint64_t* reuses) {
+    if (!c) return LIC_EINVAL;
+    std::lock_guard<std::mutex> g(const_cast<lic_codec*>(c)->pool_mu);
+    if (allocations) *allocations = c->pool_allocs;
+    if (reuses) *reuses = c->pool_reuses;
+    return LIC_OK;
+}
+
+// ------------------------------------------------------------------ encode / decode
+struct OutBuf { void* dev; void* user; size_t bytes; };
+
+static OutBuf route_out(void* user, void* staging, size_t bytes) {
+    void* d = device_alias(user);
+    return d ? OutBuf{d, nullptr, bytes} : OutBuf{staging, user, bytes};
+}
+
+static lic_status finish_out(lic_codec* c, const OutBuf& o, cudaStream_t st) {
+    if (o.user) CK(cudaMemcpyAsync(o.user, o.dev, o.bytes, cudaMemcpyDeviceToHost, st));
+    return LIC_OK;
+}
+
+static lic_status check_codec(lic_codec* c, uint32_t batch) {
+    if (!c) return LIC_EINVAL;
+    if (c->sticky) return LIC_ECUDA;
+    if (batch == 0 || (int)batch > c->max_batch) return fail(c, LIC_ESHAPE, "batch %u > max_batch %d", batch, c->max_batch);
+    if (cudaSetDevice(c->device) != cudaSuccess) return fail(c, LIC_ECUDA, "cudaSetDevice");
+    return LIC_OK;
+}
+
+// h_s chain: z-hat (bufZ) -> y indexes (hyper decoder GPU1 and the tail of encode)
+static lic_status run_hs(lic_codec* c, int B, uint8_t* idx_dev, float* dbg_sigma, cudaStream_t st) {
+    lic_status r;
+    if ((r = run_layer(c, c->layers[HS1], c->layers[HS1].prm, B, st))) return r;
+    if ((r = run_layer(c, c->layers[HS2], c->layers[HS2].prm, B, st))) return r;
+    ConvParams p = c->layers[HS3].prm;
+    p.out_sym = idx_dev;
+    p.out_f32 = dbg_sigma;
+    return run_layer(c, c->layers[HS3], p, B, st);
+}
+
+static lic_status encode_impl(lic_codec* c, const void* frames, int hwc, uint32_t batch, int8_t* y_sym,
+                              uint8_t* y_idx, int8_t* z_sym, uint64_t* n_sat, void* stream) {
+    lic_status r = check_codec(c, batch);
+    if (r) return r;
+    if (!frames || !y_sym) return fail(c, LIC_EINVAL, "null frames / y_sym");
+    const bool hyper = c->kind == 1;
+    if (hyper != (y_idx != nullptr) || hyper != (z_sym != nullptr))
+        return fail(c, LIC_EINVAL, "y_idx / z_sym must be given iff the codec is a hyperprior");
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    const int B = (int)batch;
+    const size_t fbytes = (size_t)B * 3 * c->H * c->W * (hwc ? 1 : 4);
+    const void* fdev = device_alias(frames);
+    if (!fdev) {
+        CK(cudaMemcpyAsync(c->d_frames, frames, fbytes, cudaMemcpyHostToDevice, st));
+        fdev = c->d_frames;
+    }
+    const size_t ny = (size_t)B * c->M * (c->Hp / 16) * (c->Wp / 16);
+    const size_t nz = hyper ? (size_t)B * c->N * (c->Hp / 64) * (c->Wp / 64) : 0;
+    OutBuf oy = route_out(y_sym, c->d_ysym, ny);
+    OutBuf oi = hyper ? route_out(y_idx, c->d_yidx, ny) : OutBuf{nullptr, nullptr, 0};
+    OutBuf oz = hyper ? route_out(z_sym, c->d_zsym, nz) : OutBuf{nullptr, nullptr, 0};
+    CK(cudaMemsetAsync(c->d_sat, 0, 8, st));
+    CK(launch_ingest(fdev, hwc, B, c->H, c->W, c->top, c->left, c->Hp / 2, c->Wp / 2, c->bufI, c->planeI,
+                     c->split, st));
+    for (int id : {GA1, GA2, GA3})
+        if ((r = run_layer(c, c->layers[id], c->layers[id].prm, B, st))) return r;
+    {
+        ConvParams p = c->layers[GA4].prm;
+        p.out_sym = oy.dev;
+        p.sat_count = c->d_sat;
+        p.out_f32 = c->debug ? c->dbg_y : nullptr;
+        if ((r = run_layer(c, c->layers[GA4], p, B, st))) return r;
+    }
+    if (hyper) {
+        if ((r = run_layer(c, c->layers[HA1], c->layers[HA1].prm, B, st))) return r;
+        if ((r = run_layer(c, c->layers[HA2], c->layers[HA2].prm, B, st))) return r;
+        ConvParams p = c->layers[HA3].prm;
+        p.out_sym = oz.dev;
+        p.sat_count = c->d_sat;
+        p.out_f32 = c->debug ? c->dbg_z : nullptr;
+        if ((r = run_layer(c, c->layers[HA3], p, B, st))) return r;
+        if ((r = run_hs(c, B, (uint8_t*)oi.dev, c->debug ? c->dbg_s : nullptr, st))) return r;
+    }
+    if ((r = finish_out(c, oy, st))) return r;
+    if (hyper && ((r = finish_out(c, oi, st)) || (r = finish_out(c, oz, st)))) return r;
+    if (n_sat) CK(cudaMemcpyAsync(n_sat, c->d_sat, 8, cudaMemcpyDeviceToHost, st));
+    if (!stream) CK(cudaStreamSynchronize(st));
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_encode(lic_codec* c, const float* frames, uint32_t batch, int8_t* y_sym, uint8_t* y_idx,
+                                 int8_t* z_sym, uint64_t* n_sat, void* stream) {
+    return encode_impl(c, frames, 0, batch, y_sym, y_idx, z_sym, n_sat, stream);
+}
+extern "C" lic_status lic_encode_u8(lic_codec* c, const uint8_t* frames, uint32_t batch, int8_t* y_sym,
+                                    uint8_t* y_idx, int8_t* z_sym, uint64_t* n_sat, void* stream) {
+    return encode_impl(c, frames, 1, batch, y_sym, y_idx, z_sym, n_sat, stream);
+}
+
+extern "C" lic_status lic_hyper_indexes(lic_codec* c, const int8_t* z_sym, uint32_t batch, uint8_t* y_idx,
+                                        void* stream) {
+    lic_status r = check_codec(c, batch);
+    if (r) return r;
+    if (c->kind != 1) return fail(c, LIC_EINVAL, "not a hyperprior codec");
+    if (!z_sym || !y_idx) return fail(c, LIC_EINVAL, "null argument");
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    const int B = (int)batch;
+    const int Hz = c->Hp / 64, Wz = c->Wp / 64;
+    const size_t nz = (size_t)B * c->N * Hz * Wz, ny = (size_t)B * c->M * (c->Hp / 16) * (c->Wp / 16);
+    const int8_t* zd = (const int8_t*)device_alias(z_sym);
+    if (!zd) {
+        CK(cudaMemcpyAsync(c->d_zsym, z_sym, nz, cudaMemcpyHostToDevice, st));
+        zd = c->d_zsym;
+    }
+    OutBuf oi = route_out(y_idx, c->d_yidx, ny);
+    CK(launch_sym_ingest(zd, c->mu_z, B, c->N, Hz, Wz, c->bufZ, c->planeZ, c->split, st));
+    if ((r = run_hs(c, B, (uint8_t*)oi.dev, nullptr, st))) return r;
+    if ((r = finish_out(c, oi, st))) return r;
+    if (!stream) CK(cudaStreamSynchronize(st));
+    return LIC_OK;
+}
+
+static lic_status decode_impl(lic_codec* c, const int8_t* y_sym, uint32_t batch, void* frames, int u8, void* stream) {
+    lic_status r = check_codec(c, batch);
+    if (r) return r;
+    if (!y_sym || !frames) return fail(c, LIC_EINVAL, "null argument");
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    const int B = (int)batch;
+    const int Hy = c->Hp / 16, Wy = c->Wp / 16;
+    const size_t ny = (size_t)B * c->M * Hy * Wy;
+    const int8_t* yd = (const int8_t*)device_alias(y_sym);
+    if (!yd) {
+        CK(cudaMemcpyAsync(c->d_ysym, y_sym, ny, cudaMemcpyHostToDevice, st));
+        yd = c->d_ysym;
+    }
+    const size_t fbytes = (size_t)B * 3 * c->H * c->W * (u8 ? 1 : 4);
+    OutBuf of = route_out(frames, c->d_frames, fbytes);
+    CK(launch_sym_ingest(yd, c->kind == 0 ? c->mu_y : nullptr, B, c->M, Hy, Wy, c->bufY, c->planeY, c->split, st));
+    for (int id : {GS1, GS2, GS3})
+        if ((r = run_layer(c, c->layers[id], c->layers[id].prm, B, st))) return r;
+    ConvParams p = c->layers[GS4].prm;
+    p.out_f32 = u8 ? nullptr : (float*)of.dev;
+    p.out_u8 = u8 ? (uint8_t*)of.dev : nullptr;
+    if ((r = run_layer(c, c->layers[GS4], p, B, st))) return r;
+    if ((r = finish_out(c, of, st))) return r;
+    if (!stream) CK(cudaStreamSynchronize(st));
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_decode(lic_codec* c, const int8_t* y_sym, uint32_t batch, float* frames, void* stream) {
+    return decode_impl(c, y_sym, batch, frames, 0, stream);
+}
+extern "C" lic_status lic_decode_u8(lic_codec* c, const int8_t* y_sym, uint32_t batch, uint8_t* frames,
+                                    void* stream) {
+    return decode_impl(c, y_sym, batch, frames, 1, stream);
+}
+
+// ------------------------------------------------------------------ test exports
+static lic_status ensure_dbg(lic_codec* c) {
+    if (c->d_dbg) return LIC_OK;
+    lic_status r;
+    const size_t ny = (size_t)c->max_batch * c->M * (c->Hp / 16) * (c->Wp / 16);
+    const size_t nz = (size_t)c->max_batch * c->N * std::max(1, c->Hp / 64) * std::max(1, c->Wp / 64);
+    if ((r = dalloc(c, &c->d_dbg, c->dbg_elems * 4)) || (r = dalloc(c, &c->dbg_y, ny * 4)) ||
+        (r = dalloc(c, &c->dbg_z, nz * 4)) || (r = dalloc(c, &c->dbg_s, ny * 4)))
+        return r;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_set_debug(lic_codec* c, int on) {
+    if (!c) return LIC_EINVAL;
+    lic_status r = ensure_dbg(c);
+    if (r) return r;
+    c->debug = on;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_debug_latents(lic_codec* c, uint32_t batch, float* y, float* z, float* sigma) {
+    lic_status r = check_codec(c, batch);
+    if (r) return r;
+    if (!c->debug) return fail(c, LIC_EINVAL, "debug not enabled");
+    const size_t ny = (size_t)batch * c->M * (c->Hp / 16) * (c->Wp / 16);
+    const size_t nz = (size_t)batch * c->N * (c->Hp / 64) * (c->Wp / 64);
+    CK(cudaStreamSynchronize(c->stream));
+    if (y) CK(cudaMemcpy(y, c->dbg_y, ny * 4, cudaMemcpyDefault));
+    if (c->kind == 1) {
+        if (z) CK(cudaMemcpy(z, c->dbg_z, nz * 4, cudaMemcpyDefault));
+        if (sigma) CK(cudaMemcpy(sigma, c->dbg_s, ny * 4, cudaMemcpyDefault));
+    }
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_test_layer(lic_codec* c, int id, const float* in, uint32_t batch, float* out,
+                                     void* stream) {
+    lic_status r = check_codec(c, batch);
+    if (r) return r;
+    if (id < 0 || id >= NLAYER || !c->layers[id].present || !in || !out) return fail(c, LIC_EINVAL, "bad layer");
+    if ((r = ensure_dbg(c))) return r;
+    cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
+    Layer& Ly = c->layers[id];
+    const int B = (int)batch;
+    const size_t nin = (size_t)B * Ly.Cin * Ly.Hin * Ly.Win;
+    const size_t nout = (size_t)B * Ly.Cout * Ly.Hout * Ly.Wout;
+    const float* ind = (const float*)device_alias(in);
+    if (!ind) {
+        CK(cudaMemcpyAsync(c->d_dbg, in, nin * 4, cudaMemcpyHostToDevice, st));
+        ind = c->d_dbg;
+    }
+    if (id == GA1)
+        CK(launch_ingest(ind, 0, B, Ly.Hin, Ly.Win, 0, 0, Ly.Hout, Ly.Wout, c->bufI, c->planeI, c->split, st));
+    else
+        CK(launch_pack_chw(ind, B, Ly.Cin, Ly.Hin, Ly.Win, Ly.in_buf, Ly.in_plane, c->split, st));
+    ConvParams p = Ly.prm;
+    OutBuf o = route_out(out, c->d_dbg, nout * 4);
+    p.out_f32 = (float*)o.dev;
+    p.sat_count = nullptr;
+    if (Ly.ep == EP_YQUANT || Ly.ep == EP_ZQUANT) p.out_sym = c->d_ysym;   // symbols discarded
+    if (Ly.ep == EP_ZQUANT) p.out_sym = c->d_zsym;
+    if (Ly.ep == EP_SIGMA) p.out_sym = c->d_yidx;
+    if (Ly.ep == EP_FINAL) { p.crop_top = 0; p.crop_left = 0; p.crop_H = Ly.Hout; p.crop_W = Ly.Wout; p.out_u8 = nullptr; }
+    if ((r = run_layer(c, Ly, p, B, st))) return r;
+    if ((r = finish_out(c, o, st))) return r;
+    if (!stream) CK(cudaStreamSynchronize(st));
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_test_sigma_to_index(lic_codec* c, const float* sigma, size_t n, uint8_t* idx) {
+    if (!c || !sigma || !idx) return LIC_EINVAL;
+    if (c->sticky) return LIC_ECUDA;
+    float* ds = nullptr;
+    uint8_t* di = nullptr;
+    CK(cudaMalloc(&ds, n * 4 + 16));
+    CK(cudaMalloc(&di, n + 16));
+    CK(cudaMemcpy(ds, sigma, n * 4, cudaMemcpyDefault));
+    CK(launch_sigma_index(ds, n, c->table, di, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(idx, di, n, cudaMemcpyDefault));
+    cudaFree(ds);
+    cudaFree(di);
+    return LIC_OK;
+}

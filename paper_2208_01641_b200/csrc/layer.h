@@ -1,0 +1,66 @@
+// layer.h -- host/device description of one implicit-GEMM layer launch.
+//
+// Every transform layer of the codec (Fig. 1: g_a, g_s, h_a, h_s; layer shapes
+// SPEC.md:319) runs through ONE persistent tcgen05 kernel (conv_umma.cu).  A layer is
+//   D[pixel, co] = sum_{tap, ci} A[pixel shifted by tap, ci] * W[tap][co][ci]
+// over a GEMM grid of output pixels (conv) or of input pixels per sub-pixel phase
+// (stride-2 transposed conv, 4 phases with 9/6/6/4 taps), followed by a fused epilogue
+// (GDN / IGDN / ReLU / quantise / sigma->index / clamp+crop).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace lic {
+
+enum EpKind : int {
+    EP_F32 = 0,     // acc + bias -> f32 CHW (test export)
+    EP_GDN = 1,     // GDN  (x / sqrt(beta + gamma x^2))  -> fp16 hi/lo NHWC
+    EP_IGDN = 2,    // IGDN (x * sqrt(beta + gamma x^2))  -> fp16 hi/lo NHWC
+    EP_RELU = 3,    // max(x, 0)                          -> fp16 hi/lo NHWC
+    EP_YQUANT = 4,  // s = clamp(round(y - mu)) -> int8 CHW; optional |y| -> hi/lo NHWC
+    EP_ZQUANT = 5,  // s = clamp(round(z - mu)) -> int8 CHW; z-hat = s + mu -> hi/lo NHWC
+    EP_SIGMA = 6,   // sigma = relu(x); idx = #{table_j < max(sigma, 0.11f)} -> uint8 CHW
+    EP_FINAL = 7,   // clamp(x, 0, 1), crop -> f32 CHW and/or u8 HWC
+};
+
+constexpr int kMaxTaps = 32;
+constexpr int kBM = 128;        // pixels per tile (UMMA M)
+constexpr int kBK = 64;         // channels per K chunk (one 128-byte swizzle row of fp16)
+
+struct ConvParams {
+    // ---- GEMM geometry
+    int batch;
+    int Cin, kchunks;                 // Cin multiple of 64
+    int Cout, BN, n_ntiles;           // real output channels, N tile, #N tiles
+    int Hg, Wg;                       // GEMM grid (conv: output; deconv: input grid, per phase)
+    int Wt, Ht, tiles_x, tiles_y;     // tile = Ht x Wt pixels, Wt * Ht = 128
+    int nphase;                       // 1 conv, 4 deconv
+    int stride;                       // A coordinate = stride * g + tap offset
+    int out_s;                        // output pixel = out_s * g + phase offset
+    int ntaps[4], tap0[4];
+    int tap_dy[kMaxTaps], tap_dx[kMaxTaps], tap_w[kMaxTaps];
+    int split;                        // 2: activations are fp16 hi + lo planes; 1: hi only
+    int total_tiles;
+    // ---- kernel resources (host-computed)
+    int stages;
+    uint32_t stage_bytes, off_gamma, off_xsq, off_bar, smem_bytes;
+    int tmem_cols, acc_stride, n_accbuf;
+    // ---- epilogue
+    int ep;
+    int Hout, Wout;                   // output tensor spatial size (padded coordinates)
+    const float* bias;                // [Cout]
+    const float* beta;                // [Cout] (GDN/IGDN)
+    const float* mu;                  // [Cout] quantisation offsets, nullable (= 0)
+    const float* table;               // [64] scale table (EP_SIGMA)
+    int L;                            // symbol support bound
+    void* out_act;                    // fp16 [split][batch][Hout][Wout][Cout]
+    size_t act_plane;                 // elements per plane of out_act
+    void* out_sym;                    // int8 / uint8 [batch][Cout][Hout][Wout]
+    float* out_f32;                   // f32 [batch][Cout][Hout or crop_H][Wout or crop_W]
+    uint8_t* out_u8;                  // u8 [batch][crop_H][crop_W][3]
+    int abs_out;                      // EP_YQUANT: also write |y| planes
+    int crop_top, crop_left, crop_H, crop_W;
+    unsigned long long* sat_count;    // saturation counter (nullable)
+};
+
+}  // namespace lic

@@ -1,0 +1,263 @@
+"""Thin ctypes binding of ``include/lic.h`` (argument marshalling only).
+
+Every step of the codec runs in ``liblic.so`` (sm_100a kernels + the native host coder);
+there is no Python or CPU fallback: if the library is missing this module raises on
+import.  Arrays may be numpy arrays (host memory) or torch tensors (device or pinned
+host memory); they are passed to the C ABI as raw pointers.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblic.so")
+
+LIC_OK, LIC_EINVAL, LIC_ESHAPE, LIC_ECORRUPT, LIC_EDIGEST, LIC_ENOMEM, LIC_ECUDA, LIC_EFOREIGN, \
+    LIC_ENOSPACE = range(9)
+PREC_SPLIT, PREC_F16 = 0, 1
+LAYERS = ["ga1", "ga2", "ga3", "ga4", "gs1", "gs2", "gs3", "gs4", "ha1", "ha2", "ha3", "hs1", "hs2", "hs3"]
+
+
+class LicError(RuntimeError):
+    def __init__(self, status, msg=""):
+        super().__init__(f"lic status {status}: {msg}")
+        self.status = status
+
+
+class CorruptStream(LicError):
+    pass
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("c", ctypes.c_uint32), ("h", ctypes.c_uint32), ("w", ctypes.c_uint32)]
+
+    def tuple(self):
+        return (self.c, self.h, self.w)
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_2208_01641_b200.build` "
+                      "(there is no fallback path)")
+_L = ctypes.CDLL(LIB_PATH)
+_P = ctypes.c_void_p
+_u32, _sz, _i = ctypes.c_uint32, ctypes.c_size_t, ctypes.c_int
+_L.lic_open.argtypes = [_P, _sz, _i, _u32, _u32, _u32, _i, ctypes.POINTER(_P)]
+_L.lic_close.argtypes = [_P]
+_L.lic_close.restype = None
+_L.lic_shapes.argtypes = [_P, ctypes.POINTER(Shape), ctypes.POINTER(Shape), ctypes.POINTER(_i)]
+_L.lic_last_error.argtypes = [_P]
+_L.lic_last_error.restype = ctypes.c_char_p
+_L.lic_buf_acquire.argtypes = [_P, _sz, ctypes.POINTER(_P)]
+_L.lic_buf_release.argtypes = [_P, _P]
+_L.lic_buf_stats.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+_L.lic_encode.argtypes = [_P, _P, _u32, _P, _P, _P, _P, _P]
+_L.lic_encode_u8.argtypes = [_P, _P, _u32, _P, _P, _P, _P, _P]
+_L.lic_hyper_indexes.argtypes = [_P, _P, _u32, _P, _P]
+_L.lic_decode.argtypes = [_P, _P, _u32, _P, _P]
+_L.lic_decode_u8.argtypes = [_P, _P, _u32, _P, _P]
+_L.lic_test_layer.argtypes = [_P, _i, _P, _u32, _P, _P]
+_L.lic_layer_shapes.argtypes = [_P, _i, ctypes.POINTER(Shape), ctypes.POINTER(Shape)]
+_L.lic_test_sigma_to_index.argtypes = [_P, _P, _sz, _P]
+_L.lic_set_debug.argtypes = [_P, _i]
+_L.lic_debug_latents.argtypes = [_P, _u32, _P, _P, _P]
+_L.lic_cdf.argtypes = [_P, _i, ctypes.POINTER(ctypes.POINTER(ctypes.c_uint32)), ctypes.POINTER(_u32),
+                       ctypes.POINTER(_u32)]
+_L.lic_cdf_build.argtypes = [_P, _u32, _u32, _P]
+_L.lic_rans_encode.argtypes = [_P, _P, Shape, _P, _u32, _u32, _i, _P, _sz, ctypes.POINTER(_sz)]
+_L.lic_rans_decode.argtypes = [_P, _sz, _P, Shape, _P, _u32, _u32, _i, _P]
+_L.lic_version.restype = ctypes.c_char_p
+
+EXPORTED = [n for n in dir(_L) if n.startswith("lic_")]
+
+
+def lib():
+    return _L
+
+
+def _ptr(a):
+    """Raw address of a numpy array / torch tensor / int / None."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    raise TypeError(type(a))
+
+
+def _stream(s):
+    if s is None:
+        return None
+    return s.cuda_stream if hasattr(s, "cuda_stream") else int(s)
+
+
+def version():
+    return _L.lic_version().decode()
+
+
+# ---------------------------------------------------------------- host coder
+def cdf_build(sigmas, L):
+    s = np.ascontiguousarray(sigmas, np.float32)
+    out = np.empty((s.size, 2 * L + 2), np.uint32)
+    st = _L.lic_cdf_build(_ptr(s), s.size, L, _ptr(out))
+    if st:
+        raise LicError(st, "cdf_build")
+    return out
+
+
+def rans_encode(sym, cdf, rows=None, sym_min=None):
+    """sym: int8 [C,H,W] (rows None -> row = channel) or any shape with uint8 rows."""
+    sym = np.ascontiguousarray(sym, np.int8)
+    cdf = np.ascontiguousarray(cdf, np.uint32)
+    if sym.ndim == 3:
+        shp = Shape(*sym.shape)
+    else:
+        shp = Shape(1, 1, sym.size)
+    if rows is not None:
+        rows = np.ascontiguousarray(rows, np.uint8)
+        assert rows.size == sym.size
+    if sym_min is None:
+        sym_min = -((cdf.shape[1] - 2) // 2)
+    cap = 2 * sym.size + 64
+    out = np.empty(cap, np.uint8)
+    n = ctypes.c_size_t(0)
+    st = _L.lic_rans_encode(_ptr(sym), _ptr(rows), shp, _ptr(cdf), cdf.shape[0], cdf.shape[1], int(sym_min),
+                            _ptr(out), cap, ctypes.byref(n))
+    if st:
+        raise LicError(st, "rans_encode")
+    return out[: n.value].tobytes()
+
+
+def rans_decode(data, shape, cdf, rows=None, sym_min=None, out=None):
+    cdf = np.ascontiguousarray(cdf, np.uint32)
+    shp = Shape(*shape) if len(shape) == 3 else Shape(1, 1, int(np.prod(shape)))
+    if rows is not None:
+        rows = np.ascontiguousarray(rows, np.uint8)
+    if sym_min is None:
+        sym_min = -((cdf.shape[1] - 2) // 2)
+    if out is None:
+        out = np.empty(shape, np.int8)
+    buf = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)
+    st = _L.lic_rans_decode(_ptr(buf), len(data), _ptr(rows), shp, _ptr(cdf), cdf.shape[0], cdf.shape[1],
+                            int(sym_min), _ptr(out))
+    if st == LIC_ECORRUPT:
+        raise CorruptStream(st, "corrupt stream")
+    if st:
+        raise LicError(st, "rans_decode")
+    return out
+
+
+# ---------------------------------------------------------------- codec
+class Codec:
+    """One lic_codec: (weights, geometry, device, max_batch)."""
+
+    def __init__(self, licw: bytes, height: int, width: int, max_batch: int = 1, device: int = 0,
+                 precision: int = PREC_SPLIT):
+        self._h = _P()
+        buf = (ctypes.c_uint8 * len(licw)).from_buffer_copy(licw)
+        st = _L.lic_open(buf, len(licw), device, height, width, max_batch, precision, ctypes.byref(self._h))
+        if st:
+            raise LicError(st, "lic_open")
+        self.height, self.width, self.max_batch = height, width, max_batch
+        y, z, k = Shape(), Shape(), _i()
+        _L.lic_shapes(self._h, ctypes.byref(y), ctypes.byref(z), ctypes.byref(k))
+        self.y_shape, self.z_shape, self.hyper = y.tuple(), z.tuple(), bool(k.value)
+
+    def close(self):
+        if self._h:
+            _L.lic_close(self._h)
+            self._h = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st, what):
+        if st:
+            msg = _L.lic_last_error(self._h)
+            raise LicError(st, f"{what}: {msg.decode() if msg else ''}")
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- tables
+    def cdf(self, which):
+        rows = ctypes.POINTER(ctypes.c_uint32)()
+        n, rl = _u32(), _u32()
+        self._chk(_L.lic_cdf(self._h, which, ctypes.byref(rows), ctypes.byref(n), ctypes.byref(rl)), "lic_cdf")
+        return np.ctypeslib.as_array(rows, shape=(n.value, rl.value)).copy()
+
+    # -- GPU entry points (arrays are caller-owned; numpy or torch)
+    def encode(self, frames, y_sym, y_idx=None, z_sym=None, stream=None, u8=False):
+        n = ctypes.c_uint64(0)
+        fn = _L.lic_encode_u8 if u8 else _L.lic_encode
+        batch = frames.shape[0]
+        self._chk(fn(self._h, _ptr(frames), batch, _ptr(y_sym), _ptr(y_idx), _ptr(z_sym),
+                     ctypes.addressof(n) if stream is None else None, _stream(stream)), "lic_encode")
+        return n.value
+
+    def hyper_indexes(self, z_sym, y_idx, stream=None):
+        self._chk(_L.lic_hyper_indexes(self._h, _ptr(z_sym), z_sym.shape[0], _ptr(y_idx), _stream(stream)),
+                  "lic_hyper_indexes")
+
+    def decode(self, y_sym, frames, stream=None, u8=False):
+        fn = _L.lic_decode_u8 if u8 else _L.lic_decode
+        self._chk(fn(self._h, _ptr(y_sym), y_sym.shape[0], _ptr(frames), _stream(stream)), "lic_decode")
+
+    # -- pool
+    def buf_acquire(self, nbytes):
+        p = _P()
+        self._chk(_L.lic_buf_acquire(self._h, nbytes, ctypes.byref(p)), "lic_buf_acquire")
+        return p.value
+
+    def buf_release(self, ptr):
+        return _L.lic_buf_release(self._h, ptr)
+
+    def buf_stats(self):
+        a, r = ctypes.c_uint64(), ctypes.c_uint64()
+        _L.lic_buf_stats(self._h, ctypes.byref(a), ctypes.byref(r))
+        return a.value, r.value
+
+    # -- test exports
+    def layer_shapes(self, layer):
+        lid = LAYERS.index(layer) if isinstance(layer, str) else layer
+        i, o = Shape(), Shape()
+        self._chk(_L.lic_layer_shapes(self._h, lid, ctypes.byref(i), ctypes.byref(o)), "lic_layer_shapes")
+        return i.tuple(), o.tuple()
+
+    def test_layer(self, layer, x):
+        """x: f32 [B, Cin, Hin, Win] numpy -> f32 [B, Cout, Hout, Wout]."""
+        lid = LAYERS.index(layer) if isinstance(layer, str) else layer
+        _, o = self.layer_shapes(lid)
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty((x.shape[0],) + o, np.float32)
+        self._chk(_L.lic_test_layer(self._h, lid, _ptr(x), x.shape[0], _ptr(out), None), "lic_test_layer")
+        return out
+
+    def test_sigma_to_index(self, sigma):
+        s = np.ascontiguousarray(sigma, np.float32)
+        idx = np.empty(s.shape, np.uint8)
+        self._chk(_L.lic_test_sigma_to_index(self._h, _ptr(s), s.size, _ptr(idx)), "lic_test_sigma_to_index")
+        return idx
+
+    def set_debug(self, on=True):
+        self._chk(_L.lic_set_debug(self._h, int(on)), "lic_set_debug")
+
+    def debug_latents(self, batch):
+        y = np.empty((batch,) + self.y_shape, np.float32)
+        z = np.empty((batch,) + self.z_shape, np.float32) if self.hyper else None
+        s = np.empty((batch,) + self.y_shape, np.float32) if self.hyper else None
+        self._chk(_L.lic_debug_latents(self._h, batch, _ptr(y), _ptr(z), _ptr(s)), "lic_debug_latents")
+        return y, z, s

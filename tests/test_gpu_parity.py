@@ -1,0 +1,204 @@
+"""CUDA path vs the oracle, through the C ABI (-m gpu).
+
+Stage-wise on identical inputs: every layer is fed the oracle's
+input for that layer; decode is fed the oracle's symbols; hyper_indexes the oracle's z
+symbols.  Sizes span several tiles with ragged tails (240 x 300 pads to 256 x 320:
+y grid 16 x 20, z grid 4 x 5) plus the factorized 64 x 64 configs[0] case.
+"""
+import numpy as np
+import pytest
+
+from lic_synth import ModelSpec, generate_weights, synth_frames_u8, u8_to_f32_chw, write_licw
+from oracle import oracle as O
+
+from parity import check_float, check_indexes, check_symbols
+
+pytestmark = pytest.mark.gpu
+
+H, W = 240, 300
+HYPER = ModelSpec(kind=1, N=128, M=192)
+
+
+@pytest.fixture(scope="module")
+def lic():
+    from paper_2208_01641_b200 import lic as L
+    return L
+
+
+@pytest.fixture(scope="module")
+def hyper():
+    w = generate_weights(HYPER, seed=0)
+    blob = write_licw(HYPER, w)
+    fr = synth_frames_u8(2, H, W, seed=11)
+    x = u8_to_f32_chw(fr)                       # f32 input frames (data)
+    # oracle chain on frame 0 and 1 (padded, f32 as given)
+    ref = []
+    for b in range(2):
+        xp, crop = O.pad_chw(x[b], hyper=True)
+        acts = {"x": xp}
+        h = xp
+        for i in (1, 2, 3):
+            h = O.gdn(O.conv2d(h, w[f"ga{i}.w"], w[f"ga{i}.b"], 2, 2), w[f"ga{i}.beta"], w[f"ga{i}.gamma"])
+            acts[f"ga{i}"] = h
+        y = O.conv2d(h, w["ga4.w"], w["ga4.b"], 2, 2)
+        acts["ga4"] = y
+        a = O.relu(O.conv2d(np.abs(y), w["ha1.w"], w["ha1.b"], 1, 1)); acts["ha1"] = a
+        a = O.relu(O.conv2d(a, w["ha2.w"], w["ha2.b"], 2, 2)); acts["ha2"] = a
+        z = O.conv2d(a, w["ha3.w"], w["ha3.b"], 2, 2); acts["ha3"] = z
+        zs, zhat, _ = O.quantize(z, w["mu_z"], 32)
+        acts["zhat"], acts["z_sym"] = zhat, zs
+        s = O.relu(O.deconv2d(zhat, w["hs1.w"], w["hs1.b"], 2, 2, 1)); acts["hs1"] = s
+        s = O.relu(O.deconv2d(s, w["hs2.w"], w["hs2.b"], 2, 2, 1)); acts["hs2"] = s
+        sig = O.relu(O.conv2d(s, w["hs3.w"], w["hs3.b"], 1, 1)); acts["hs3"] = sig
+        acts["y_idx"] = O.scale_index(sig, w["scale_table"])
+        ys, yhat, _ = O.quantize(y, None, 32)
+        acts["y_sym"], acts["yhat"] = ys, yhat
+        g = yhat
+        for i in (1, 2, 3):
+            g = O.gdn(O.deconv2d(g, w[f"gs{i}.w"], w[f"gs{i}.b"], 2, 2, 1), w[f"gs{i}.beta"], w[f"gs{i}.gamma"],
+                      inverse=True)
+            acts[f"gs{i}"] = g
+        g = np.clip(O.deconv2d(g, w["gs4.w"], w["gs4.b"], 2, 2, 1), 0, 1)
+        acts["gs4"] = g
+        top, left = crop
+        acts["xhat"] = g[:, top:top + H, left:left + W]
+        ref.append(acts)
+    return dict(w=w, blob=blob, fr=fr, x=x, ref=ref)
+
+
+@pytest.fixture(scope="module")
+def codec(lic, hyper):
+    c = lic.Codec(hyper["blob"], H, W, max_batch=2)
+    yield c
+    c.close()
+
+
+LAYER_IO = {  # layer -> (input key, output key)
+    "ga1": ("x", "ga1"), "ga2": ("ga1", "ga2"), "ga3": ("ga2", "ga3"), "ga4": ("ga3", "ga4"),
+    "ha1": ("absy", "ha1"), "ha2": ("ha1", "ha2"), "ha3": ("ha2", "ha3"),
+    "hs1": ("zhat", "hs1"), "hs2": ("hs1", "hs2"), "hs3": ("hs2", "hs3"),
+    "gs1": ("yhat", "gs1"), "gs2": ("gs1", "gs2"), "gs3": ("gs2", "gs3"), "gs4": ("gs3", "gs4"),
+}
+
+
+@pytest.mark.parametrize("layer", list(LAYER_IO))
+def test_layer_parity(codec, hyper, layer):
+    src, dst = LAYER_IO[layer]
+    def get(b, k):
+        return np.abs(hyper["ref"][b]["ga4"]) if k == "absy" else hyper["ref"][b][k]
+    x = np.stack([get(b, src) for b in range(2)])
+    ref = np.stack([get(b, dst) for b in range(2)])
+    got = codec.test_layer(layer, x)
+    worst = check_float(got, ref, what=layer)
+    print(f"{layer}: max-abs {worst:.2e} (|ref| max {np.abs(ref).max():.2f})")
+
+
+def test_encode_planes(codec, hyper):
+    B = 2
+    ys = np.empty((B,) + codec.y_shape, np.int8)
+    yi = np.empty((B,) + codec.y_shape, np.uint8)
+    zs = np.empty((B,) + codec.z_shape, np.int8)
+    codec.set_debug(True)
+    nsat = codec.encode(hyper["x"], ys, yi, zs)
+    y, z, sig = codec.debug_latents(B)
+    codec.set_debug(False)
+    assert nsat == 0
+    tab = hyper["w"]["scale_table"]
+    for b in range(B):
+        r = hyper["ref"][b]
+        check_float(y[b], r["ga4"], what="y")
+        check_float(z[b], r["ha3"], what="z")
+        nz = check_symbols(zs[b], r["z_sym"], r["ha3"] - hyper["w"]["mu_z"][:, None, None], what="z_sym")
+        ny = check_symbols(ys[b], r["y_sym"], r["ga4"], what="y_sym")
+        if nz == 0:     # identical z-hat -> indexes differ only at table boundaries
+            check_float(sig[b], r["hs3"], what="sigma")
+            check_indexes(yi[b], r["y_idx"], r["hs3"], tab, what="y_idx")
+        print(f"frame {b}: y_sym mismatches {ny}, z_sym {nz}, y_idx {(yi[b] != r['y_idx']).sum()}")
+
+
+def test_encode_u8_matches_f32(codec, hyper):
+    """x = u8/255 on the GPU equals the f32 frames the generator made the same way."""
+    B = 2
+    a = [np.empty((B,) + codec.y_shape, np.int8), np.empty((B,) + codec.y_shape, np.uint8),
+         np.empty((B,) + codec.z_shape, np.int8)]
+    b = [np.empty_like(t) for t in a]
+    codec.encode(hyper["x"], *a)
+    codec.encode(np.ascontiguousarray(hyper["fr"]), *b, u8=True)
+    for t, u in zip(a, b):
+        assert np.array_equal(t, u)
+
+
+def test_hyper_indexes_from_oracle_z(codec, hyper):
+    zs = np.stack([hyper["ref"][b]["z_sym"] for b in range(2)])
+    yi = np.empty((2,) + codec.y_shape, np.uint8)
+    codec.hyper_indexes(zs, yi)
+    for b in range(2):
+        r = hyper["ref"][b]
+        check_indexes(yi[b], r["y_idx"], r["hs3"], hyper["w"]["scale_table"], what="hyper_indexes")
+
+
+def test_decode_from_oracle_symbols(codec, hyper):
+    ys = np.stack([hyper["ref"][b]["y_sym"] for b in range(2)])
+    out = np.empty((2, 3, H, W), np.float32)
+    codec.decode(ys, out)
+    for b in range(2):
+        check_float(out[b], hyper["ref"][b]["xhat"], what="xhat")
+    # u8 output = round_half_away(255 * x-hat)
+    o8 = np.empty((2, H, W, 3), np.uint8)
+    codec.decode(ys, o8, u8=True)
+    ref8 = np.floor(np.moveaxis(hyper["ref"][0]["xhat"], 0, -1).astype(np.float64) * 255 + 0.5)
+    assert np.max(np.abs(o8[0].astype(np.int32) - ref8)) <= 1
+
+
+def test_sigma_to_index_exact(codec, hyper, lic):
+    """c18: the sigma->index function itself is exact on the oracle's sigma."""
+    tab = hyper["w"]["scale_table"]
+    sig = np.concatenate([hyper["ref"][0]["hs3"].ravel(), tab, np.nextafter(tab, 0), np.nextafter(tab, 1e9),
+                          np.array([0, 0.05, 0.11, 1e9], np.float32)]).astype(np.float32)
+    assert np.array_equal(codec.test_sigma_to_index(sig), O.scale_index(sig, tab))
+
+
+def test_bitstreams_bit_exact(codec, hyper, lic):
+    """c19 (ii): GPU planes + product coder == oracle planes + oracle coder, byte for byte."""
+    B = 2
+    ys = np.empty((B,) + codec.y_shape, np.int8)
+    yi = np.empty((B,) + codec.y_shape, np.uint8)
+    zs = np.empty((B,) + codec.z_shape, np.int8)
+    codec.encode(hyper["x"], ys, yi, zs)
+    w = hyper["w"]
+    tabs = O.build_tables(w, True, 32)
+    assert np.array_equal(codec.cdf(1), tabs.z) and np.array_equal(codec.cdf(2), tabs.gauss)
+    for b in range(B):
+        r = hyper["ref"][b]
+        yb_ref, zb_ref = O.code_planes({"y_sym": r["y_sym"], "y_idx": r["y_idx"], "z_sym": r["z_sym"]}, tabs, True)
+        yb = lic.rans_encode(ys[b].ravel(), codec.cdf(2), rows=yi[b].ravel())
+        zb = lic.rans_encode(zs[b], codec.cdf(1))
+        if np.array_equal(ys[b], r["y_sym"]) and np.array_equal(yi[b], r["y_idx"]) and np.array_equal(zs[b], r["z_sym"]):
+            assert yb == yb_ref and zb == zb_ref
+        # every build bitstream decodes losslessly with the oracle decoder (c19 iii)
+        assert np.array_equal(O.rans_decode(yb, yi[b].astype(np.int32), tabs.gauss).reshape(ys[b].shape), ys[b])
+
+
+def test_factorized_c1(lic):
+    """configs[0]: factorized N=128 M=192 on one 64x64 image, full encode + decode."""
+    spec = ModelSpec(kind=0, N=128, M=192)
+    w = generate_weights(spec, seed=0)
+    fr = synth_frames_u8(1, 64, 64, seed=42)
+    x = u8_to_f32_chw(fr)
+    c = lic.Codec(write_licw(spec, w), 64, 64, max_batch=1)
+    ys = np.empty((1,) + c.y_shape, np.int8)
+    c.set_debug(True)
+    c.encode(x, ys)
+    y, _, _ = c.debug_latents(1)
+    xp, crop = O.pad_chw(x[0], hyper=False)
+    p = O.encode_planes(xp, w, False, 32)
+    check_float(y[0], p["y"], what="y")
+    check_symbols(ys[0], p["y_sym"], p["y"] - w["mu_y"][:, None, None], what="y_sym")
+    out = np.empty((1, 3, 64, 64), np.float32)
+    c.decode(p["y_sym"][None], out)
+    check_float(out[0], O.decode_frame(p["y_sym"], w, False, crop, 64, 64), what="xhat")
+    tabs = O.build_tables(w, False, 32)
+    assert np.array_equal(c.cdf(0), tabs.fact_y)
+    if np.array_equal(ys[0], p["y_sym"]):
+        assert lic.rans_encode(ys[0], c.cdf(0)) == O.code_planes(p, tabs, False)[0]
+    c.close()

@@ -1,0 +1,87 @@
+"""Product host coder (liblic.so) vs the oracle, bit-exact (-m "not gpu").
+
+SURVEY.md §8(c) c19 (i): rANS(planes) == oracle rANS(planes) byte-for-byte, always;
+CDF tables identical to the oracle's.
+"""
+import numpy as np
+import pytest
+
+from lic_synth import ModelSpec, generate_weights, scale_table, write_licw, read_licw_blocks
+from oracle import oracle as O
+
+RNG = np.random.default_rng(7)
+
+
+@pytest.fixture(scope="module")
+def lic():
+    from paper_2208_01641_b200 import build
+    build.build()
+    from paper_2208_01641_b200 import lic as L
+    return L
+
+
+def test_cdf_tables_bit_exact(lic):
+    t = scale_table()
+    sig = np.concatenate([t, RNG.uniform(0.05, 300, 200).astype(np.float32),
+                          np.array([0.11, 0.5, 1.0, 1.5], np.float32)])
+    for L in (8, 32):
+        assert np.array_equal(lic.cdf_build(sig, L), O.cdf_table(sig, L))
+
+
+def test_rans_kats(lic):
+    c = np.array([[0, 100, 40000, 65536]], np.uint32)
+    b = lic.rans_encode(np.array([2, 1, 0, 1, 2, 2, 1, 1], np.int8), c, rows=np.zeros(8, np.uint8), sym_min=0)
+    assert b.hex() == "009dc5b89250"
+    c = np.array([[0, 32768, 65536]], np.uint32)
+    assert lic.rans_encode(np.zeros((0,), np.int8), c, rows=np.zeros(0, np.uint8), sym_min=0).hex() == "00800000"
+
+
+@pytest.mark.parametrize("C,H,W,scale", [(192, 12, 20, 1.5), (128, 3, 5, 0.3), (8, 1, 1, 3.0), (320, 17, 30, 6.0)])
+def test_rans_channel_rows_bit_exact(lic, C, H, W, scale):
+    L = 32
+    cdf = O.cdf_table(RNG.uniform(0.5, 1.5, C), L)
+    sym = np.clip(np.round(RNG.standard_normal((C, H, W)) * scale), -L, L).astype(np.int8)
+    ref = O.rans_encode(sym, O.channel_rows(sym.shape), cdf)
+    got = lic.rans_encode(sym, cdf)
+    assert got == ref
+    assert np.array_equal(lic.rans_decode(got, sym.shape, cdf), sym)
+    assert np.array_equal(O.rans_decode(got, O.channel_rows(sym.shape), cdf).reshape(sym.shape), sym)
+
+
+def test_rans_indexed_rows_bit_exact(lic):
+    L = 32
+    cdf = O.cdf_table(scale_table(), L)
+    n = 200_000
+    idx = RNG.integers(0, 64, n).astype(np.uint8)
+    sig = scale_table()[idx]
+    sym = np.clip(np.round(RNG.standard_normal(n) * sig * 0.7), -L, L).astype(np.int8)
+    ref = O.rans_encode(sym, idx.astype(np.int32), cdf)
+    got = lic.rans_encode(sym, cdf, rows=idx)
+    assert got == ref
+    assert np.array_equal(lic.rans_decode(got, (n,), cdf, rows=idx), sym)
+
+
+def test_rans_corrupt(lic):
+    L = 32
+    cdf = O.cdf_table([1.0, 2.0, 4.0], L)
+    sym = np.clip(np.round(RNG.standard_normal((3, 16, 16)) * 2), -L, L).astype(np.int8)
+    b = lic.rans_encode(sym, cdf)
+    for cut in (1, 3, len(b) // 2):
+        with pytest.raises(lic.CorruptStream):
+            lic.rans_decode(b[:-cut], sym.shape, cdf)
+    with pytest.raises(lic.CorruptStream):
+        lic.rans_decode(b + b"\x01", sym.shape, cdf)
+    with pytest.raises(lic.LicError):
+        lic.rans_encode(np.full((3, 1, 1), 40, np.int8), cdf)      # outside [-L, L]
+
+
+def test_licw_roundtrip():
+    for kind in (0, 1):
+        spec = ModelSpec(kind=kind, N=128, M=192)
+        w = generate_weights(spec, 5)
+        blob = write_licw(spec, w)
+        spec2, w2 = read_licw_blocks(blob)
+        assert spec2 == spec
+        assert all(np.array_equal(w[k], w2[k]) for k in w)
+        assert write_licw(spec, generate_weights(spec, 5)) == blob          # deterministic
+        assert blob[:4] == b"LICW"
