@@ -84,6 +84,12 @@ void lic_close(lic_codec* codec);
  * for the factorized codec).  `kind` receives 0 (factorized) or 1 (hyperprior). */
 lic_status lic_shapes(const lic_codec* codec, lic_shape* y, lic_shape* z, int* kind);
 
+/* Zero-copy toggle ("we offer a command-line option ... to quickly toggle
+ * this option on or off").  Off (default): host symbol planes move by DMA through
+ * device staging buffers.  On: kernels read/write pinned host planes in place over PCIe
+ * (the paper's unified-memory Jetson path). */
+lic_status lic_set_zero_copy(lic_codec* codec, int on);
+
 /* Message for the last error on this codec (owned by the codec). */
 const char* lic_last_error(const lic_codec* codec);
 
@@ -143,6 +149,15 @@ lic_status lic_test_sigma_to_index(lic_codec* codec, const float* sigma, size_t 
 lic_status lic_set_debug(lic_codec* codec, int on);
 lic_status lic_debug_latents(lic_codec* codec, uint32_t batch, float* y, float* z, float* sigma);
 
+/* ---------------------------------------------------------------- measurement
+ * When profiling is on, every GEMM-engine launch is bracketed by CUDA events recorded on
+ * the stream it is launched on; lic_profile_read synchronises and returns the summed
+ * device time and launch count per layer since profiling was enabled (then resets). */
+lic_status lic_profile(lic_codec* codec, int on);
+lic_status lic_profile_read(lic_codec* codec, int layer_id, double* ms, uint64_t* launches);
+/* Total kernels this codec has launched (GEMM engine + ingest kernels). */
+lic_status lic_launch_count(const lic_codec* codec, uint64_t* n);
+
 /* ---------------------------------------------------------------- HOST entropy coder */
 
 /* CDF tables of this codec: which = 0 factorized y rows (one per
@@ -170,6 +185,42 @@ lic_status lic_rans_encode(const int8_t* sym, const uint8_t* row, lic_shape plan
 lic_status lic_rans_decode(const uint8_t* in, size_t len, const uint8_t* row, lic_shape plane,
                            const uint32_t* cdf, uint32_t n_rows, uint32_t row_len, int sym_min,
                            int8_t* sym_out);
+
+/* ---------------------------------------------------------------- streaming pipeline
+ * The paper's architecture (§III.A-B, Fig. 2): every frame is a task that moves
+ * through GPU and CPU workloads; one dedicated control thread drives the GPU (encode,
+ * decoder GPU1 = lic_hyper_indexes, decoder GPU2 = lic_decode) and a pool of worker
+ * threads runs the rANS coder (encode y/z, decode z, decode y).  Batches of frames are
+ * double-buffered in pooled pinned slots so that no GPU work waits on the host coder and
+ * vice versa.  lic_pipeline_run pushes `nframes` frames through the full round trip
+ * encode -> bitstreams -> decode.  serial = 1 runs the serial reference instead (each
+ * batch completes every stage before the next starts). */
+typedef struct lic_pipeline lic_pipeline;
+typedef struct {
+    uint32_t coder_threads;   /* host coder workers (the paper uses 3 and 10: PAPER.md:155, :163) */
+    uint32_t batch;           /* frames per GPU call (<= codec max_batch) */
+    uint32_t inflight;        /* batches in flight (>= 2 double-buffers) */
+    int u8;                   /* frames are u8 [H][W][3] (1) or f32 [3][H][W] (0) */
+    int serial;               /* 1: no overlap between stages (reference) */
+    int keep_bitstreams;      /* 1: keep every frame's strings for lic_pipeline_bitstream */
+} lic_pipeline_config;
+typedef struct {
+    uint64_t frames;          /* frames completed */
+    double seconds;           /* wall time of the run */
+    double latency_p50_ms, latency_p95_ms, latency_max_ms; /* per batch: encode start -> decode end */
+    uint64_t y_bytes, z_bytes;/* total bitstream bytes */
+    uint64_t symbol_mismatches; /* decoded != encoded symbols (must be 0: lossless) */
+    double gpu_busy_s, coder_busy_s; /* summed busy time of the GPU thread / coder threads */
+} lic_pipeline_stats;
+lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_config* cfg, lic_pipeline** out);
+void lic_pipeline_close(lic_pipeline* p);
+/* frames_in / frames_out: nframes frames, device or pinned-host pointers (zero-copy).
+ * nframes must be a multiple of cfg->batch. */
+lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, uint32_t nframes, void* frames_out,
+                            lic_pipeline_stats* stats);
+/* strings of frame i of the last run (keep_bitstreams = 1); z is NULL/0 for factorized. */
+lic_status lic_pipeline_bitstream(const lic_pipeline* p, uint32_t frame, const uint8_t** y, size_t* y_len,
+                                  const uint8_t** z, size_t* z_len);
 
 /* Library version string. */
 const char* lic_version(void);

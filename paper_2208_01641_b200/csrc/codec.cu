@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "../../include/lic.h"
+#include "internal.h"
 #include "layer.h"
 
 namespace lic {
@@ -159,6 +160,7 @@ struct lic_codec {
     size_t dbg_elems = 0;
     float *dbg_y = nullptr, *dbg_z = nullptr, *dbg_s = nullptr;
     int debug = 0;
+    int zero_copy = 0;
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
     std::vector<void*> allocs;          // device allocations to free
@@ -167,7 +169,28 @@ struct lic_codec {
     std::map<size_t, std::vector<void*>> free_lists;
     std::map<void*, size_t> owned;
     uint64_t pool_allocs = 0, pool_reuses = 0;
+    // measurement
+    uint64_t launches = 0;
+    int profiling = 0;
+    std::vector<cudaEvent_t> ev;            // [2 * kProfSlots]
+    std::vector<int> ev_layer;              // layer of each recorded pair
+    int ev_used = 0;
+    double prof_ms[NLAYER] = {0};
+    uint64_t prof_n[NLAYER] = {0};
 };
+static constexpr int kProfSlots = 2048;
+
+static void prof_flush(lic_codec* c) {
+    if (!c->ev_used) return;
+    cudaEventSynchronize(c->ev[2 * (c->ev_used - 1) + 1]);
+    for (int i = 0; i < c->ev_used; ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]);
+        c->prof_ms[c->ev_layer[i]] += ms;
+        c->prof_n[c->ev_layer[i]] += 1;
+    }
+    c->ev_used = 0;
+}
 
 static lic_status fail(lic_codec* c, lic_status st, const char* fmt, ...) {
     if (c) {
@@ -347,11 +370,23 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
     P.batch = batch;
     P.total_tiles = batch * P.nphase * P.tiles_y * P.tiles_x * P.n_ntiles;
     const int grid = std::min(P.total_tiles, c->num_sms);
+    const int lid = (int)(&Ly - c->layers);
+    if (c->profiling) {
+        if (c->ev_used == kProfSlots) prof_flush(c);
+        CK(cudaEventRecord(c->ev[2 * c->ev_used], st));
+    }
     CK(launch_conv_umma(Ly.mapA, Ly.mapB, Ly.mapG, P, grid, st));
+    ++c->launches;
+    if (c->profiling) {
+        CK(cudaEventRecord(c->ev[2 * c->ev_used + 1], st));
+        c->ev_layer[c->ev_used++] = lid;
+    }
     return LIC_OK;
 }
 
 // ------------------------------------------------------------------ pointer handling
+struct OutBuf { void* dev; void* user; size_t bytes; };
+static void* device_only(const void* p);
 // Returns a device-accessible alias of p (device memory or pinned/mapped host memory),
 // or nullptr if p is pageable host memory that must be staged.
 static void* device_alias(const void* p) {
@@ -363,6 +398,21 @@ static void* device_alias(const void* p) {
     return nullptr;
 }
 
+// Device memory only (frames: host frames are moved by DMA into the staging buffer, since the
+// ingest gather and the per-channel frame stores would be uncoalesced over PCIe).
+static void* device_only(const void* p) {
+    if (!p) return nullptr;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return const_cast<void*>(p);
+    return nullptr;
+}
+
+static OutBuf route_frames_out(void* user, void* staging, size_t bytes) {
+    void* d = device_only(user);
+    return d ? OutBuf{d, nullptr, bytes} : OutBuf{staging, user, bytes};
+}
+
 // ------------------------------------------------------------------ ABI
 extern "C" const char* lic_version(void) { return "lic-b200 0.1 (sm_100a tcgen05)"; }
 
@@ -372,6 +422,7 @@ extern "C" void lic_close(lic_codec* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     for (void* p : c->allocs) cudaFree(p);
     {
         std::lock_guard<std::mutex> g(c->pool_mu);
@@ -636,11 +687,13 @@ extern "C" lic_status lic_buf_stats(const lic_codec* c, uint64_t* allocations, u
 }
 
 // ------------------------------------------------------------------ encode / decode
-struct OutBuf { void* dev; void* user; size_t bytes; };
 
-static OutBuf route_out(void* user, void* staging, size_t bytes) {
-    void* d = device_alias(user);
+static OutBuf route_out(lic_codec* c, void* user, void* staging, size_t bytes) {
+    void* d = c->zero_copy ? device_alias(user) : device_only(user);
     return d ? OutBuf{d, nullptr, bytes} : OutBuf{staging, user, bytes};
+}
+static const void* route_in(lic_codec* c, const void* user) {
+    return c->zero_copy ? device_alias(user) : device_only(user);
 }
 
 static lic_status finish_out(lic_codec* c, const OutBuf& o, cudaStream_t st) {
@@ -678,19 +731,20 @@ static lic_status encode_impl(lic_codec* c, const void* frames, int hwc, uint32_
     cudaStream_t st = stream ? (cudaStream_t)stream : c->stream;
     const int B = (int)batch;
     const size_t fbytes = (size_t)B * 3 * c->H * c->W * (hwc ? 1 : 4);
-    const void* fdev = device_alias(frames);
+    const void* fdev = device_only(frames);
     if (!fdev) {
         CK(cudaMemcpyAsync(c->d_frames, frames, fbytes, cudaMemcpyHostToDevice, st));
         fdev = c->d_frames;
     }
     const size_t ny = (size_t)B * c->M * (c->Hp / 16) * (c->Wp / 16);
     const size_t nz = hyper ? (size_t)B * c->N * (c->Hp / 64) * (c->Wp / 64) : 0;
-    OutBuf oy = route_out(y_sym, c->d_ysym, ny);
-    OutBuf oi = hyper ? route_out(y_idx, c->d_yidx, ny) : OutBuf{nullptr, nullptr, 0};
-    OutBuf oz = hyper ? route_out(z_sym, c->d_zsym, nz) : OutBuf{nullptr, nullptr, 0};
+    OutBuf oy = route_out(c, y_sym, c->d_ysym, ny);
+    OutBuf oi = hyper ? route_out(c, y_idx, c->d_yidx, ny) : OutBuf{nullptr, nullptr, 0};
+    OutBuf oz = hyper ? route_out(c, z_sym, c->d_zsym, nz) : OutBuf{nullptr, nullptr, 0};
     CK(cudaMemsetAsync(c->d_sat, 0, 8, st));
     CK(launch_ingest(fdev, hwc, B, c->H, c->W, c->top, c->left, c->Hp / 2, c->Wp / 2, c->bufI, c->planeI,
                      c->split, st));
+    ++c->launches;
     for (int id : {GA1, GA2, GA3})
         if ((r = run_layer(c, c->layers[id], c->layers[id].prm, B, st))) return r;
     {
@@ -736,13 +790,14 @@ extern "C" lic_status lic_hyper_indexes(lic_codec* c, const int8_t* z_sym, uint3
     const int B = (int)batch;
     const int Hz = c->Hp / 64, Wz = c->Wp / 64;
     const size_t nz = (size_t)B * c->N * Hz * Wz, ny = (size_t)B * c->M * (c->Hp / 16) * (c->Wp / 16);
-    const int8_t* zd = (const int8_t*)device_alias(z_sym);
+    const int8_t* zd = (const int8_t*)route_in(c, z_sym);
     if (!zd) {
         CK(cudaMemcpyAsync(c->d_zsym, z_sym, nz, cudaMemcpyHostToDevice, st));
         zd = c->d_zsym;
     }
-    OutBuf oi = route_out(y_idx, c->d_yidx, ny);
+    OutBuf oi = route_out(c, y_idx, c->d_yidx, ny);
     CK(launch_sym_ingest(zd, c->mu_z, B, c->N, Hz, Wz, c->bufZ, c->planeZ, c->split, st));
+    ++c->launches;
     if ((r = run_hs(c, B, (uint8_t*)oi.dev, nullptr, st))) return r;
     if ((r = finish_out(c, oi, st))) return r;
     if (!stream) CK(cudaStreamSynchronize(st));
@@ -757,14 +812,15 @@ static lic_status decode_impl(lic_codec* c, const int8_t* y_sym, uint32_t batch,
     const int B = (int)batch;
     const int Hy = c->Hp / 16, Wy = c->Wp / 16;
     const size_t ny = (size_t)B * c->M * Hy * Wy;
-    const int8_t* yd = (const int8_t*)device_alias(y_sym);
+    const int8_t* yd = (const int8_t*)route_in(c, y_sym);
     if (!yd) {
         CK(cudaMemcpyAsync(c->d_ysym, y_sym, ny, cudaMemcpyHostToDevice, st));
         yd = c->d_ysym;
     }
     const size_t fbytes = (size_t)B * 3 * c->H * c->W * (u8 ? 1 : 4);
-    OutBuf of = route_out(frames, c->d_frames, fbytes);
+    OutBuf of = route_frames_out(frames, c->d_frames, fbytes);
     CK(launch_sym_ingest(yd, c->kind == 0 ? c->mu_y : nullptr, B, c->M, Hy, Wy, c->bufY, c->planeY, c->split, st));
+    ++c->launches;
     for (int id : {GS1, GS2, GS3})
         if ((r = run_layer(c, c->layers[id], c->layers[id].prm, B, st))) return r;
     ConvParams p = c->layers[GS4].prm;
@@ -830,7 +886,7 @@ extern "C" lic_status lic_test_layer(lic_codec* c, int id, const float* in, uint
     const int B = (int)batch;
     const size_t nin = (size_t)B * Ly.Cin * Ly.Hin * Ly.Win;
     const size_t nout = (size_t)B * Ly.Cout * Ly.Hout * Ly.Wout;
-    const float* ind = (const float*)device_alias(in);
+    const float* ind = (const float*)device_only(in);
     if (!ind) {
         CK(cudaMemcpyAsync(c->d_dbg, in, nin * 4, cudaMemcpyHostToDevice, st));
         ind = c->d_dbg;
@@ -840,7 +896,7 @@ extern "C" lic_status lic_test_layer(lic_codec* c, int id, const float* in, uint
     else
         CK(launch_pack_chw(ind, B, Ly.Cin, Ly.Hin, Ly.Win, Ly.in_buf, Ly.in_plane, c->split, st));
     ConvParams p = Ly.prm;
-    OutBuf o = route_out(out, c->d_dbg, nout * 4);
+    OutBuf o = route_out(c, out, c->d_dbg, nout * 4);
     p.out_f32 = (float*)o.dev;
     p.sat_count = nullptr;
     if (Ly.ep == EP_YQUANT || Ly.ep == EP_ZQUANT) p.out_sym = c->d_ysym;   // symbols discarded
@@ -866,5 +922,44 @@ extern "C" lic_status lic_test_sigma_to_index(lic_codec* c, const float* sigma, 
     CK(cudaMemcpy(idx, di, n, cudaMemcpyDefault));
     cudaFree(ds);
     cudaFree(di);
+    return LIC_OK;
+}
+
+// ------------------------------------------------------------------ measurement
+extern "C" lic_status lic_profile(lic_codec* c, int on) {
+    if (!c) return LIC_EINVAL;
+    cudaSetDevice(c->device);
+    if (on && c->ev.empty()) {
+        c->ev.resize(2 * kProfSlots);
+        c->ev_layer.resize(kProfSlots);
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    }
+    if (!on) prof_flush(c);
+    for (int i = 0; i < NLAYER; ++i) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
+    c->ev_used = 0;
+    c->profiling = on;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_profile_read(lic_codec* c, int id, double* ms, uint64_t* n) {
+    if (!c || id < 0 || id >= NLAYER) return LIC_EINVAL;
+    cudaSetDevice(c->device);
+    prof_flush(c);
+    if (ms) *ms = c->prof_ms[id];
+    if (n) *n = c->prof_n[id];
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_launch_count(const lic_codec* c, uint64_t* n) {
+    if (!c || !n) return LIC_EINVAL;
+    *n = c->launches;
+    return LIC_OK;
+}
+
+size_t lic_internal_frame_pixels(const lic_codec* c) { return c ? (size_t)c->H * c->W : 0; }
+
+extern "C" lic_status lic_set_zero_copy(lic_codec* c, int on) {
+    if (!c) return LIC_EINVAL;
+    c->zero_copy = on ? 1 : 0;
     return LIC_OK;
 }

@@ -1,0 +1,350 @@
+// pipeline.cpp -- the streaming runtime: GPU workloads and the host entropy coder overlapped.
+//
+// PAPER.md §III.A: "Each frame ... is represented by a state-machine pattern task, which
+// must be processed by the above workloads sequentially.  For each workload, a FIFO task
+// queue implementing a multi-threaded producer-consumer pattern manages the execution of
+// the tasks ... for a GPU-intensive workload, a dedicated control thread fetches the tasks
+// and communicate with the GPU; for a CPU-intensive workload, multiple worker threads
+// perform the computations."  §III.B: the hyperprior encoder is 2-stage (GPU: g_a, h_a,
+// Q(z), h_s; CPU: Q(y), E(y), E(z)) and the decoder 4-stage (CPU1 E^-1(z), GPU1 h_s,
+// CPU2 E^-1(y), GPU2 g_s).  §III.D: memory is pooled, never freed in steady state.
+//
+// B200 design: the calling thread is the GPU control thread; it services three GPU task
+// kinds (ENC, IDX = decoder GPU1, DEC = decoder GPU2) from a ready queue, oldest-batch
+// and latest-stage first.  Worker threads run the per-frame coder tasks (C1: rANS encode
+// y and z, then decode z; C2: decode y).  Batches live in `inflight` pinned, device-mapped
+// slots: encode kernels write symbol planes straight into them (zero-copy)
+// and the decoder kernels read the decoded planes from them.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "../../include/lic.h"
+#include "internal.h"
+
+namespace {
+
+using clk = std::chrono::steady_clock;
+inline double now_s() { return std::chrono::duration<double>(clk::now().time_since_epoch()).count(); }
+
+enum GpuKind { G_ENC = 0, G_IDX = 1, G_DEC = 2 };
+enum CpuKind { C_ONE = 0, C_TWO = 1 };
+
+struct Slot {
+    int8_t* y_sym = nullptr;  uint8_t* y_idx = nullptr;  int8_t* z_sym = nullptr;
+    int8_t* z_dec = nullptr;  uint8_t* idx_dec = nullptr; int8_t* y_dec = nullptr;
+    std::vector<std::vector<uint8_t>> ystr, zstr;
+    std::vector<size_t> ylen, zlen;
+    int batch = -1;
+    int remaining = 0;
+    double t_start = 0;
+};
+
+struct GpuTask { GpuKind kind; int slot; };
+struct CpuTask { CpuKind kind; int slot; int frame; };
+
+}  // namespace
+
+struct lic_pipeline {
+    lic_codec* codec = nullptr;
+    lic_pipeline_config cfg{};
+    int hyper = 0;
+    lic_shape ys{}, zs{};
+    size_t ny = 0, nz = 0, in_bytes = 0, out_bytes = 0;
+    const uint32_t* cdf_y = nullptr; uint32_t rows_y = 0;
+    const uint32_t* cdf_z = nullptr; uint32_t rows_z = 0;
+    uint32_t row_len = 0;
+    int sym_min = 0;
+    std::vector<Slot> slots;
+    std::vector<void*> pinned;
+    // threading
+    std::mutex mu;
+    std::condition_variable cv_gpu, cv_cpu;
+    std::deque<CpuTask> cpu_q;
+    std::vector<GpuTask> gpu_q;
+    std::vector<std::thread> workers;
+    std::condition_variable cv_idle;
+    int active = 0;
+    bool stop = false;
+    // run state
+    const uint8_t* in = nullptr;
+    uint8_t* out = nullptr;
+    int nbatches = 0, next_enc = 0, done = 0;
+    std::vector<int> free_slots;
+    std::vector<double> lat;
+    uint64_t mismatches = 0, y_bytes = 0, z_bytes = 0;
+    double coder_busy = 0, gpu_busy = 0;
+    lic_status err = LIC_OK;
+    std::vector<std::vector<uint8_t>> keep_y, keep_z;
+};
+
+static void coder_task(lic_pipeline* p, const CpuTask& t) {
+    Slot& s = p->slots[t.slot];
+    const size_t f = (size_t)t.frame;
+    lic_status st = LIC_OK;
+    uint64_t mism = 0;
+    if (t.kind == C_ONE) {
+        // encoder CPU workload: E(y) (and E(z)); then decoder CPU1: E^-1(z) (hyper) or E^-1(y)
+        st = lic_rans_encode(s.y_sym + f * p->ny, p->hyper ? s.y_idx + f * p->ny : nullptr, p->ys, p->cdf_y,
+                             p->rows_y, p->row_len, p->sym_min, s.ystr[f].data(), s.ystr[f].size(), &s.ylen[f]);
+        if (!st && p->hyper)
+            st = lic_rans_encode(s.z_sym + f * p->nz, nullptr, p->zs, p->cdf_z, p->rows_z, p->row_len, p->sym_min,
+                                 s.zstr[f].data(), s.zstr[f].size(), &s.zlen[f]);
+        if (!st && p->hyper) {
+            st = lic_rans_decode(s.zstr[f].data(), s.zlen[f], nullptr, p->zs, p->cdf_z, p->rows_z, p->row_len,
+                                 p->sym_min, s.z_dec + f * p->nz);
+            if (!st && std::memcmp(s.z_dec + f * p->nz, s.z_sym + f * p->nz, p->nz) != 0) mism += 1;
+        } else if (!st) {
+            st = lic_rans_decode(s.ystr[f].data(), s.ylen[f], nullptr, p->ys, p->cdf_y, p->rows_y, p->row_len,
+                                 p->sym_min, s.y_dec + f * p->ny);
+            if (!st && std::memcmp(s.y_dec + f * p->ny, s.y_sym + f * p->ny, p->ny) != 0) mism += 1;
+        }
+    } else {
+        // decoder CPU2: E^-1(y) with the indexes from decoder GPU1
+        st = lic_rans_decode(s.ystr[f].data(), s.ylen[f], s.idx_dec + f * p->ny, p->ys, p->cdf_y, p->rows_y,
+                             p->row_len, p->sym_min, s.y_dec + f * p->ny);
+        if (!st && std::memcmp(s.y_dec + f * p->ny, s.y_sym + f * p->ny, p->ny) != 0) mism += 1;
+    }
+    std::lock_guard<std::mutex> g(p->mu);
+    if (st && !p->err) p->err = st;
+    p->mismatches += mism;
+    if (--s.remaining == 0) {
+        if (t.kind == C_ONE && p->hyper) p->gpu_q.push_back({G_IDX, t.slot});
+        else p->gpu_q.push_back({G_DEC, t.slot});
+        p->cv_gpu.notify_one();
+    }
+}
+
+static void worker_main(lic_pipeline* p) {
+    for (;;) {
+        CpuTask t;
+        {
+            std::unique_lock<std::mutex> lk(p->mu);
+            p->cv_cpu.wait(lk, [&] { return p->stop || !p->cpu_q.empty(); });
+            if (p->stop) return;
+            t = p->cpu_q.front();
+            p->cpu_q.pop_front();
+            ++p->active;
+        }
+        const double t0 = now_s();
+        coder_task(p, t);
+        const double dt = now_s() - t0;
+        std::lock_guard<std::mutex> g(p->mu);
+        p->coder_busy += dt;
+        if (--p->active == 0) p->cv_idle.notify_all();
+    }
+}
+
+extern "C" void lic_pipeline_close(lic_pipeline* p) {
+    if (!p) return;
+    {
+        std::lock_guard<std::mutex> g(p->mu);
+        p->stop = true;
+    }
+    p->cv_cpu.notify_all();
+    for (auto& t : p->workers) t.join();
+    for (void* q : p->pinned) cudaFreeHost(q);
+    delete p;
+}
+
+extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_config* cfg, lic_pipeline** out) {
+    if (!codec || !cfg || !out || cfg->batch == 0 || cfg->coder_threads == 0) return LIC_EINVAL;
+    *out = nullptr;
+    lic_pipeline* p = new lic_pipeline();
+    p->codec = codec;
+    p->cfg = *cfg;
+    if (p->cfg.inflight == 0) p->cfg.inflight = 2;
+    if (p->cfg.serial) p->cfg.inflight = 1;
+    lic_status st = lic_shapes(codec, &p->ys, &p->zs, &p->hyper);
+    if (st) { delete p; return st; }
+    p->ny = (size_t)p->ys.c * p->ys.h * p->ys.w;
+    p->nz = (size_t)p->zs.c * p->zs.h * p->zs.w;
+    uint32_t rl = 0;
+    if (p->hyper) {
+        if ((st = lic_cdf(codec, 2, &p->cdf_y, &p->rows_y, &rl)) || (st = lic_cdf(codec, 1, &p->cdf_z, &p->rows_z, &rl))) {
+            delete p;
+            return st;
+        }
+    } else if ((st = lic_cdf(codec, 0, &p->cdf_y, &p->rows_y, &rl))) {
+        delete p;
+        return st;
+    }
+    p->row_len = rl;
+    p->sym_min = -(int)((rl - 2) / 2);
+    const size_t B = cfg->batch;
+    auto pin = [&](size_t bytes) -> void* {
+        void* q = nullptr;
+        if (cudaHostAlloc(&q, bytes ? bytes : 16, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        p->pinned.push_back(q);
+        return q;
+    };
+    p->slots.resize(p->cfg.inflight);
+    for (Slot& s : p->slots) {
+        s.y_sym = (int8_t*)pin(B * p->ny);
+        s.y_dec = (int8_t*)pin(B * p->ny);
+        s.y_idx = (uint8_t*)pin(p->hyper ? B * p->ny : 16);
+        s.idx_dec = (uint8_t*)pin(p->hyper ? B * p->ny : 16);
+        s.z_sym = (int8_t*)pin(p->hyper ? B * p->nz : 16);
+        s.z_dec = (int8_t*)pin(p->hyper ? B * p->nz : 16);
+        if (!s.y_sym || !s.y_dec || !s.y_idx || !s.idx_dec || !s.z_sym || !s.z_dec) {
+            lic_pipeline_close(p);
+            return LIC_ENOMEM;
+        }
+        s.ystr.assign(B, std::vector<uint8_t>(2 * p->ny + 64));
+        s.zstr.assign(B, std::vector<uint8_t>(2 * p->nz + 64));
+        s.ylen.assign(B, 0);
+        s.zlen.assign(B, 0);
+    }
+    for (uint32_t i = 0; i < cfg->coder_threads; ++i) p->workers.emplace_back(worker_main, p);
+    *out = p;
+    return LIC_OK;
+}
+
+static lic_status gpu_call(lic_pipeline* p, const GpuTask& t) {
+    Slot& s = p->slots[t.slot];
+    const uint32_t B = p->cfg.batch;
+    const size_t b = (size_t)s.batch;
+    switch (t.kind) {
+    case G_ENC: {
+        const uint8_t* fr = p->in + b * B * p->in_bytes;
+        return p->cfg.u8 ? lic_encode_u8(p->codec, fr, B, s.y_sym, p->hyper ? s.y_idx : nullptr,
+                                         p->hyper ? s.z_sym : nullptr, nullptr, nullptr)
+                         : lic_encode(p->codec, (const float*)fr, B, s.y_sym, p->hyper ? s.y_idx : nullptr,
+                                      p->hyper ? s.z_sym : nullptr, nullptr, nullptr);
+    }
+    case G_IDX:
+        return lic_hyper_indexes(p->codec, s.z_dec, B, s.idx_dec, nullptr);
+    case G_DEC: {
+        uint8_t* fr = p->out + b * B * p->out_bytes;
+        return p->cfg.u8 ? lic_decode_u8(p->codec, s.y_dec, B, fr, nullptr)
+                         : lic_decode(p->codec, s.y_dec, B, (float*)fr, nullptr);
+    }
+    }
+    return LIC_EINVAL;
+}
+
+extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, uint32_t nframes, void* frames_out,
+                                       lic_pipeline_stats* stats) {
+    if (!p || !frames_in || !frames_out || nframes == 0 || nframes % p->cfg.batch) return LIC_EINVAL;
+    const uint32_t B = p->cfg.batch;
+    const size_t px = lic_internal_frame_pixels(p->codec);
+    p->in_bytes = px * 3 * (p->cfg.u8 ? 1 : 4);
+    p->out_bytes = p->in_bytes;
+    {
+        std::lock_guard<std::mutex> g(p->mu);
+        p->in = (const uint8_t*)frames_in;
+        p->out = (uint8_t*)frames_out;
+        p->nbatches = (int)(nframes / B);
+        p->next_enc = 0;
+        p->done = 0;
+        p->free_slots.clear();
+        for (int i = (int)p->slots.size() - 1; i >= 0; --i) p->free_slots.push_back(i);
+        p->gpu_q.clear();
+        p->cpu_q.clear();
+        p->lat.clear();
+        p->mismatches = p->y_bytes = p->z_bytes = 0;
+        p->coder_busy = p->gpu_busy = 0;
+        p->err = LIC_OK;
+        if (p->cfg.keep_bitstreams) {
+            p->keep_y.assign(nframes, {});
+            p->keep_z.assign(nframes, {});
+        }
+    }
+    const double t_run0 = now_s();
+    for (;;) {
+        GpuTask t{};
+        {
+            std::unique_lock<std::mutex> lk(p->mu);
+            auto can_enc = [&] {
+                if (p->next_enc >= p->nbatches || p->free_slots.empty()) return false;
+                return !p->cfg.serial || p->done == p->next_enc;
+            };
+            p->cv_gpu.wait(lk, [&] { return p->err || p->done == p->nbatches || !p->gpu_q.empty() || can_enc(); });
+            if (p->err || p->done == p->nbatches) break;
+            if (!p->gpu_q.empty()) {
+                // latest stage first, then oldest batch: drains frames, bounds latency
+                auto best = std::max_element(p->gpu_q.begin(), p->gpu_q.end(), [&](const GpuTask& a, const GpuTask& b) {
+                    if (a.kind != b.kind) return a.kind < b.kind;
+                    return p->slots[a.slot].batch > p->slots[b.slot].batch;
+                });
+                t = *best;
+                p->gpu_q.erase(best);
+            } else {
+                const int s = p->free_slots.back();
+                p->free_slots.pop_back();
+                p->slots[s].batch = p->next_enc++;
+                p->slots[s].t_start = now_s();
+                t = {G_ENC, s};
+            }
+        }
+        const double g0 = now_s();
+        lic_status st = gpu_call(p, t);
+        const double g1 = now_s();
+        std::lock_guard<std::mutex> g(p->mu);
+        p->gpu_busy += g1 - g0;
+        if (st) { p->err = st; break; }
+        Slot& s = p->slots[t.slot];
+        if (t.kind == G_ENC || t.kind == G_IDX) {
+            s.remaining = (int)B;
+            for (uint32_t f = 0; f < B; ++f) p->cpu_q.push_back({t.kind == G_ENC ? C_ONE : C_TWO, t.slot, (int)f});
+            p->cv_cpu.notify_all();
+        } else {
+            for (uint32_t f = 0; f < B; ++f) {
+                p->y_bytes += s.ylen[f];
+                p->z_bytes += p->hyper ? s.zlen[f] : 0;
+                if (p->cfg.keep_bitstreams) {
+                    const size_t gi = (size_t)s.batch * B + f;
+                    p->keep_y[gi].assign(s.ystr[f].begin(), s.ystr[f].begin() + s.ylen[f]);
+                    if (p->hyper) p->keep_z[gi].assign(s.zstr[f].begin(), s.zstr[f].begin() + s.zlen[f]);
+                }
+            }
+            p->lat.push_back((g1 - s.t_start) * 1e3);
+            p->free_slots.push_back(t.slot);
+            ++p->done;
+        }
+    }
+    const double t_run1 = now_s();
+    // error path: drop queued coder work and wait for tasks already running
+    std::unique_lock<std::mutex> g(p->mu);
+    p->cpu_q.clear();
+    p->cv_idle.wait(g, [&] { return p->active == 0; });
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->frames = (uint64_t)p->done * B;
+        stats->seconds = t_run1 - t_run0;
+        std::vector<double> l = p->lat;
+        std::sort(l.begin(), l.end());
+        if (!l.empty()) {
+            stats->latency_p50_ms = l[l.size() / 2];
+            stats->latency_p95_ms = l[std::min(l.size() - 1, (size_t)(0.95 * l.size()))];
+            stats->latency_max_ms = l.back();
+        }
+        stats->y_bytes = p->y_bytes;
+        stats->z_bytes = p->z_bytes;
+        stats->symbol_mismatches = p->mismatches;
+        stats->gpu_busy_s = p->gpu_busy;
+        stats->coder_busy_s = p->coder_busy;
+    }
+    return p->err;
+}
+
+extern "C" lic_status lic_pipeline_bitstream(const lic_pipeline* p, uint32_t frame, const uint8_t** y, size_t* y_len,
+                                             const uint8_t** z, size_t* z_len) {
+    if (!p || !p->cfg.keep_bitstreams || frame >= p->keep_y.size()) return LIC_EINVAL;
+    if (y) *y = p->keep_y[frame].data();
+    if (y_len) *y_len = p->keep_y[frame].size();
+    if (z) *z = p->hyper ? p->keep_z[frame].data() : nullptr;
+    if (z_len) *z_len = p->hyper ? p->keep_z[frame].size() : 0;
+    return LIC_OK;
+}

@@ -69,6 +69,35 @@ _L.lic_cdf_build.argtypes = [_P, _u32, _u32, _P]
 _L.lic_rans_encode.argtypes = [_P, _P, Shape, _P, _u32, _u32, _i, _P, _sz, ctypes.POINTER(_sz)]
 _L.lic_rans_decode.argtypes = [_P, _sz, _P, Shape, _P, _u32, _u32, _i, _P]
 _L.lic_version.restype = ctypes.c_char_p
+_L.lic_profile.argtypes = [_P, _i]
+_L.lic_profile_read.argtypes = [_P, _i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
+_L.lic_launch_count.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64)]
+_L.lic_set_zero_copy.argtypes = [_P, _i]
+
+
+
+class PipelineConfig(ctypes.Structure):
+    _fields_ = [("coder_threads", ctypes.c_uint32), ("batch", ctypes.c_uint32), ("inflight", ctypes.c_uint32),
+                ("u8", ctypes.c_int), ("serial", ctypes.c_int), ("keep_bitstreams", ctypes.c_int)]
+
+
+class PipelineStats(ctypes.Structure):
+    _fields_ = [("frames", ctypes.c_uint64), ("seconds", ctypes.c_double), ("latency_p50_ms", ctypes.c_double),
+                ("latency_p95_ms", ctypes.c_double), ("latency_max_ms", ctypes.c_double),
+                ("y_bytes", ctypes.c_uint64), ("z_bytes", ctypes.c_uint64), ("symbol_mismatches", ctypes.c_uint64),
+                ("gpu_busy_s", ctypes.c_double), ("coder_busy_s", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_L.lic_pipeline_open.argtypes = [_P, ctypes.POINTER(PipelineConfig), ctypes.POINTER(_P)]
+_L.lic_pipeline_close.argtypes = [_P]
+_L.lic_pipeline_close.restype = None
+_L.lic_pipeline_run.argtypes = [_P, _P, _u32, _P, ctypes.POINTER(PipelineStats)]
+_L.lic_pipeline_bitstream.argtypes = [_P, _u32, ctypes.POINTER(ctypes.POINTER(ctypes.c_uint8)),
+                                      ctypes.POINTER(_sz), ctypes.POINTER(ctypes.POINTER(ctypes.c_uint8)),
+                                      ctypes.POINTER(_sz)]
 
 EXPORTED = [n for n in dir(_L) if n.startswith("lic_")]
 
@@ -230,6 +259,27 @@ class Codec:
         _L.lic_buf_stats(self._h, ctypes.byref(a), ctypes.byref(r))
         return a.value, r.value
 
+    def set_zero_copy(self, on=True):
+        self._chk(_L.lic_set_zero_copy(self._h, int(on)), "lic_set_zero_copy")
+
+    # -- measurement
+    def profile(self, on=True):
+        self._chk(_L.lic_profile(self._h, int(on)), "lic_profile")
+
+    def profile_read(self):
+        """{layer: (ms, launches)} accumulated since profile(True); resets."""
+        out = {}
+        for i, name in enumerate(LAYERS):
+            ms, n = ctypes.c_double(), ctypes.c_uint64()
+            if _L.lic_profile_read(self._h, i, ctypes.byref(ms), ctypes.byref(n)) == 0 and n.value:
+                out[name] = (ms.value, n.value)
+        return out
+
+    def launch_count(self):
+        n = ctypes.c_uint64()
+        self._chk(_L.lic_launch_count(self._h, ctypes.byref(n)), "lic_launch_count")
+        return n.value
+
     # -- test exports
     def layer_shapes(self, layer):
         lid = LAYERS.index(layer) if isinstance(layer, str) else layer
@@ -261,3 +311,46 @@ class Codec:
         s = np.empty((batch,) + self.y_shape, np.float32) if self.hyper else None
         self._chk(_L.lic_debug_latents(self._h, batch, _ptr(y), _ptr(z), _ptr(s)), "lic_debug_latents")
         return y, z, s
+
+
+class Pipeline:
+    """lic_pipeline: GPU control thread (the caller) + native coder worker pool."""
+
+    def __init__(self, codec: Codec, coder_threads: int, batch: int, inflight: int = 2, u8: bool = True,
+                 serial: bool = False, keep_bitstreams: bool = False):
+        self.codec = codec
+        self.cfg = PipelineConfig(coder_threads, batch, inflight, int(u8), int(serial), int(keep_bitstreams))
+        self._h = _P()
+        st = _L.lic_pipeline_open(codec.handle, ctypes.byref(self.cfg), ctypes.byref(self._h))
+        if st:
+            raise LicError(st, "lic_pipeline_open")
+
+    def run(self, frames_in, frames_out, nframes=None):
+        n = nframes if nframes is not None else frames_in.shape[0]
+        st = PipelineStats()
+        rc = _L.lic_pipeline_run(self._h, _ptr(frames_in), n, _ptr(frames_out), ctypes.byref(st))
+        if rc:
+            raise LicError(rc, "lic_pipeline_run: " + (_L.lic_last_error(self.codec.handle) or b"").decode())
+        return st.as_dict()
+
+    def bitstream(self, i):
+        y, z = ctypes.POINTER(ctypes.c_uint8)(), ctypes.POINTER(ctypes.c_uint8)()
+        yl, zl = ctypes.c_size_t(), ctypes.c_size_t()
+        rc = _L.lic_pipeline_bitstream(self._h, i, ctypes.byref(y), ctypes.byref(yl), ctypes.byref(z),
+                                       ctypes.byref(zl))
+        if rc:
+            raise LicError(rc, "lic_pipeline_bitstream")
+        yb = ctypes.string_at(y, yl.value)
+        zb = ctypes.string_at(z, zl.value) if zl.value else None
+        return yb, zb
+
+    def close(self):
+        if self._h:
+            _L.lic_pipeline_close(self._h)
+            self._h = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
