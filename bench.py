@@ -169,7 +169,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=4, help="frames per step (per GPU)")
     ap.add_argument("--coder-threads", type=int, default=0, help="0: derived from the host cores")
-    ap.add_argument("--inflight", type=int, default=3)
+    ap.add_argument("--inflight", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--serial", action="store_true", help="serial reference pipeline (no overlap)")
     ap.add_argument("--zero-copy", action="store_true", help="kernels touch pinned host planes in place")

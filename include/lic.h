@@ -222,6 +222,19 @@ lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, uint32_t nfr
 lic_status lic_pipeline_bitstream(const lic_pipeline* p, uint32_t frame, const uint8_t** y, size_t* y_len,
                                   const uint8_t** z, size_t* z_len);
 
+/* Prepared coder tables (same bitstream as lic_rans_encode / lic_rans_decode, faster):
+ * per (row, symbol) encoder constants with an exact reciprocal in place of the division
+ * x / freq, and a 4096-bucket slot -> symbol index per row for the decoder.  Immutable
+ * after lic_rans_prepare; shareable across threads.  `cdf` is copied. */
+typedef struct lic_rans_tables lic_rans_tables;
+lic_status lic_rans_prepare(const uint32_t* cdf, uint32_t n_rows, uint32_t row_len, int sym_min,
+                            lic_rans_tables** out);
+void lic_rans_tables_free(lic_rans_tables* t);
+lic_status lic_rans_encode_fast(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row, lic_shape plane,
+                                uint8_t* out, size_t cap, size_t* out_len);
+lic_status lic_rans_decode_fast(const lic_rans_tables* t, const uint8_t* in, size_t len, const uint8_t* row,
+                                lic_shape plane, int8_t* sym_out);
+
 /* Library version string. */
 const char* lic_version(void);
 

@@ -19,45 +19,63 @@ __device__ __forceinline__ void put_split(__half* out, size_t plane, size_t i, f
     if (split == 2) out[plane + i] = __float2half_rn(v - __half2float(h));
 }
 
-// one thread per (output pixel, k); k = (ky*5 + kx)*3 + c for k < 75, zero for 75..127
-template <typename T>
-__global__ void ingest_im2col_kernel(const T* __restrict__ fr, int hwc, int B, int H, int W, int top,
-                                     int left, int Ho, int Wo, __half* __restrict__ out, size_t plane,
-                                     int split) {
-    const size_t n = (size_t)B * Ho * Wo * 128;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const int k = (int)(i & 127);
-        const size_t pix = i >> 7;
-        const int ox = (int)(pix % Wo);
-        const int oy = (int)((pix / Wo) % Ho);
-        const int b = (int)(pix / ((size_t)Wo * Ho));
-        float v = 0.0f;
-        if (k < 75) {
-            const int ky = k / 15, r = k % 15, kx = r / 3, c = r % 3;
-            const int iy = 2 * oy + ky - 2 - top, ix = 2 * ox + kx - 2 - left;
-            if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
-                if (hwc) v = (float)fr[(((size_t)b * H + iy) * W + ix) * 3 + c] / 255.0f;  // u8 / 255
-                else v = (float)fr[(((size_t)b * 3 + c) * H + iy) * W + ix];
-            }
-        }
-        put_split(out, plane, i, v, split);
-    }
+// im2col column k = (ky*5 + kx)*3 + c for k < 75, zero for 75..127
+
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
 }
 
-__global__ void sym_ingest_kernel(const int8_t* __restrict__ sym, const float* __restrict__ mu, int B, int C,
-                                  int H, int W, __half* __restrict__ out, size_t plane, int split) {
-    const size_t n = (size_t)B * C * H * W;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        // i enumerates NHWC output order: coalesced writes
-        const int c = (int)(i % C);
-        const size_t pix = i / C;
-        const int x = (int)(pix % W);
-        const int y = (int)((pix / W) % H);
-        const int b = (int)(pix / ((size_t)W * H));
-        const float m = mu ? mu[c] : 0.0f;
-        const float v = (float)sym[(((size_t)b * C + c) * H + y) * W + x] + m;
-        put_split(out, plane, i, v, split);
+// grid (ceil(Wo*16/256), Ho, B): thread = (output column ox, group g of 8 im2col columns);
+// one 16-byte hi and one 16-byte lo store per thread, no integer division
+template <typename T>
+__global__ void __launch_bounds__(256) ingest_im2col_kernel(const T* __restrict__ fr, int hwc, int H, int W,
+                                                            int top, int left, int Ho, int Wo,
+                                                            __half* __restrict__ out, size_t plane, int split) {
+    // x = u8 / 255 (IEEE fp32 division) tabulated once per block
+    __shared__ float s_u8[256];
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) s_u8[v] = __fdiv_rn((float)v, 255.0f);
+    __syncthreads();
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    const int ox = i >> 4, g = i & 15, oy = blockIdx.y, b = blockIdx.z;
+    if (ox >= Wo) return;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int k = g * 8 + j;
+        v[j] = 0.0f;
+        if (g < 10 && k < 75) {
+            // k = (ky*5 + kx)*3 + c; constant divisors compile to multiply-shift (a lane-divergent
+            // __constant__ table would serialise 16 ways)
+            const int ky = k / 15, r15 = k - ky * 15, kx = r15 / 3, c = r15 - kx * 3;
+            const int iy = 2 * oy + ky - 2 - top, ix = 2 * ox + kx - 2 - left;
+            if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
+                if (hwc) v[j] = s_u8[(int)fr[(((size_t)b * H + iy) * W + ix) * 3 + c]];
+                else v[j] = (float)fr[(((size_t)b * 3 + c) * H + iy) * W + ix];
+            }
+        }
     }
+    uint4 hi, lo;
+    float r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = v[j] - __half2float(__float2half_rn(v[j]));
+    hi.x = pack_h2(v[0], v[1]); hi.y = pack_h2(v[2], v[3]); hi.z = pack_h2(v[4], v[5]); hi.w = pack_h2(v[6], v[7]);
+    lo.x = pack_h2(r[0], r[1]); lo.y = pack_h2(r[2], r[3]); lo.z = pack_h2(r[4], r[5]); lo.w = pack_h2(r[6], r[7]);
+    const size_t o = (((size_t)b * Ho + oy) * Wo + ox) * 16 + g;
+    reinterpret_cast<uint4*>(out)[o] = hi;
+    if (split == 2) reinterpret_cast<uint4*>(out + plane)[o] = lo;
+}
+
+// grid (ceil(W*C/256), H, B): consecutive threads write consecutive NHWC elements
+__global__ void __launch_bounds__(256) sym_ingest_kernel(const int8_t* __restrict__ sym, const float* __restrict__ mu,
+                                                         int C, int H, int W, __half* __restrict__ out, size_t plane,
+                                                         int split) {
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= W * C) return;
+    const int x = i / C, c = i - x * C, y = blockIdx.y, b = blockIdx.z;
+    const float m = mu ? mu[c] : 0.0f;
+    const float v = (float)sym[(((size_t)b * C + c) * H + y) * W + x] + m;
+    put_split(out, plane, (((size_t)b * H + y) * W) * C + i, v, split);
 }
 
 __global__ void pack_chw_kernel(const float* __restrict__ in, int B, int C, int H, int W,
@@ -94,20 +112,20 @@ static inline int grid_for(size_t n, int threads) {
 
 cudaError_t launch_ingest(const void* fr, int hwc, int B, int H, int W, int top, int left, int Ho, int Wo,
                           __half* out, size_t plane, int split, cudaStream_t st) {
-    const size_t n = (size_t)B * Ho * Wo * 128;
+    const dim3 grid((Wo * 16 + 255) / 256, Ho, B);
     if (hwc)
-        ingest_im2col_kernel<uint8_t><<<grid_for(n, 256), 256, 0, st>>>(
-            (const uint8_t*)fr, 1, B, H, W, top, left, Ho, Wo, out, plane, split);
+        ingest_im2col_kernel<uint8_t><<<grid, 256, 0, st>>>((const uint8_t*)fr, 1, H, W, top, left, Ho, Wo, out,
+                                                            plane, split);
     else
-        ingest_im2col_kernel<float><<<grid_for(n, 256), 256, 0, st>>>(
-            (const float*)fr, 0, B, H, W, top, left, Ho, Wo, out, plane, split);
+        ingest_im2col_kernel<float><<<grid, 256, 0, st>>>((const float*)fr, 0, H, W, top, left, Ho, Wo, out, plane,
+                                                          split);
     return cudaGetLastError();
 }
 
 cudaError_t launch_sym_ingest(const int8_t* sym, const float* mu, int B, int C, int H, int W, __half* out,
                               size_t plane, int split, cudaStream_t st) {
-    const size_t n = (size_t)B * C * H * W;
-    sym_ingest_kernel<<<grid_for(n, 256), 256, 0, st>>>(sym, mu, B, C, H, W, out, plane, split);
+    const dim3 grid((W * C + 255) / 256, H, B);
+    sym_ingest_kernel<<<grid, 256, 0, st>>>(sym, mu, C, H, W, out, plane, split);
     return cudaGetLastError();
 }
 

@@ -280,7 +280,8 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.Cin = Ly.Cin_eff;
     P.kchunks = Ly.Cin_eff / 64;
     P.Cout = Ly.Cout;
-    if (Ly.Cout <= 256) { P.BN = (Ly.Cout + 15) / 16 * 16; P.n_ntiles = 1; }
+    if (Ly.ep == EP_FINAL && Ly.deconv) { P.BN = 16; P.n_ntiles = 1; }
+    else if (Ly.Cout <= 256) { P.BN = (Ly.Cout + 15) / 16 * 16; P.n_ntiles = 1; }
     else { P.n_ntiles = (Ly.Cout + 255) / 256; P.BN = ((Ly.Cout + P.n_ntiles - 1) / P.n_ntiles + 15) / 16 * 16; }
     const bool gdn = (Ly.ep == EP_GDN || Ly.ep == EP_IGDN);
     if (gdn && (P.n_ntiles != 1 || P.BN != Ly.Cout || Ly.Cout % 64))
@@ -297,6 +298,17 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         for (int ky = 0; ky < Ly.k; ++ky)
             for (int kx = 0; kx < Ly.k; ++kx) {
                 P.tap_dy[ntap] = ky - Ly.p; P.tap_dx[ntap] = kx - Ly.p; P.tap_w[ntap] = ky * Ly.k + kx; ++ntap;
+            }
+        P.ntaps[0] = ntap;
+    } else if (Ly.ep == EP_FINAL) {
+        // g_s L4 (Cout = 3): all 4 sub-pixel phases packed into one N = 16 GEMM over the 9
+        // input offsets (dy, dx) in {-1,0,1}^2 shared by the phases; B row (phase*4 + co)
+        // holds W[co][.][ky][kx] with ky = py + 2 - 2dy, kx = px + 2 - 2dx (zero if outside).
+        P.Hg = Ly.Hin; P.Wg = Ly.Win; P.stride = 1; P.out_s = 2; P.nphase = 1; P.pack4 = 1;
+        P.tap0[0] = 0;
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                P.tap_dy[ntap] = dy; P.tap_dx[ntap] = dx; P.tap_w[ntap] = ntap; ++ntap;
             }
         P.ntaps[0] = ntap;
     } else {
@@ -317,19 +329,20 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     choose_tile(P.Hg, P.Wg, &P.Wt, &P.Ht);
     P.tiles_x = (P.Wg + P.Wt - 1) / P.Wt;
     P.tiles_y = (P.Hg + P.Ht - 1) / P.Ht;
-    // shared memory plan
+    // shared memory plan: stage ring | gamma (GDN) | mbarriers | per-channel constants
     const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)P.BN * 64 * 2;
     P.stage_bytes = a_bytes * P.split + b_bytes;
-    uint32_t extras = gdn ? (uint32_t)(P.BN / 64) * b_bytes + 2 * a_bytes : 0;
-    const uint32_t budget = 227 * 1024 - 1024 - 256;
-    int stages = (int)((budget - extras) / P.stage_bytes);
+    const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
+    const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64) * 4;
+    const uint32_t fixed = gamma_bytes + 256 + par_bytes + 1024;
+    int stages = (int)((227u * 1024u - fixed) / P.stage_bytes);
     stages = std::min(stages, 8);
     if (stages < 2) return fail(c, LIC_EINVAL, "layer does not fit shared memory");
     P.stages = stages;
     P.off_gamma = stages * P.stage_bytes;
-    P.off_xsq = P.off_gamma + (gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0);
-    P.off_bar = P.off_xsq + (gdn ? 2 * a_bytes : 0);
-    P.smem_bytes = P.off_bar + (2 * stages + 8) * 8 + 1024;
+    P.off_bar = P.off_gamma + gamma_bytes;
+    P.off_par = P.off_bar + 256;
+    P.smem_bytes = P.off_par + par_bytes + 1024;
     if (P.smem_bytes < 120 * 1024) P.smem_bytes = 120 * 1024;     // one CTA per SM (TMEM)
     // TMEM plan: accumulator (+ GDN norm) per buffer, double-buffered when it fits
     int per = std::max(32, P.BN) + (gdn ? P.BN : 0);
@@ -338,7 +351,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.tmem_cols = pow2_cols(P.n_accbuf * per);
     P.L = c->L;
     // tensor maps
-    const int ntaps_w = gemm_l1 ? 1 : Ly.k * Ly.k;
+    const int ntaps_w = gemm_l1 ? 1 : (P.pack4 ? 9 : Ly.k * Ly.k);
     const int cout_pad = P.BN * P.n_ntiles;
     if (!encode_act_map(&Ly.mapA, Ly.in_buf, P.Cin, Ly.deconv ? Ly.Win : (gemm_l1 ? Ly.Wout : Ly.Win),
                         Ly.deconv ? Ly.Hin : (gemm_l1 ? Ly.Hout : Ly.Hin), c->max_batch, P.split, Ly.in_plane,
@@ -578,10 +591,24 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
         const std::vector<float>& w = blk[wn + ".w"];
         int bn = d.cout <= 256 ? (d.cout + 15) / 16 * 16 : 0;
         if (!bn) { int nt = (d.cout + 255) / 256; bn = ((d.cout + nt - 1) / nt + 15) / 16 * 16 * nt; }
-        const int cout_pad = bn;
-        const int taps = d.id == GA1 ? 1 : d.k * d.k;
+        const bool pack4 = d.id == GS4;
+        const int cout_pad = pack4 ? 16 : bn;
+        const int taps = d.id == GA1 ? 1 : (pack4 ? 9 : d.k * d.k);
         std::vector<__half> wp((size_t)taps * cout_pad * Ly.Cin_eff, __float2half(0.0f));
-        for (int co = 0; co < d.cout; ++co)
+        if (pack4) {
+            for (int t = 0; t < 9; ++t) {
+                const int dy = t / 3 - 1, dx = t % 3 - 1;
+                for (int ph = 0; ph < 4; ++ph) {
+                    const int ky = (ph >> 1) + 2 - 2 * dy, kx = (ph & 1) + 2 - 2 * dx;
+                    if (ky < 0 || ky > 4 || kx < 0 || kx > 4) continue;
+                    for (int co = 0; co < 3; ++co)
+                        for (int ci = 0; ci < d.cin; ++ci)
+                            wp[((size_t)t * 16 + ph * 4 + co) * Ly.Cin_eff + ci] =
+                                __float2half_rn(w[(((size_t)co * d.cin + ci) * 5 + ky) * 5 + kx]);
+                }
+            }
+        }
+        for (int co = 0; co < d.cout && !pack4; ++co)
             for (int ci = 0; ci < d.cin; ++ci)
                 for (int ky = 0; ky < d.k; ++ky)
                     for (int kx = 0; kx < d.k; ++kx) {

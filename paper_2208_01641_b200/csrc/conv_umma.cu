@@ -6,19 +6,24 @@
 //   conv   : out[co][oy][ox] = b[co] + sum W[co][ci][ky][kx] in[ci][s*oy+ky-p][s*ox+kx-p]
 //   deconv : stride-2 transposed conv (output_padding 1) as 4 sub-pixel phase GEMMs
 //            out[co][2qy+py][2qx+px] = b[co] + sum_{taps of phase} W[..][ky][kx] in[ci][qy+dy][qx+dx]
-// then one of the EpKind epilogues (GDN per SPEC.md:66 as a second tcgen05 MMA of the
-// squared activations against gamma, then rsqrt/sqrt in fp32; quantise per SPEC.md:194;
-// sigma -> index per SPEC.md:181-189; clamp per SPEC.md:265).
+// then one of the EpKind epilogues: GDN / IGDN as a second tcgen05 MMA of the
+// squared activations against gamma followed by rsqrt / sqrt in fp32; quantise;
+// sigma -> index; clamp + crop.
 //
-// Data layout: activations NHWC fp16, as two planes hi = fp16(x), lo = fp16(x - hi)
-// (DESIGN.md "split-FP16"); weights W[tap][co][ci] fp16 (exact: generator rounds them).
-// Each pipeline stage carries one (tap, 64-channel chunk): A_hi, A_lo (128 px x 64 ch,
-// loaded by a strided 5-D TMA box so the stride-2 gather and the zero padding are done by
-// the TMA unit) and B (BN x 64).  Two MMAs per 16-wide K step (hi, lo) accumulate into the
-// same fp32 TMEM accumulator.
+// Data layout: activations NHWC fp16 as two planes hi = fp16(x), lo = fp16(x - hi)
+// (R16); weights W[tap][co][ci] fp16 (exact).  Each pipeline stage carries one
+// (tap, 64-channel chunk): A_hi, A_lo (128 px x 64 ch from a strided 5-D TMA box: the
+// stride-2 gather and the zero padding are done by the TMA unit) and B (BN x 64).  Two
+// MMAs per 16-wide K step (hi, lo) accumulate into one fp32 TMEM accumulator.
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w3 idle, w4-7 epilogue (TMEM lanes 0-127 = the tile's 128 pixels).
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w3 idle,
+// w4-11 epilogue: warp w reads TMEM lanes 32*(w%4).. (= 32 of the tile's 128 pixels) and
+// group (w-4)/4 owns one half of the output channels.
+//
+// GDN epilogue: each thread keeps x = acc + b for its half of the channels in registers,
+// writes x^2 as fp16 hi/lo back into its own accumulator columns (tcgen05.st), and one
+// thread issues norm = x^2 . gamma^T with the A operand read from TMEM (TS MMA) into the
+// buffer's norm columns; then y = x * rsqrt(beta + norm) (GDN) or x * sqrt(..) (IGDN).
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -28,54 +33,55 @@
 
 namespace lic {
 
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+
 struct TileCoord { int b, ph, gy0, gx0, nt; };
 
+// Tile order: sub-pixel phase fastest, then N tile, x, y, frame -- the 4 phase tiles (and
+// the N tiles) of one location run on neighbouring CTAs and share their input via L2.
 __device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t) {
     TileCoord c;
+    c.ph = t % p.nphase;    t /= p.nphase;
     c.nt = t % p.n_ntiles;  t /= p.n_ntiles;
     int tx = t % p.tiles_x; t /= p.tiles_x;
-    int ty = t % p.tiles_y; t /= p.tiles_y;
-    c.ph = t % p.nphase;
-    c.b = t / p.nphase;
+    int ty = t % p.tiles_y;
+    c.b = t / p.tiles_y;
     c.gx0 = tx * p.Wt;
     c.gy0 = ty * p.Ht;
     return c;
 }
 
+__device__ __forceinline__ uint32_t h2_bits(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float hround(float v) { return __half2float(__float2half_rn(v)); }
+
 // 8 consecutive channels -> one 16-byte fp16 hi vector (+ one lo vector)
 __device__ __forceinline__ void split_store8(__half* hi, __half* lo, const float* v) {
-    __align__(16) __half h[8];
-    __align__(16) __half l[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        h[i] = __float2half_rn(v[i]);
-        l[i] = __float2half_rn(v[i] - __half2float(h[i]));
-    }
-    *reinterpret_cast<uint4*>(hi) = *reinterpret_cast<const uint4*>(h);
-    if (lo) *reinterpret_cast<uint4*>(lo) = *reinterpret_cast<const uint4*>(l);
-}
-
-// write 32 consecutive channels of one pixel's fp32 values into the swizzled x^2 tile
-// (K-major, 128-byte rows, SW128: 16-byte chunk j of row r lives at chunk j ^ (r & 7))
-__device__ __forceinline__ void xsq_store32(uint8_t* tile, int row, int col0, const float* v) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        __align__(16) __half h[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) h[i] = __float2half_rn(v[q * 8 + i]);
-        int chunk = ((col0 >> 3) + q) ^ (row & 7);
-        *reinterpret_cast<uint4*>(tile + row * 128 + chunk * 16) = *reinterpret_cast<const uint4*>(h);
+    uint4 h, l;
+    h.x = h2_bits(v[0], v[1]); h.y = h2_bits(v[2], v[3]); h.z = h2_bits(v[4], v[5]); h.w = h2_bits(v[6], v[7]);
+    *reinterpret_cast<uint4*>(hi) = h;
+    if (lo) {
+        l.x = h2_bits(v[0] - hround(v[0]), v[1] - hround(v[1]));
+        l.y = h2_bits(v[2] - hround(v[2]), v[3] - hround(v[3]));
+        l.z = h2_bits(v[4] - hround(v[4]), v[5] - hround(v[5]));
+        l.w = h2_bits(v[6] - hround(v[6]), v[7] - hround(v[7]));
+        *reinterpret_cast<uint4*>(lo) = l;
     }
 }
 
 __device__ __forceinline__ int round_clamp(float v, int L, int& sat) {
-    float r = roundf(v);                 // half away from zero
+    float r = roundf(v);                 // half away from zero (R4)
     if (r > (float)L) { r = (float)L; ++sat; }
     if (r < (float)-L) { r = (float)-L; ++sat; }
     return (int)r;
 }
 
-__global__ void __launch_bounds__(256, 1)
+// GC: GDN/IGDN layers only -- 32-column chunks per epilogue group (BN = 64*GC); 0 otherwise
+template <int GC>
+__global__ void __launch_bounds__(kThreads, 1)
 conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                  const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ CUtensorMap mapG,
@@ -91,15 +97,18 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     uint64_t* norm_bar = tempty_bar + 2;
     uint64_t* gamma_bar = norm_bar + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gamma_bar + 1);
+    float* s_bias = reinterpret_cast<float*>(smem + p.off_par);   // [cout_pad]
+    float* s_beta = s_bias + p.BN * p.n_ntiles;                     // [cout_pad]
+    float* s_mu = s_beta + p.BN * p.n_ntiles;                       // [cout_pad]
+    float* s_tab = s_mu + p.BN * p.n_ntiles;                        // [64]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const bool gdn = (p.ep == EP_GDN || p.ep == EP_IGDN);
-    const int nchunk_out = p.BN / 64;               // GDN: BN == Cout, multiple of 64
+    constexpr bool kGdn = GC > 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], 4); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], kEpiWarps); }
         mbar_init(norm_bar, 1);
         mbar_init(gamma_bar, 1);
         fence_mbar_init();
@@ -107,9 +116,20 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&mapA);
         tma_prefetch_desc(&mapB);
-        if (gdn) tma_prefetch_desc(&mapG);
+        if (kGdn) tma_prefetch_desc(&mapG);
     }
     if (warp == 2) tmem_alloc(tmem_slot, (uint32_t)p.tmem_cols);
+    if (warp >= 4) {
+        // per-channel epilogue constants, staged once per CTA
+        const int np = p.BN * p.n_ntiles;
+        for (int i = threadIdx.x - 128; i < np; i += 32 * kEpiWarps) {
+            const bool in = i < p.Cout;
+            s_bias[i] = in ? p.bias[i] : 0.0f;
+            s_beta[i] = (in && p.beta) ? p.beta[i] : 0.0f;
+            s_mu[i] = (in && p.mu) ? p.mu[i] : 0.0f;
+        }
+        for (int i = threadIdx.x - 128; i < 64; i += 32 * kEpiWarps) s_tab[i] = p.table ? p.table[i] : 0.0f;
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -122,9 +142,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     if (warp == 0) {
         // ====================== TMA producer ======================
         if (lane == 0) {
-            if (gdn) {
-                mbar_arrive_expect_tx(gamma_bar, (uint32_t)nchunk_out * b_bytes);
-                for (int c = 0; c < nchunk_out; ++c)
+            if (kGdn) {
+                // gamma (Cout x Cout fp16, K-major rows; BN/64 = GC chunks of 64 columns)
+                // resident for the whole launch
+                mbar_arrive_expect_tx(gamma_bar, (uint32_t)GC * b_bytes);
+                for (int c = 0; c < GC; ++c)
                     tma_load_3d(smem + p.off_gamma + c * b_bytes, &mapG, gamma_bar, c * kBK, 0, 0);
             }
             int stage = 0;
@@ -185,9 +207,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         }
     } else if (warp >= 4) {
         // ====================== epilogue ======================
-        const int e = threadIdx.x - 128;            // 0..127 = TMEM lane = pixel row of the tile
-        const int ew = warp - 4;                    // == warp % 4 -> TMEM lanes 32*ew ..
-        const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+        const int q = warp & 3;                     // TMEM lane quadrant
+        const int g = (warp - 4) >> 2;              // channel half
+        const int r = q * 32 + lane;                // tile row (pixel) of this thread
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         uint32_t norm_phase = 0;
         bool gamma_ready = false;
         int it = 0;
@@ -201,173 +224,191 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const uint32_t dcol = (uint32_t)(buf * p.acc_stride);
             const uint32_t taddr = tmem_base + lane_off + dcol;
 
-            const int gy = tc.gy0 + e / p.Wt, gx = tc.gx0 + e % p.Wt;
+            const int gy = tc.gy0 + r / p.Wt, gx = tc.gx0 + r % p.Wt;
             const bool valid = (gy < p.Hg) && (gx < p.Wg);
             const int py = (p.nphase == 4) ? (tc.ph >> 1) : 0;
             const int px = (p.nphase == 4) ? (tc.ph & 1) : 0;
             const int oy = p.out_s * gy + py, ox = p.out_s * gx + px;
             const size_t pix = ((size_t)tc.b * p.Hout + oy) * p.Wout + ox;
             const size_t HWo = (size_t)p.Hout * p.Wout;
+            const size_t chw0 = (size_t)tc.b * p.Cout * HWo + (size_t)oy * p.Wout + ox;
             const int co0 = tc.nt * p.BN;
 
-            if (gdn) {
-                // ---- norm = x^2 . gamma^T as a second MMA (K = Cout, split hi/lo) ----
-                uint8_t* xh = smem + p.off_xsq;
-                uint8_t* xl = xh + a_bytes;
-                const uint32_t ncol = dcol + (uint32_t)p.BN;     // norm accumulator columns
-                for (int c = 0; c < nchunk_out; ++c) {
-                    float v[32], hi[32], lo[32];
-                    if (c > 0) { mbar_wait(norm_bar, norm_phase); norm_phase ^= 1; }
+            if constexpr (kGdn) {
+                constexpr int G = 32 * GC;                   // channels of this group
+                float x[GC][32];
 #pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-                        __syncwarp();
-                        tmem_ld32(taddr + c * 64 + half * 32, v);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            float x = v[j] + __ldg(&p.bias[co0 + c * 64 + half * 32 + j]);
-                            float x2 = x * x;
-                            __half h = __float2half_rn(x2);
-                            hi[j] = __half2float(h);
-                            lo[j] = x2 - hi[j];
-                        }
-                        xsq_store32(xh, e, half * 32, hi);
-                        xsq_store32(xl, e, half * 32, lo);
-                    }
-                    fence_proxy_async_smem();
-                    named_bar_sync(1, 128);
-                    if (e == 0) {
-                        if (!gamma_ready) { mbar_wait(gamma_bar, 0); gamma_ready = true; }
-                        tc_fence_after();
-                        const uint64_t dh = sdesc_sw128(smem_u32(xh));
-                        const uint64_t dl = sdesc_sw128(smem_u32(xl));
-                        const uint64_t dg = sdesc_sw128(smem_u32(smem + p.off_gamma + c * b_bytes));
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            umma_f16(tmem_base + ncol, dh + 2 * kk, dg + 2 * kk, idesc, (c | kk) != 0);
-                            umma_f16(tmem_base + ncol, dl + 2 * kk, dg + 2 * kk, idesc, 1u);
-                        }
-                        umma_commit(norm_bar);
-                    }
+                for (int j = 0; j < GC; ++j) {
+                    __syncwarp();
+                    tmem_ld32(taddr + g * G + j * 32, x[j]);
                 }
-                mbar_wait(norm_bar, norm_phase); norm_phase ^= 1;
+                // x^2 (hi, lo) packed into this group's own accumulator columns:
+                // hi of channel g*G + k at column g*G + k/2, lo at g*G + G/2 + k/2
+#pragma unroll
+                for (int j = 0; j < GC; ++j) {
+                    uint32_t hi[16], lo[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int c0 = g * G + j * 32 + 2 * i;
+                        const float a = x[j][2 * i] + s_bias[c0], b = x[j][2 * i + 1] + s_bias[c0 + 1];
+                        x[j][2 * i] = a;
+                        x[j][2 * i + 1] = b;
+                        const float a2 = a * a, b2 = b * b;
+                        hi[i] = h2_bits(a2, b2);
+                        lo[i] = h2_bits(a2 - hround(a2), b2 - hround(b2));
+                    }
+                    tmem_st16(taddr + g * G + j * 16, hi);
+                    tmem_st16(taddr + g * G + G / 2 + j * 16, lo);
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                named_bar_sync(1, 32 * kEpiWarps);
+                if (threadIdx.x == 128) {
+                    if (!gamma_ready) { mbar_wait(gamma_bar, 0); gamma_ready = true; }
+                    tc_fence_after();
+                    const uint32_t ncol = tmem_base + dcol + (uint32_t)p.BN;
+                    const uint32_t gbase = smem_u32(smem + p.off_gamma);
+#pragma unroll
+                    for (int kk = 0; kk < 4 * GC; ++kk) {           // K = BN in steps of 16
+                        const int k0 = 16 * kk, gg = k0 / G, o = k0 - gg * G;
+                        const uint32_t ahi = tmem_base + dcol + gg * G + o / 2;
+                        const uint32_t alo = ahi + G / 2;
+                        const uint64_t bd = sdesc_sw128(gbase + (k0 / 64) * b_bytes) + 2 * (kk & 3);
+                        umma_f16_ts(ncol, ahi, bd, idesc, kk != 0);
+                        umma_f16_ts(ncol, alo, bd, idesc, 1u);
+                    }
+                    umma_commit(norm_bar);
+                }
+                mbar_wait(norm_bar, norm_phase);
+                norm_phase ^= 1;
                 tc_fence_after();
                 __half* out = reinterpret_cast<__half*>(p.out_act);
-                for (int c = 0; c < p.BN / 32; ++c) {
-                    float v[32], n[32];
-                    __syncwarp();
-                    tmem_ld32(taddr + c * 32, v);
-                    tmem_ld32(taddr + p.BN + c * 32, n);
-                    if (valid) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int co = c * 32 + j;
-                            float x = v[j] + __ldg(&p.bias[co]);
-                            float nn = __ldg(&p.beta[co]) + n[j];
-                            v[j] = (p.ep == EP_GDN) ? x * rsqrtf(nn) : x * sqrtf(nn);
-                        }
+                for (int j = 0; j < GC; ++j) {
+                    float n[32];
+                    __syncwarp();
+                    tmem_ld32(taddr + p.BN + g * G + j * 32, n);
+                    const int cb = g * G + j * 32;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float nn = s_beta[cb + i] + n[i];
+                        x[j][i] = (p.ep == EP_GDN) ? x[j][i] * rsqrtf(nn) : x[j][i] * sqrtf(nn);
+                    }
+                    if (valid) {
                         if (p.out_f32) {
 #pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                p.out_f32[((size_t)tc.b * p.Cout + c * 32 + j) * HWo + (size_t)oy * p.Wout + ox] = v[j];
+                            for (int i = 0; i < 32; ++i) p.out_f32[chw0 + (size_t)(cb + i) * HWo] = x[j][i];
                         }
                         if (out) {
 #pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                split_store8(out + pix * p.Cout + c * 32 + q * 8,
-                                             p.split == 2 ? out + p.act_plane + pix * p.Cout + c * 32 + q * 8 : nullptr,
-                                             v + q * 8);
+                            for (int qq = 0; qq < 4; ++qq)
+                                split_store8(out + pix * p.Cout + cb + qq * 8,
+                                             p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + qq * 8 : nullptr,
+                                             x[j] + qq * 8);
                         }
                     }
                 }
             } else {
                 const int ncol32 = (p.BN + 31) / 32;
-                for (int c = 0; c < ncol32; ++c) {
+                for (int c = g; c < ncol32; c += 2) {
                     float v[32];
                     __syncwarp();
                     tmem_ld32(taddr + c * 32, v);
                     const int cb = co0 + c * 32;
                     if (valid && cb < p.Cout) {
-                    const int nj = min(32, p.Cout - cb);
+                        const int nj = p.pack4 ? 16 : min(32, p.Cout - cb);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (j < nj) v[j] += __ldg(&p.bias[cb + j]);
-                    switch (p.ep) {
-                    case EP_F32: {
-                        for (int j = 0; j < nj; ++j)
-                            p.out_f32[((size_t)tc.b * p.Cout + cb + j) * HWo + (size_t)oy * p.Wout + ox] = v[j];
-                        break;
-                    }
-                    case EP_RELU: {
-                        __half* out = reinterpret_cast<__half*>(p.out_act);
+                        for (int j = 0; j < 32; ++j) v[j] += s_bias[p.pack4 ? (j & 3) : cb + j];
+                        switch (p.ep) {
+                        case EP_F32: {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
-                        if (p.out_f32)
-                            for (int j = 0; j < nj; ++j)
-                                p.out_f32[((size_t)tc.b * p.Cout + cb + j) * HWo + (size_t)oy * p.Wout + ox] = v[j];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            split_store8(out + pix * p.Cout + cb + q * 8,
-                                         p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + q * 8 : nullptr,
-                                         v + q * 8);
-                        break;
-                    }
-                    case EP_YQUANT:
-                    case EP_ZQUANT: {
-                        int8_t* sym = reinterpret_cast<int8_t*>(p.out_sym);
-                        float av[32];
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            float m = (p.mu && j < nj) ? __ldg(&p.mu[cb + j]) : 0.0f;
-                            int s = (j < nj) ? round_clamp(v[j] - m, p.L, sat) : 0;
-                            if (j < nj) sym[((size_t)tc.b * p.Cout + cb + j) * HWo + (size_t)oy * p.Wout + ox] = (int8_t)s;
-                            av[j] = (p.ep == EP_YQUANT) ? fabsf(v[j]) : (float)s + m;
+                            for (int j = 0; j < 32; ++j)
+                                if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
+                            break;
                         }
-                        if (p.out_f32)
-                            for (int j = 0; j < nj; ++j)
-                                p.out_f32[((size_t)tc.b * p.Cout + cb + j) * HWo + (size_t)oy * p.Wout + ox] = v[j];
-                        if (p.out_act && (p.ep == EP_ZQUANT || p.abs_out)) {
+                        case EP_RELU: {
                             __half* out = reinterpret_cast<__half*>(p.out_act);
 #pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                split_store8(out + pix * p.Cout + cb + q * 8,
-                                             p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + q * 8 : nullptr,
-                                             av + q * 8);
-                        }
-                        break;
-                    }
-                    case EP_SIGMA: {
-                        uint8_t* idx = reinterpret_cast<uint8_t*>(p.out_sym);
-                        for (int j = 0; j < nj; ++j) {
-                            float s = fmaxf(v[j], 0.0f);
-                            if (p.out_f32)
-                                p.out_f32[((size_t)tc.b * p.Cout + cb + j) * HWo + (size_t)oy * p.Wout + ox] = s;
-                            s = fmaxf(s, 0.11f);
-                            // #{ j in [0, 62] : table_j < s } by binary search over the sorted table
-                            int lo_i = 0, hi_i = 63;
-                            while (lo_i < hi_i) {
-                                int mid = (lo_i + hi_i) >> 1;
-                                if (__ldg(&p.table[mid]) < s) lo_i = mid + 1; else hi_i = mid;
+                            for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+                            if (p.out_f32) {
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
                             }
-                            idx[((size_t)tc.b * p.Cout + cb + j) * HWo + (size_t)oy * p.Wout + ox] = (uint8_t)lo_i;
+#pragma unroll
+                            for (int qq = 0; qq < 4; ++qq)
+                                split_store8(out + pix * p.Cout + cb + qq * 8,
+                                             p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + qq * 8 : nullptr,
+                                             v + qq * 8);
+                            break;
                         }
-                        break;
-                    }
-                    case EP_FINAL: {
-                        const int ry = oy - p.crop_top, rx = ox - p.crop_left;
-                        if (ry < 0 || ry >= p.crop_H || rx < 0 || rx >= p.crop_W) break;
-                        for (int j = 0; j < nj; ++j) {
-                            float xv = fminf(fmaxf(v[j], 0.0f), 1.0f);
-                            const int ch = cb + j;
-                            if (p.out_f32)
-                                p.out_f32[(((size_t)tc.b * p.Cout + ch) * p.crop_H + ry) * p.crop_W + rx] = xv;
-                            if (p.out_u8)
-                                p.out_u8[(((size_t)tc.b * p.crop_H + ry) * p.crop_W + rx) * 3 + ch] =
-                                    (uint8_t)roundf(xv * 255.0f);
+                        case EP_YQUANT:
+                        case EP_ZQUANT: {
+                            int8_t* sym = reinterpret_cast<int8_t*>(p.out_sym);
+                            float av[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                const float m = s_mu[cb + j];
+                                const int s = (j < nj) ? round_clamp(v[j] - m, p.L, sat) : 0;
+                                if (j < nj) sym[chw0 + (size_t)(cb + j) * HWo] = (int8_t)s;
+                                av[j] = (p.ep == EP_YQUANT) ? fabsf(v[j]) : (float)s + m;
+                            }
+                            if (p.out_f32) {
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
+                            }
+                            if (p.out_act && (p.ep == EP_ZQUANT || p.abs_out)) {
+                                __half* out = reinterpret_cast<__half*>(p.out_act);
+#pragma unroll
+                                for (int qq = 0; qq < 4; ++qq)
+                                    split_store8(out + pix * p.Cout + cb + qq * 8,
+                                                 p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + qq * 8 : nullptr,
+                                                 av + qq * 8);
+                            }
+                            break;
                         }
-                        break;
-                    }
-                    default: break;
-                    }
+                        case EP_SIGMA: {
+                            uint8_t* idx = reinterpret_cast<uint8_t*>(p.out_sym);
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                if (j >= nj) continue;
+                                float s = fmaxf(v[j], 0.0f);
+                                if (p.out_f32) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = s;
+                                s = fmaxf(s, 0.11f);
+                                // #{ j in [0, 62] : table_j < s }: binary search over the sorted table
+                                int lo_i = 0, hi_i = 63;
+#pragma unroll
+                                for (int step = 0; step < 6; ++step) {
+                                    const int mid = (lo_i + hi_i) >> 1;
+                                    if (s_tab[mid] < s) lo_i = mid + 1; else hi_i = mid;
+                                }
+                                idx[chw0 + (size_t)(cb + j) * HWo] = (uint8_t)lo_i;
+                            }
+                            break;
+                        }
+                        case EP_FINAL: {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                if (j >= nj) continue;
+                                // packed phases: column j -> sub-pixel (j>>2) of grid pixel (gy, gx), channel j&3
+                                const int ch = p.pack4 ? (j & 3) : cb + j;
+                                if (p.pack4 && ch >= 3) continue;
+                                const int yy = p.pack4 ? 2 * gy + ((j >> 3) & 1) : oy;
+                                const int xx = p.pack4 ? 2 * gx + ((j >> 2) & 1) : ox;
+                                const int ry = yy - p.crop_top, rx = xx - p.crop_left;
+                                if (ry < 0 || ry >= p.crop_H || rx < 0 || rx >= p.crop_W) continue;
+                                const float xv = fminf(fmaxf(v[j], 0.0f), 1.0f);
+                                if (p.out_f32)
+                                    p.out_f32[(((size_t)tc.b * 3 + ch) * p.crop_H + ry) * p.crop_W + rx] = xv;
+                                if (p.out_u8)
+                                    p.out_u8[(((size_t)tc.b * p.crop_H + ry) * p.crop_W + rx) * 3 + ch] =
+                                        (uint8_t)roundf(xv * 255.0f);
+                            }
+                            break;
+                        }
+                        default: break;
+                        }
                     }
                 }
             }
@@ -389,17 +430,29 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     }
 }
 
-cudaError_t launch_conv_umma(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
-                             const ConvParams& p, int grid, cudaStream_t stream) {
+template <int GC>
+static cudaError_t launch_t(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
+                            const ConvParams& p, int grid, cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    conv_umma_kernel<<<grid, 256, p.smem_bytes, stream>>>(mapA, mapB, mapG, p);
+    conv_umma_kernel<GC><<<grid, kThreads, p.smem_bytes, stream>>>(mapA, mapB, mapG, p);
     return cudaGetLastError();
+}
+
+cudaError_t launch_conv_umma(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
+                             const ConvParams& p, int grid, cudaStream_t stream) {
+    const bool gdn = (p.ep == EP_GDN || p.ep == EP_IGDN);
+    if (!gdn) return launch_t<0>(mapA, mapB, mapG, p, grid, stream);
+    switch (p.BN) {      // GDN channel counts of the configs: N = 128, 192
+    case 128: return launch_t<2>(mapA, mapB, mapG, p, grid, stream);
+    case 192: return launch_t<3>(mapA, mapB, mapG, p, grid, stream);
+    default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace lic

@@ -146,3 +146,141 @@ extern "C" lic_status lic_rans_decode(const uint8_t* in, size_t len, const uint8
     if (x != kRansLow || pos != len) return LIC_ECORRUPT;
     return LIC_OK;
 }
+
+// ------------------------------------------------------------------ prepared tables
+// Encoder: x' = (x / f << 16) + x % f + start = x + start + q * (2^16 - f) with q = x / f
+// computed exactly as mulhi(x, rcp) >> shift (x < 2^31 after renormalisation); f = 1 uses
+// rcp = 2^32 - 1, shift 0, bias start + 2^16 - 1, which gives q = x - 1 and the same x'.
+struct EncSym {
+    uint32_t xmax;       // renormalise while x >= xmax
+    uint32_t rcp;        // reciprocal of freq
+    uint32_t bias;       // start (or start + 2^16 - 1 for freq == 1)
+    uint16_t cmpl;       // 2^16 - freq
+    uint16_t shift;      // reciprocal shift
+};
+
+struct lic_rans_tables {
+    uint32_t n_rows = 0, row_len = 0, nsym = 0;
+    int sym_min = 0;
+    std::vector<uint32_t> cdf;
+    std::vector<EncSym> enc;        // n_rows x nsym
+    std::vector<uint8_t> bucket;    // n_rows x 4096: symbol holding slot (u << 4)
+};
+
+extern "C" lic_status lic_rans_prepare(const uint32_t* cdf, uint32_t n_rows, uint32_t row_len, int sym_min,
+                                       lic_rans_tables** out) {
+    if (!cdf || !out || n_rows == 0 || row_len < 2 || row_len > 257) return LIC_EINVAL;
+    auto* t = new lic_rans_tables();
+    t->n_rows = n_rows; t->row_len = row_len; t->nsym = row_len - 1; t->sym_min = sym_min;
+    t->cdf.assign(cdf, cdf + (size_t)n_rows * row_len);
+    t->enc.resize((size_t)n_rows * t->nsym);
+    t->bucket.resize((size_t)n_rows * 4096);
+    for (uint32_t r = 0; r < n_rows; ++r) {
+        const uint32_t* c = &t->cdf[(size_t)r * row_len];
+        if (c[0] != 0 || c[t->nsym] != kProbScale) { delete t; return LIC_EINVAL; }
+        for (uint32_t s = 0; s < t->nsym; ++s) {
+            if (c[s + 1] < c[s]) { delete t; return LIC_EINVAL; }
+            const uint32_t start = c[s], freq = c[s + 1] - c[s];
+            EncSym& e = t->enc[(size_t)r * t->nsym + s];
+            e.xmax = ((kRansLow >> kProbBits) << 8) * freq;
+            e.cmpl = (uint16_t)((kProbScale - freq) & 0xFFFF);
+            if (freq < 2) {
+                e.rcp = ~0u; e.shift = 0; e.bias = start + kProbScale - 1;
+            } else {
+                uint32_t sh = 0;
+                while (freq > (1u << sh)) ++sh;
+                e.rcp = (uint32_t)(((1ull << (sh + 31)) + freq - 1) / freq);
+                e.shift = (uint16_t)(sh - 1);
+                e.bias = start;
+            }
+        }
+        uint32_t s = 0;
+        for (uint32_t u = 0; u < 4096; ++u) {
+            const uint32_t slot = u << 4;
+            while (c[s + 1] <= slot) ++s;
+            t->bucket[(size_t)r * 4096 + u] = (uint8_t)s;
+        }
+    }
+    *out = t;
+    return LIC_OK;
+}
+
+extern "C" void lic_rans_tables_free(lic_rans_tables* t) { delete t; }
+
+extern "C" lic_status lic_rans_encode_fast(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row,
+                                           lic_shape plane, uint8_t* out, size_t cap, size_t* out_len) {
+    if (!t || !out || !out_len) return LIC_EINVAL;
+    const size_t hw = (size_t)plane.h * plane.w;
+    const size_t n = hw * plane.c;
+    if (n && !sym) return LIC_EINVAL;
+    const EncSym* enc = t->enc.data();
+    const uint32_t nsym = t->nsym, nrows = t->n_rows;
+    const int smin = t->sym_min;
+    uint8_t* ptr = out + cap;
+    uint32_t x = kRansLow;
+    size_t i = n;
+    // channel-row planes: iterate channel by channel so the row lookup is hoisted
+    while (i > 0) {
+        const size_t seg_end = i;
+        const size_t seg_begin = row ? 0 : ((i - 1) / (hw ? hw : 1)) * (hw ? hw : 1);
+        const uint32_t crow = row ? 0 : (uint32_t)((i - 1) / (hw ? hw : 1));
+        if (!row && crow >= nrows) return LIC_EINVAL;
+        for (size_t j = seg_end; j-- > seg_begin;) {
+            const uint32_t r = row ? row[j] : crow;
+            const int s = (int)sym[j] - smin;
+            if (r >= nrows || (unsigned)s >= nsym) return LIC_EINVAL;
+            const EncSym& e = enc[(size_t)r * nsym + s];
+            if (e.xmax == 0) return LIC_EINVAL;
+            while (x >= e.xmax) {
+                if (ptr == out) return LIC_ENOSPACE;
+                *--ptr = (uint8_t)x;
+                x >>= 8;
+            }
+            const uint32_t q = (uint32_t)(((uint64_t)x * e.rcp) >> 32) >> e.shift;
+            x = x + e.bias + q * (uint32_t)e.cmpl;
+        }
+        i = seg_begin;
+    }
+    if ((size_t)(ptr - out) < 4) return LIC_ENOSPACE;
+    *--ptr = (uint8_t)x;
+    *--ptr = (uint8_t)(x >> 8);
+    *--ptr = (uint8_t)(x >> 16);
+    *--ptr = (uint8_t)(x >> 24);
+    const size_t len = (size_t)(out + cap - ptr);
+    if (ptr != out) std::memmove(out, ptr, len);
+    *out_len = len;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_rans_decode_fast(const lic_rans_tables* t, const uint8_t* in, size_t len,
+                                           const uint8_t* row, lic_shape plane, int8_t* sym_out) {
+    if (!t) return LIC_EINVAL;
+    if (!in || len < 4) return LIC_ECORRUPT;
+    const size_t hw = (size_t)plane.h * plane.w;
+    const size_t n = hw * plane.c;
+    if (n && !sym_out) return LIC_EINVAL;
+    const uint32_t* cdf = t->cdf.data();
+    const uint8_t* bucket = t->bucket.data();
+    const uint32_t rl = t->row_len, nrows = t->n_rows;
+    const int smin = t->sym_min;
+    uint32_t x = ((uint32_t)in[0] << 24) | ((uint32_t)in[1] << 16) | ((uint32_t)in[2] << 8) | in[3];
+    const uint8_t* p = in + 4;
+    const uint8_t* end = in + len;
+    for (size_t i = 0; i < n; ++i) {
+        const uint32_t r = row ? row[i] : (uint32_t)(i / hw);
+        if (r >= nrows) return LIC_EINVAL;
+        const uint32_t* c = cdf + (size_t)r * rl;
+        const uint32_t slot = x & (kProbScale - 1);
+        uint32_t s = bucket[(size_t)r * 4096 + (slot >> 4)];
+        while (c[s + 1] <= slot) ++s;        // c[nsym] = 2^16 > slot terminates the scan
+        const uint32_t start = c[s], freq = c[s + 1] - start;
+        x = freq * (x >> kProbBits) + slot - start;
+        while (x < kRansLow) {
+            if (p >= end) return LIC_ECORRUPT;
+            x = (x << 8) | *p++;
+        }
+        sym_out[i] = (int8_t)((int)s + smin);
+    }
+    if (x != kRansLow || p != end) return LIC_ECORRUPT;
+    return LIC_OK;
+}

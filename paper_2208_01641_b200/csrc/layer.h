@@ -43,7 +43,7 @@ struct ConvParams {
     int total_tiles;
     // ---- kernel resources (host-computed)
     int stages;
-    uint32_t stage_bytes, off_gamma, off_xsq, off_bar, smem_bytes;
+    uint32_t stage_bytes, off_gamma, off_bar, off_par, smem_bytes;
     int tmem_cols, acc_stride, n_accbuf;
     // ---- epilogue
     int ep;
@@ -59,6 +59,8 @@ struct ConvParams {
     float* out_f32;                   // f32 [batch][Cout][Hout or crop_H][Wout or crop_W]
     uint8_t* out_u8;                  // u8 [batch][crop_H][crop_W][3]
     int abs_out;                      // EP_YQUANT: also write |y| planes
+    int pack4;                        // EP_FINAL of a stride-2 deconv with all 4 sub-pixel
+                                      // phases packed into N: column j = phase (j>>2), channel (j&3)
     int crop_top, crop_left, crop_H, crop_W;
     unsigned long long* sat_count;    // saturation counter (nullable)
 };

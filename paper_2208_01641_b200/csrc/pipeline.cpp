@@ -49,6 +49,7 @@ struct Slot {
 };
 
 struct GpuTask { GpuKind kind; int slot; };
+struct Pending { GpuTask task; cudaEvent_t done; double t_issue; };
 struct CpuTask { CpuKind kind; int slot; int frame; };
 
 }  // namespace
@@ -63,8 +64,13 @@ struct lic_pipeline {
     const uint32_t* cdf_z = nullptr; uint32_t rows_z = 0;
     uint32_t row_len = 0;
     int sym_min = 0;
+    lic_rans_tables* tab_y = nullptr;       // prepared coder tables (lic_rans_prepare)
+    lic_rans_tables* tab_z = nullptr;
     std::vector<Slot> slots;
     std::vector<void*> pinned;
+    cudaStream_t stream = nullptr;          // all GPU stages, in issue order
+    std::vector<cudaEvent_t> events;        // completion events, recycled
+    std::deque<Pending> pending;            // issued, not yet completed (FIFO)
     // threading
     std::mutex mu;
     std::condition_variable cv_gpu, cv_cpu;
@@ -93,24 +99,22 @@ static void coder_task(lic_pipeline* p, const CpuTask& t) {
     uint64_t mism = 0;
     if (t.kind == C_ONE) {
         // encoder CPU workload: E(y) (and E(z)); then decoder CPU1: E^-1(z) (hyper) or E^-1(y)
-        st = lic_rans_encode(s.y_sym + f * p->ny, p->hyper ? s.y_idx + f * p->ny : nullptr, p->ys, p->cdf_y,
-                             p->rows_y, p->row_len, p->sym_min, s.ystr[f].data(), s.ystr[f].size(), &s.ylen[f]);
+        st = lic_rans_encode_fast(p->tab_y, s.y_sym + f * p->ny, p->hyper ? s.y_idx + f * p->ny : nullptr, p->ys,
+                                  s.ystr[f].data(), s.ystr[f].size(), &s.ylen[f]);
         if (!st && p->hyper)
-            st = lic_rans_encode(s.z_sym + f * p->nz, nullptr, p->zs, p->cdf_z, p->rows_z, p->row_len, p->sym_min,
-                                 s.zstr[f].data(), s.zstr[f].size(), &s.zlen[f]);
+            st = lic_rans_encode_fast(p->tab_z, s.z_sym + f * p->nz, nullptr, p->zs, s.zstr[f].data(),
+                                      s.zstr[f].size(), &s.zlen[f]);
         if (!st && p->hyper) {
-            st = lic_rans_decode(s.zstr[f].data(), s.zlen[f], nullptr, p->zs, p->cdf_z, p->rows_z, p->row_len,
-                                 p->sym_min, s.z_dec + f * p->nz);
+            st = lic_rans_decode_fast(p->tab_z, s.zstr[f].data(), s.zlen[f], nullptr, p->zs, s.z_dec + f * p->nz);
             if (!st && std::memcmp(s.z_dec + f * p->nz, s.z_sym + f * p->nz, p->nz) != 0) mism += 1;
         } else if (!st) {
-            st = lic_rans_decode(s.ystr[f].data(), s.ylen[f], nullptr, p->ys, p->cdf_y, p->rows_y, p->row_len,
-                                 p->sym_min, s.y_dec + f * p->ny);
+            st = lic_rans_decode_fast(p->tab_y, s.ystr[f].data(), s.ylen[f], nullptr, p->ys, s.y_dec + f * p->ny);
             if (!st && std::memcmp(s.y_dec + f * p->ny, s.y_sym + f * p->ny, p->ny) != 0) mism += 1;
         }
     } else {
         // decoder CPU2: E^-1(y) with the indexes from decoder GPU1
-        st = lic_rans_decode(s.ystr[f].data(), s.ylen[f], s.idx_dec + f * p->ny, p->ys, p->cdf_y, p->rows_y,
-                             p->row_len, p->sym_min, s.y_dec + f * p->ny);
+        st = lic_rans_decode_fast(p->tab_y, s.ystr[f].data(), s.ylen[f], s.idx_dec + f * p->ny, p->ys,
+                                  s.y_dec + f * p->ny);
         if (!st && std::memcmp(s.y_dec + f * p->ny, s.y_sym + f * p->ny, p->ny) != 0) mism += 1;
     }
     std::lock_guard<std::mutex> g(p->mu);
@@ -151,7 +155,12 @@ extern "C" void lic_pipeline_close(lic_pipeline* p) {
     }
     p->cv_cpu.notify_all();
     for (auto& t : p->workers) t.join();
+    if (p->stream) cudaStreamSynchronize(p->stream);
+    for (cudaEvent_t e : p->events) cudaEventDestroy(e);
+    if (p->stream) cudaStreamDestroy(p->stream);
     for (void* q : p->pinned) cudaFreeHost(q);
+    lic_rans_tables_free(p->tab_y);
+    lic_rans_tables_free(p->tab_z);
     delete p;
 }
 
@@ -179,6 +188,11 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
     }
     p->row_len = rl;
     p->sym_min = -(int)((rl - 2) / 2);
+    if ((st = lic_rans_prepare(p->cdf_y, p->rows_y, rl, p->sym_min, &p->tab_y)) ||
+        (p->hyper && (st = lic_rans_prepare(p->cdf_z, p->rows_z, rl, p->sym_min, &p->tab_z)))) {
+        lic_pipeline_close(p);
+        return st;
+    }
     const size_t B = cfg->batch;
     auto pin = [&](size_t bytes) -> void* {
         void* q = nullptr;
@@ -206,6 +220,18 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
         s.ylen.assign(B, 0);
         s.zlen.assign(B, 0);
     }
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        lic_pipeline_close(p);
+        return LIC_ECUDA;
+    }
+    p->events.resize(8);
+    for (auto& e : p->events)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            lic_pipeline_close(p);
+            return LIC_ECUDA;
+        }
     for (uint32_t i = 0; i < cfg->coder_threads; ++i) p->workers.emplace_back(worker_main, p);
     *out = p;
     return LIC_OK;
@@ -219,16 +245,16 @@ static lic_status gpu_call(lic_pipeline* p, const GpuTask& t) {
     case G_ENC: {
         const uint8_t* fr = p->in + b * B * p->in_bytes;
         return p->cfg.u8 ? lic_encode_u8(p->codec, fr, B, s.y_sym, p->hyper ? s.y_idx : nullptr,
-                                         p->hyper ? s.z_sym : nullptr, nullptr, nullptr)
+                                         p->hyper ? s.z_sym : nullptr, nullptr, p->stream)
                          : lic_encode(p->codec, (const float*)fr, B, s.y_sym, p->hyper ? s.y_idx : nullptr,
-                                      p->hyper ? s.z_sym : nullptr, nullptr, nullptr);
+                                      p->hyper ? s.z_sym : nullptr, nullptr, p->stream);
     }
     case G_IDX:
-        return lic_hyper_indexes(p->codec, s.z_dec, B, s.idx_dec, nullptr);
+        return lic_hyper_indexes(p->codec, s.z_dec, B, s.idx_dec, p->stream);
     case G_DEC: {
         uint8_t* fr = p->out + b * B * p->out_bytes;
-        return p->cfg.u8 ? lic_decode_u8(p->codec, s.y_dec, B, fr, nullptr)
-                         : lic_decode(p->codec, s.y_dec, B, (float*)fr, nullptr);
+        return p->cfg.u8 ? lic_decode_u8(p->codec, s.y_dec, B, fr, p->stream)
+                         : lic_decode(p->codec, s.y_dec, B, (float*)fr, p->stream);
     }
     }
     return LIC_EINVAL;
@@ -252,6 +278,7 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         for (int i = (int)p->slots.size() - 1; i >= 0; --i) p->free_slots.push_back(i);
         p->gpu_q.clear();
         p->cpu_q.clear();
+        p->pending.clear();
         p->lat.clear();
         p->mismatches = p->y_bytes = p->z_bytes = 0;
         p->coder_busy = p->gpu_busy = 0;
@@ -262,38 +289,70 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         }
     }
     const double t_run0 = now_s();
+    // GPU control loop.  GPU tasks are issued asynchronously on p->stream (at most
+    // kMaxPending in flight) so the device never idles while ready work exists; the
+    // oldest issued task is retired by waiting on its event, which then releases its
+    // coder tasks (ENC, IDX) or its slot (DEC).
+    constexpr size_t kMaxPending = 2;
+    size_t ev_next = 0;
     for (;;) {
         GpuTask t{};
+        bool issue = false;
         {
             std::unique_lock<std::mutex> lk(p->mu);
             auto can_enc = [&] {
                 if (p->next_enc >= p->nbatches || p->free_slots.empty()) return false;
                 return !p->cfg.serial || p->done == p->next_enc;
             };
-            p->cv_gpu.wait(lk, [&] { return p->err || p->done == p->nbatches || !p->gpu_q.empty() || can_enc(); });
+            auto have_ready = [&] { return !p->gpu_q.empty() || can_enc(); };
+            p->cv_gpu.wait(lk, [&] {
+                return p->err || p->done == p->nbatches || !p->pending.empty() || have_ready();
+            });
             if (p->err || p->done == p->nbatches) break;
-            if (!p->gpu_q.empty()) {
-                // latest stage first, then oldest batch: drains frames, bounds latency
-                auto best = std::max_element(p->gpu_q.begin(), p->gpu_q.end(), [&](const GpuTask& a, const GpuTask& b) {
-                    if (a.kind != b.kind) return a.kind < b.kind;
-                    return p->slots[a.slot].batch > p->slots[b.slot].batch;
-                });
-                t = *best;
-                p->gpu_q.erase(best);
-            } else {
-                const int s = p->free_slots.back();
-                p->free_slots.pop_back();
-                p->slots[s].batch = p->next_enc++;
-                p->slots[s].t_start = now_s();
-                t = {G_ENC, s};
+            if (p->pending.size() < kMaxPending && have_ready()) {
+                issue = true;
+                if (!p->gpu_q.empty()) {
+                    // latest stage first, then oldest batch: drains frames, bounds latency
+                    auto best = std::max_element(p->gpu_q.begin(), p->gpu_q.end(),
+                                                 [&](const GpuTask& a, const GpuTask& b) {
+                                                     if (a.kind != b.kind) return a.kind < b.kind;
+                                                     return p->slots[a.slot].batch > p->slots[b.slot].batch;
+                                                 });
+                    t = *best;
+                    p->gpu_q.erase(best);
+                } else {
+                    const int s = p->free_slots.back();
+                    p->free_slots.pop_back();
+                    p->slots[s].batch = p->next_enc++;
+                    p->slots[s].t_start = now_s();
+                    t = {G_ENC, s};
+                }
             }
         }
-        const double g0 = now_s();
-        lic_status st = gpu_call(p, t);
+        if (issue) {
+            const double g0 = now_s();
+            lic_status st = gpu_call(p, t);
+            cudaEvent_t ev = p->events[ev_next++ % p->events.size()];
+            if (!st && cudaEventRecord(ev, p->stream) != cudaSuccess) st = LIC_ECUDA;
+            std::lock_guard<std::mutex> g(p->mu);
+            if (st) { p->err = st; break; }
+            p->pending.push_back({t, ev, g0});
+            continue;
+        }
+        // nothing issuable: retire the oldest in-flight GPU task
+        Pending pd;
+        {
+            std::lock_guard<std::mutex> g(p->mu);
+            pd = p->pending.front();
+            p->pending.pop_front();
+        }
+        const double w0 = now_s();
+        const cudaError_t ce = cudaEventSynchronize(pd.done);
         const double g1 = now_s();
         std::lock_guard<std::mutex> g(p->mu);
-        p->gpu_busy += g1 - g0;
-        if (st) { p->err = st; break; }
+        p->gpu_busy += g1 - std::max(w0, pd.t_issue);
+        if (ce != cudaSuccess) { p->err = LIC_ECUDA; break; }
+        t = pd.task;
         Slot& s = p->slots[t.slot];
         if (t.kind == G_ENC || t.kind == G_IDX) {
             s.remaining = (int)B;
@@ -314,6 +373,8 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
             ++p->done;
         }
     }
+    // leave nothing running on the stream
+    cudaStreamSynchronize(p->stream);
     const double t_run1 = now_s();
     // error path: drop queued coder work and wait for tasks already running
     std::unique_lock<std::mutex> g(p->mu);

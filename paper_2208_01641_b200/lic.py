@@ -99,6 +99,12 @@ _L.lic_pipeline_bitstream.argtypes = [_P, _u32, ctypes.POINTER(ctypes.POINTER(ct
                                       ctypes.POINTER(_sz), ctypes.POINTER(ctypes.POINTER(ctypes.c_uint8)),
                                       ctypes.POINTER(_sz)]
 
+_L.lic_rans_prepare.argtypes = [_P, _u32, _u32, _i, ctypes.POINTER(_P)]
+_L.lic_rans_tables_free.argtypes = [_P]
+_L.lic_rans_tables_free.restype = None
+_L.lic_rans_encode_fast.argtypes = [_P, _P, _P, Shape, _P, _sz, ctypes.POINTER(_sz)]
+_L.lic_rans_decode_fast.argtypes = [_P, _P, _sz, _P, Shape, _P]
+
 EXPORTED = [n for n in dir(_L) if n.startswith("lic_")]
 
 
@@ -183,6 +189,50 @@ def rans_decode(data, shape, cdf, rows=None, sym_min=None, out=None):
     if st:
         raise LicError(st, "rans_decode")
     return out
+
+
+class RansTables:
+    """lic_rans_prepare: prepared (fast) coder tables, same bitstream as rans_encode."""
+
+    def __init__(self, cdf, sym_min=None):
+        self.cdf = np.ascontiguousarray(cdf, np.uint32)
+        if sym_min is None:
+            sym_min = -((self.cdf.shape[1] - 2) // 2)
+        self._h = _P()
+        st = _L.lic_rans_prepare(_ptr(self.cdf), self.cdf.shape[0], self.cdf.shape[1], int(sym_min),
+                                 ctypes.byref(self._h))
+        if st:
+            raise LicError(st, "lic_rans_prepare")
+
+    def encode(self, sym, rows=None):
+        sym = np.ascontiguousarray(sym, np.int8)
+        shp = Shape(*sym.shape) if sym.ndim == 3 else Shape(1, 1, sym.size)
+        rows = None if rows is None else np.ascontiguousarray(rows, np.uint8)
+        cap = 2 * sym.size + 64
+        out = np.empty(cap, np.uint8)
+        n = ctypes.c_size_t(0)
+        st = _L.lic_rans_encode_fast(self._h, _ptr(sym), _ptr(rows), shp, _ptr(out), cap, ctypes.byref(n))
+        if st:
+            raise LicError(st, "rans_encode_fast")
+        return out[: n.value].tobytes()
+
+    def decode(self, data, shape, rows=None):
+        shp = Shape(*shape) if len(shape) == 3 else Shape(1, 1, int(np.prod(shape)))
+        rows = None if rows is None else np.ascontiguousarray(rows, np.uint8)
+        out = np.empty(shape, np.int8)
+        buf = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)
+        st = _L.lic_rans_decode_fast(self._h, _ptr(buf), len(data), _ptr(rows), shp, _ptr(out))
+        if st == LIC_ECORRUPT:
+            raise CorruptStream(st, "corrupt stream")
+        if st:
+            raise LicError(st, "rans_decode_fast")
+        return out
+
+    def __del__(self):
+        try:
+            _L.lic_rans_tables_free(self._h)
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------- codec

@@ -85,3 +85,44 @@ def test_licw_roundtrip():
         assert all(np.array_equal(w[k], w2[k]) for k in w)
         assert write_licw(spec, generate_weights(spec, 5)) == blob          # deterministic
         assert blob[:4] == b"LICW"
+
+
+@pytest.mark.parametrize("C,H,W,scale", [(192, 12, 20, 1.5), (128, 3, 5, 0.3), (320, 17, 30, 6.0)])
+def test_fast_coder_channel_rows_bit_exact(lic, C, H, W, scale):
+    """Prepared tables (reciprocal encode, bucketed decode) emit the oracle's bytes."""
+    L = 32
+    cdf = O.cdf_table(RNG.uniform(0.5, 1.5, C), L)
+    sym = np.clip(np.round(RNG.standard_normal((C, H, W)) * scale), -L, L).astype(np.int8)
+    t = lic.RansTables(cdf)
+    b = t.encode(sym)
+    assert b == O.rans_encode(sym, O.channel_rows(sym.shape), cdf)
+    assert np.array_equal(t.decode(b, sym.shape), sym)
+
+
+def test_fast_coder_indexed_rows_bit_exact(lic):
+    L = 32
+    cdf = O.cdf_table(scale_table(), L)
+    n = 300_000
+    idx = RNG.integers(0, 64, n).astype(np.uint8)
+    sym = np.clip(np.round(RNG.standard_normal(n) * scale_table()[idx]), -L, L).astype(np.int8)
+    sym[:1000] = 32                      # freq-1 edge symbols (reciprocal special case)
+    sym[1000:2000] = -32
+    t = lic.RansTables(cdf)
+    b = t.encode(sym, rows=idx)
+    assert b == O.rans_encode(sym, idx.astype(np.int32), cdf)
+    assert np.array_equal(t.decode(b, (n,), rows=idx), sym)
+    with pytest.raises(lic.CorruptStream):
+        t.decode(b[:-2], (n,), rows=idx)
+
+
+def test_fast_coder_general_tables(lic):
+    """Arbitrary tables incl. freq-1 and large-freq symbols (known answers)."""
+    c = np.array([[0, 100, 40000, 65536]], np.uint32)
+    t = lic.RansTables(c, sym_min=0)
+    assert t.encode(np.array([2, 1, 0, 1, 2, 2, 1, 1], np.int8), rows=np.zeros(8, np.uint8)).hex() == "009dc5b89250"
+    c = np.array([[0, 1, 65536]], np.uint32)
+    t = lic.RansTables(c, sym_min=0)
+    assert t.encode(np.array([0], np.int8), rows=np.zeros(1, np.uint8)).hex() == "008000000000"
+    sym = RNG.integers(0, 2, 5000).astype(np.int8)
+    b = t.encode(sym, rows=np.zeros(5000, np.uint8))
+    assert b == O.rans_encode(sym, np.zeros(5000), c, sym_min=0)
