@@ -16,9 +16,9 @@
 // stride-2 gather and the zero padding are done by the TMA unit) and B (BN x 64).  Two
 // MMAs per 16-wide K step (hi, lo) accumulate into one fp32 TMEM accumulator.
 //
-// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w3 idle,
-// w4-11 epilogue: warp w reads TMEM lanes 32*(w%4).. (= 32 of the tile's 128 pixels) and
-// group (w-4)/4 owns one half of the output channels.
+// Warp roles (640 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w3 idle,
+// w4-19 epilogue: warp w reads TMEM lanes 32*(w%4).. (= 32 of the tile's 128 pixels) and
+// group (w-4)/4 owns one quarter of the output channels.
 //
 // GDN epilogue: each thread keeps x = acc + b for its half of the channels in registers,
 // writes x^2 as fp16 hi/lo back into its own accumulator columns (tcgen05.st), and one
@@ -33,7 +33,8 @@
 
 namespace lic {
 
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;                 // 4 per TMEM lane quadrant
+constexpr int kEpiGroups = kEpiWarps / 4;     // channel groups (quarters of the N tile)
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 
 struct TileCoord { int b, ph, gy0, gx0, nt; };
@@ -79,7 +80,7 @@ __device__ __forceinline__ int round_clamp(float v, int L, int& sat) {
     return (int)r;
 }
 
-// GC: GDN/IGDN layers only -- 32-column chunks per epilogue group (BN = 64*GC); 0 otherwise
+// GC: GDN/IGDN layers only -- 16-column chunks per epilogue group (BN = 64*GC); 0 otherwise
 template <int GC>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
@@ -208,7 +209,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     } else if (warp >= 4) {
         // ====================== epilogue ======================
         const int q = warp & 3;                     // TMEM lane quadrant
-        const int g = (warp - 4) >> 2;              // channel half
+        const int g = (warp - 4) >> 2;              // channel group (quarter)
         const int r = q * 32 + lane;                // tile row (pixel) of this thread
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         uint32_t norm_phase = 0;
@@ -235,30 +236,33 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const int co0 = tc.nt * p.BN;
 
             if constexpr (kGdn) {
-                constexpr int G = 32 * GC;                   // channels of this group
-                float x[GC][32];
+                constexpr int G = 16 * GC;                   // channels of this group
+                float x[GC][16];
 #pragma unroll
                 for (int j = 0; j < GC; ++j) {
                     __syncwarp();
-                    tmem_ld32(taddr + g * G + j * 32, x[j]);
+                    tmem_ld16(taddr + g * G + j * 16, x[j]);
                 }
                 // x^2 (hi, lo) packed into this group's own accumulator columns:
                 // hi of channel g*G + k at column g*G + k/2, lo at g*G + G/2 + k/2
 #pragma unroll
                 for (int j = 0; j < GC; ++j) {
-                    uint32_t hi[16], lo[16];
+                    uint32_t hi[8], lo[8];
+                    const float4* b4 = reinterpret_cast<const float4*>(s_bias + g * G + j * 16);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int c0 = g * G + j * 32 + 2 * i;
-                        const float a = x[j][2 * i] + s_bias[c0], b = x[j][2 * i + 1] + s_bias[c0 + 1];
-                        x[j][2 * i] = a;
-                        x[j][2 * i + 1] = b;
-                        const float a2 = a * a, b2 = b * b;
+                    for (int i4 = 0; i4 < 4; ++i4) {
+                        const float4 bb = b4[i4];
+                        x[j][4 * i4 + 0] += bb.x; x[j][4 * i4 + 1] += bb.y;
+                        x[j][4 * i4 + 2] += bb.z; x[j][4 * i4 + 3] += bb.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float a2 = x[j][2 * i] * x[j][2 * i], b2 = x[j][2 * i + 1] * x[j][2 * i + 1];
                         hi[i] = h2_bits(a2, b2);
                         lo[i] = h2_bits(a2 - hround(a2), b2 - hround(b2));
                     }
-                    tmem_st16(taddr + g * G + j * 16, hi);
-                    tmem_st16(taddr + g * G + G / 2 + j * 16, lo);
+                    tmem_st8(taddr + g * G + j * 8, hi);
+                    tmem_st8(taddr + g * G + G / 2 + j * 8, lo);
                 }
                 tmem_st_wait();
                 tc_fence_before();
@@ -285,23 +289,31 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 __half* out = reinterpret_cast<__half*>(p.out_act);
 #pragma unroll
                 for (int j = 0; j < GC; ++j) {
-                    float n[32];
+                    float n[16];
                     __syncwarp();
-                    tmem_ld32(taddr + p.BN + g * G + j * 32, n);
-                    const int cb = g * G + j * 32;
+                    tmem_ld16(taddr + p.BN + g * G + j * 16, n);
+                    const int cb = g * G + j * 16;
+                    const float4* be4 = reinterpret_cast<const float4*>(s_beta + cb);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const float nn = s_beta[cb + i] + n[i];
-                        x[j][i] = (p.ep == EP_GDN) ? x[j][i] * rsqrtf(nn) : x[j][i] * sqrtf(nn);
+                    for (int i4 = 0; i4 < 4; ++i4) {
+                        const float4 be = be4[i4];
+                        const float bv[4] = {be.x, be.y, be.z, be.w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = 4 * i4 + u;
+                            const float nn = bv[u] + n[i];
+                            const float rs = rsqrtf(nn);           // MUFU; sqrt(nn) = nn * rsqrt(nn)
+                            x[j][i] = (p.ep == EP_GDN) ? x[j][i] * rs : x[j][i] * (nn * rs);
+                        }
                     }
                     if (valid) {
                         if (p.out_f32) {
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) p.out_f32[chw0 + (size_t)(cb + i) * HWo] = x[j][i];
+                            for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(cb + i) * HWo] = x[j][i];
                         }
                         if (out) {
 #pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
+                            for (int qq = 0; qq < 2; ++qq)
                                 split_store8(out + pix * p.Cout + cb + qq * 8,
                                              p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + qq * 8 : nullptr,
                                              x[j] + qq * 8);
@@ -309,34 +321,43 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     }
                 }
             } else {
-                const int ncol32 = (p.BN + 31) / 32;
-                for (int c = g; c < ncol32; c += 2) {
-                    float v[32];
+                const int ncol16 = (p.BN + 15) / 16;
+                for (int c = g; c < ncol16; c += kEpiGroups) {
+                    float v[16];
                     __syncwarp();
-                    tmem_ld32(taddr + c * 32, v);
-                    const int cb = co0 + c * 32;
+                    tmem_ld16(taddr + c * 16, v);
+                    const int cb = co0 + c * 16;
                     if (valid && cb < p.Cout) {
-                        const int nj = p.pack4 ? 16 : min(32, p.Cout - cb);
+                        const int nj = p.pack4 ? 16 : min(16, p.Cout - cb);
+                        if (p.pack4) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] += s_bias[p.pack4 ? (j & 3) : cb + j];
+                            for (int j = 0; j < 16; ++j) v[j] += s_bias[j & 3];
+                        } else {
+                            const float4* b4 = reinterpret_cast<const float4*>(s_bias + cb);
+#pragma unroll
+                            for (int i4 = 0; i4 < 4; ++i4) {
+                                const float4 bb = b4[i4];
+                                v[4 * i4 + 0] += bb.x; v[4 * i4 + 1] += bb.y; v[4 * i4 + 2] += bb.z; v[4 * i4 + 3] += bb.w;
+                            }
+                        }
                         switch (p.ep) {
                         case EP_F32: {
 #pragma unroll
-                            for (int j = 0; j < 32; ++j)
+                            for (int j = 0; j < 16; ++j)
                                 if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
                             break;
                         }
                         case EP_RELU: {
                             __half* out = reinterpret_cast<__half*>(p.out_act);
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+                            for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.0f);
                             if (p.out_f32) {
 #pragma unroll
-                                for (int j = 0; j < 32; ++j)
+                                for (int j = 0; j < 16; ++j)
                                     if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
                             }
 #pragma unroll
-                            for (int qq = 0; qq < 4; ++qq)
+                            for (int qq = 0; qq < 2; ++qq)
                                 split_store8(out + pix * p.Cout + cb + qq * 8,
                                              p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + qq * 8 : nullptr,
                                              v + qq * 8);
@@ -345,9 +366,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         case EP_YQUANT:
                         case EP_ZQUANT: {
                             int8_t* sym = reinterpret_cast<int8_t*>(p.out_sym);
-                            float av[32];
+                            float av[16];
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) {
+                            for (int j = 0; j < 16; ++j) {
                                 const float m = s_mu[cb + j];
                                 const int s = (j < nj) ? round_clamp(v[j] - m, p.L, sat) : 0;
                                 if (j < nj) sym[chw0 + (size_t)(cb + j) * HWo] = (int8_t)s;
@@ -355,13 +376,13 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             }
                             if (p.out_f32) {
 #pragma unroll
-                                for (int j = 0; j < 32; ++j)
+                                for (int j = 0; j < 16; ++j)
                                     if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
                             }
                             if (p.out_act && (p.ep == EP_ZQUANT || p.abs_out)) {
                                 __half* out = reinterpret_cast<__half*>(p.out_act);
 #pragma unroll
-                                for (int qq = 0; qq < 4; ++qq)
+                                for (int qq = 0; qq < 2; ++qq)
                                     split_store8(out + pix * p.Cout + cb + qq * 8,
                                                  p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + qq * 8 : nullptr,
                                                  av + qq * 8);
@@ -371,7 +392,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         case EP_SIGMA: {
                             uint8_t* idx = reinterpret_cast<uint8_t*>(p.out_sym);
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) {
+                            for (int j = 0; j < 16; ++j) {
                                 if (j >= nj) continue;
                                 float s = fmaxf(v[j], 0.0f);
                                 if (p.out_f32) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = s;
@@ -389,7 +410,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         }
                         case EP_FINAL: {
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) {
+                            for (int j = 0; j < 16; ++j) {
                                 if (j >= nj) continue;
                                 // packed phases: column j -> sub-pixel (j>>2) of grid pixel (gy, gx), channel j&3
                                 const int ch = p.pack4 ? (j & 3) : cb + j;
