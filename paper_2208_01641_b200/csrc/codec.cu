@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -161,6 +162,7 @@ struct lic_codec {
     float *dbg_y = nullptr, *dbg_z = nullptr, *dbg_s = nullptr;
     int debug = 0;
     int zero_copy = 0;
+    int halo_enabled = 1;          // LIC_NO_HALO=1 in the environment disables halo mode
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
     std::vector<void*> allocs;          // device allocations to free
@@ -326,20 +328,52 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
             P.ntaps[ph] = ntap - P.tap0[ph];
         }
     }
-    choose_tile(P.Hg, P.Wg, &P.Wt, &P.Ht);
-    P.tiles_x = (P.Wg + P.Wt - 1) / P.Wt;
-    P.tiles_y = (P.Hg + P.Ht - 1) / P.Ht;
-    // shared memory plan: stage ring | gamma (GDN) | mbarriers | per-channel constants
+    // shared memory plan: stage ring | halo ring (halo mode) | gamma (GDN) | mbarriers | constants
     const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)P.BN * 64 * 2;
-    P.stage_bytes = a_bytes * P.split + b_bytes;
     const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
     const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64) * 4;
     const uint32_t fixed = gamma_bytes + 256 + par_bytes + 1024;
-    int stages = (int)((227u * 1024u - fixed) / P.stage_bytes);
-    stages = std::min(stages, 8);
-    if (stages < 2) return fail(c, LIC_EINVAL, "layer does not fit shared memory");
-    P.stages = stages;
-    P.off_gamma = stages * P.stage_bytes;
+    const uint32_t budget = 227u * 1024u;
+    // halo mode: every stride-1 layer whose taps stay inside a 3x3 neighbourhood
+    const bool stride1 = !gemm_l1 && (Ly.deconv || (Ly.k == 3 && Ly.s == 1));
+    const uint32_t hpb = ((10 * 18 * 128) + 1023) / 1024 * 1024;      // (Wt+2) x (Ht+2) rows
+    if (stride1 && fixed + 2 * P.split * hpb + 2 * b_bytes <= budget && c->halo_enabled) {
+        P.halo = 1;
+        P.Wt = 8; P.Ht = 16;
+        P.halo_plane_bytes = hpb;
+        P.stage_bytes = b_bytes;
+        // deepest halo ring (<= 4 slots) that leaves room for >= 3 weight stages
+        int slots = 4;
+        while (slots > 2 && fixed + slots * P.split * hpb + 3 * b_bytes > budget) --slots;
+        P.halo_slots = slots;
+        // small weight sets (packed g_s L4: 9 taps x 2 chunks x 2 KB) stay resident
+        const uint32_t wtot = (uint32_t)P.ntaps[0] * P.kchunks * b_bytes;
+        if (P.nphase == 1 && fixed + slots * P.split * hpb + wtot <= budget && wtot <= 64 * 1024) {
+            P.wres = 1;
+            P.stages = 1;
+            P.stage_bytes = 0;
+            P.off_wres = 0;
+            P.off_halo = (wtot + 1023) / 1024 * 1024;
+        } else {
+            int stages = (int)((budget - fixed - slots * P.split * hpb) / P.stage_bytes);
+            P.stages = std::min(stages, 8);
+            P.off_halo = P.stages * P.stage_bytes;
+        }
+        P.off_gamma = P.off_halo + slots * P.split * hpb;
+    } else {
+        P.halo = 0;
+        P.halo_slots = 0;
+        choose_tile(P.Hg, P.Wg, &P.Wt, &P.Ht);
+        P.stage_bytes = a_bytes * P.split + b_bytes;
+        int stages = (int)((budget - fixed) / P.stage_bytes);
+        stages = std::min(stages, 8);
+        if (stages < 2) return fail(c, LIC_EINVAL, "layer does not fit shared memory");
+        P.stages = stages;
+        P.off_halo = 0;
+        P.off_gamma = stages * P.stage_bytes;
+    }
+    P.tiles_x = (P.Wg + P.Wt - 1) / P.Wt;
+    P.tiles_y = (P.Hg + P.Ht - 1) / P.Ht;
     P.off_bar = P.off_gamma + gamma_bytes;
     P.off_par = P.off_bar + 256;
     P.smem_bytes = P.off_par + par_bytes + 1024;
@@ -355,7 +389,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     const int cout_pad = P.BN * P.n_ntiles;
     if (!encode_act_map(&Ly.mapA, Ly.in_buf, P.Cin, Ly.deconv ? Ly.Win : (gemm_l1 ? Ly.Wout : Ly.Win),
                         Ly.deconv ? Ly.Hin : (gemm_l1 ? Ly.Hout : Ly.Hin), c->max_batch, P.split, Ly.in_plane,
-                        P.Wt, P.Ht, P.stride))
+                        P.halo ? P.Wt + 2 : P.Wt, P.halo ? P.Ht + 2 : P.Ht, P.stride))
         return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (activations) failed");
     if (!encode_w_map(&Ly.mapB, Ly.w, P.Cin, cout_pad, ntaps_w, P.BN))
         return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (weights) failed");
@@ -509,6 +543,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     c->num_sms = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(LIC_ECUDA);
     c->split = precision == LIC_PREC_SPLIT ? 2 : 1;
+    if (const char* e = std::getenv("LIC_NO_HALO")) c->halo_enabled = (e[0] == '0');
     c->max_batch = (int)max_batch;
     c->H = (int)height; c->W = (int)width;
     const int P = c->kind == 1 ? 64 : 16;

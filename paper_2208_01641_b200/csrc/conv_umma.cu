@@ -97,7 +97,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     uint64_t* tempty_bar = tfull_bar + 2;           // [2]
     uint64_t* norm_bar = tempty_bar + 2;
     uint64_t* gamma_bar = norm_bar + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gamma_bar + 1);
+    uint64_t* hfull_bar = gamma_bar + 1;            // [4] halo ring
+    uint64_t* hempty_bar = hfull_bar + 4;           // [4]
+    uint64_t* xsq_bar = hempty_bar + 4;             // epilogue -> MMA warp: x^2 written to TMEM
+    uint64_t* wres_bar = xsq_bar + 1;               // resident weights landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wres_bar + 1);
     float* s_bias = reinterpret_cast<float*>(smem + p.off_par);   // [cout_pad]
     float* s_beta = s_bias + p.BN * p.n_ntiles;                     // [cout_pad]
     float* s_mu = s_beta + p.BN * p.n_ntiles;                       // [cout_pad]
@@ -112,6 +116,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], kEpiWarps); }
         mbar_init(norm_bar, 1);
         mbar_init(gamma_bar, 1);
+        for (int i = 0; i < 4; ++i) { mbar_init(&hfull_bar[i], 1); mbar_init(&hempty_bar[i], 1); }
+        mbar_init(xsq_bar, kEpiWarps);
+        mbar_init(wres_bar, 1);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -141,51 +148,181 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     const uint32_t idesc = idesc_f16_f32(kBM, (uint32_t)p.BN);
 
     if (warp == 0) {
-        // ====================== TMA producer ======================
-        if (lane == 0) {
-            if (kGdn) {
-                // gamma (Cout x Cout fp16, K-major rows; BN/64 = GC chunks of 64 columns)
-                // resident for the whole launch
+        // ====================== TMA producer (weights; activations unless halo mode) ======================
+        // warp-uniform loop; one elected lane issues (keeps coordinates in uniform registers)
+        if (kGdn) {
+            // gamma (Cout x Cout fp16, K-major rows; BN/64 = GC chunks of 64 columns), resident
+            if (elect_one()) {
                 mbar_arrive_expect_tx(gamma_bar, (uint32_t)GC * b_bytes);
                 for (int c = 0; c < GC; ++c)
                     tma_load_3d(smem + p.off_gamma + c * b_bytes, &mapG, gamma_bar, c * kBK, 0, 0);
             }
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-                TileCoord tc = decode_tile(p, t);
-                const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
-                for (int ti = 0; ti < nt; ++ti) {
-                    const int x0 = p.stride * tc.gx0 + p.tap_dx[t0 + ti];
-                    const int y0 = p.stride * tc.gy0 + p.tap_dy[t0 + ti];
-                    const int wt = p.tap_w[t0 + ti];
-                    for (int c = 0; c < p.kchunks; ++c) {
+            __syncwarp();
+        }
+        if (p.wres) {
+            // every (tap, chunk) weight tile, once per CTA: tile (w, c) at (w * kchunks + c) * b_bytes
+            if (elect_one()) {
+                const int nw = p.ntaps[0];
+                mbar_arrive_expect_tx(wres_bar, (uint32_t)(nw * p.kchunks) * b_bytes);
+                for (int w = 0; w < nw; ++w)
+                    for (int c = 0; c < p.kchunks; ++c)
+                        tma_load_3d(smem + p.off_wres + (w * p.kchunks + c) * b_bytes, &mapB, wres_bar, c * kBK, 0,
+                                    p.tap_w[w]);
+            }
+            __syncwarp();
+        }
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = blockIdx.x; t < p.total_tiles && !p.wres; t += gridDim.x) {
+            TileCoord tc = decode_tile(p, t);
+            const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
+            if (p.halo) {
+                // chunk-outer, tap-inner weight tiles (halos come from warp 3)
+                for (int c = 0; c < p.kchunks; ++c)
+                    for (int ti = 0; ti < nt; ++ti) {
                         mbar_wait(&empty_bar[stage], phase ^ 1);
-                        uint8_t* st = smem + stage * p.stage_bytes;
+                        if (elect_one()) {
+                            mbar_arrive_expect_tx(&full_bar[stage], b_bytes);
+                            tma_load_3d(smem + stage * p.stage_bytes, &mapB, &full_bar[stage], c * kBK,
+                                        tc.nt * p.BN, p.tap_w[t0 + ti]);
+                        }
+                        __syncwarp();
+                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    }
+                continue;
+            }
+            for (int ti = 0; ti < nt; ++ti) {
+                const int x0 = p.stride * tc.gx0 + p.tap_dx[t0 + ti];
+                const int y0 = p.stride * tc.gy0 + p.tap_dy[t0 + ti];
+                const int wt = p.tap_w[t0 + ti];
+                for (int c = 0; c < p.kchunks; ++c) {
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    uint8_t* st = smem + stage * p.stage_bytes;
+                    if (elect_one()) {
                         mbar_arrive_expect_tx(&full_bar[stage], a_bytes * p.split + b_bytes);
                         tma_load_5d(st, &mapA, &full_bar[stage], c * kBK, x0, y0, tc.b, 0);
                         if (p.split == 2)
                             tma_load_5d(st + a_bytes, &mapA, &full_bar[stage], c * kBK, x0, y0, tc.b, 1);
-                        tma_load_3d(st + a_bytes * p.split, &mapB, &full_bar[stage], c * kBK,
-                                    tc.nt * p.BN, wt);
-                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                        tma_load_3d(st + a_bytes * p.split, &mapB, &full_bar[stage], c * kBK, tc.nt * p.BN, wt);
                     }
+                    __syncwarp();
+                    if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ====================== halo producer (halo mode) ======================
+        if (p.halo) {
+            int hs = 0;
+            uint32_t hphase = 0;
+            const uint32_t hbytes = (uint32_t)(p.Wt + 2) * (p.Ht + 2) * 128 * p.split;
+            for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+                TileCoord tc = decode_tile(p, t);
+                for (int c = 0; c < p.kchunks; ++c) {
+                    mbar_wait(&hempty_bar[hs], hphase ^ 1);
+                    uint8_t* hb = smem + p.off_halo + hs * (2 * p.halo_plane_bytes);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&hfull_bar[hs], hbytes);
+                        tma_load_5d(hb, &mapA, &hfull_bar[hs], c * kBK, tc.gx0 - 1, tc.gy0 - 1, tc.b, 0);
+                        if (p.split == 2)
+                            tma_load_5d(hb + p.halo_plane_bytes, &mapA, &hfull_bar[hs], c * kBK, tc.gx0 - 1,
+                                        tc.gy0 - 1, tc.b, 1);
+                    }
+                    __syncwarp();
+                    if (++hs == p.halo_slots) { hs = 0; hphase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
         // ====================== MMA issuer ======================
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            int it = 0;
-            for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
-                TileCoord tc = decode_tile(p, t);
-                const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
-                const uint32_t use = (p.n_accbuf == 2) ? (uint32_t)(it >> 1) : (uint32_t)it;
-                mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
-                tc_fence_after();
-                const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
+        // Warp-uniform; one elected lane issues each batch of tcgen05.mma.
+        // GDN/IGDN: the norm MMAs (x^2 . gamma^T, A from TMEM) of tile i are issued HERE, as soon
+        // as the epilogue has written x^2 (xsq_bar), between K-steps of tile i+1 -- the tensor
+        // pipe runs MMAs in issue order, so issuing them from the epilogue would queue them
+        // behind the whole next main loop.
+        int stage = 0;
+        uint32_t phase = 0;
+        int hs = 0;
+        uint32_t hphase = 0;
+        int it = 0;
+        int pend = 0;                       // a tile's norm MMAs are outstanding
+        uint32_t pend_dcol = 0, xsq_phase = 0;
+        bool gamma_ready = false;
+        auto issue_norm = [&]() {
+            if (!gamma_ready) { mbar_wait(gamma_bar, 0); gamma_ready = true; }
+            tc_fence_after();
+            constexpr int G = 16 * (GC > 0 ? GC : 1);
+            const uint32_t ncol = tmem_base + pend_dcol + (uint32_t)p.BN;
+            const uint32_t gbase = smem_u32(smem + p.off_gamma);
+            if (elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 4 * GC; ++kk) {           // K = BN in steps of 16
+                    const int k0 = 16 * kk, gg = k0 / G, o = k0 - gg * G;
+                    const uint32_t ahi = tmem_base + pend_dcol + gg * G + o / 2;
+                    const uint32_t alo = ahi + G / 2;
+                    const uint64_t bd = sdesc_sw128(gbase + (k0 / 64) * b_bytes) + 2 * (kk & 3);
+                    umma_f16_ts(ncol, ahi, bd, idesc, kk != 0);
+                    umma_f16_ts(ncol, alo, bd, idesc, 1u);
+                }
+                umma_commit(norm_bar);
+            }
+            __syncwarp();
+            pend = 0;
+        };
+        int poll_ctr = 0;
+        auto poll_norm = [&]() {       // every 4th K step: test_wait is ~150 cycles
+            if (kGdn && pend && (++poll_ctr & 3) == 0 && mbar_test(xsq_bar, xsq_phase)) {
+                xsq_phase ^= 1;
+                issue_norm();
+            }
+        };
+        if (p.wres) mbar_wait(wres_bar, 0);
+        for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
+            TileCoord tc = decode_tile(p, t);
+            const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
+            const uint32_t use = (p.n_accbuf == 2) ? (uint32_t)(it >> 1) : (uint32_t)it;
+            if (kGdn && pend && p.n_accbuf == 1) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; issue_norm(); }
+            mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
+            if (p.halo) {
+                const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
+                const uint32_t sbo = (uint32_t)(p.Wt + 2) * 128;
+                for (int c = 0; c < p.kchunks; ++c) {
+                    mbar_wait(&hfull_bar[hs], hphase);
+                    tc_fence_after();
+                    const uint32_t hb = smem_u32(smem + p.off_halo + hs * (2 * p.halo_plane_bytes));
+                    for (int ti = 0; ti < nt; ++ti) {
+                        uint32_t bsm;
+                        if (p.wres) {
+                            bsm = smem_u32(smem + p.off_wres + ((t0 + ti) * p.kchunks + c) * b_bytes);
+                        } else {
+                            mbar_wait(&full_bar[stage], phase);
+                            tc_fence_after();
+                            bsm = smem_u32(smem + stage * p.stage_bytes);
+                        }
+                        // window of this tap: halo row (dy+1)*(Wt+2) + (dx+1), 8-row groups every Wt+2 rows
+                        const uint32_t row0 = (uint32_t)((p.tap_dy[t0 + ti] + 1) * (p.Wt + 2) + p.tap_dx[t0 + ti] + 1);
+                        const uint64_t ah = sdesc_sw128_sbo(hb + row0 * 128, sbo);
+                        const uint64_t al = sdesc_sw128_sbo(hb + p.halo_plane_bytes + row0 * 128, sbo);
+                        const uint64_t bd = sdesc_sw128(bsm);
+                        if (elect_one()) {
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 16; ++kk) {
+                                umma_f16(d, ah + 2 * kk, bd + 2 * kk, idesc, (c | ti | kk) != 0);
+                                if (p.split == 2) umma_f16(d, al + 2 * kk, bd + 2 * kk, idesc, 1u);
+                            }
+                            if (!p.wres) umma_commit(&empty_bar[stage]);
+                        }
+                        __syncwarp();
+                        if (!p.wres && ++stage == p.stages) { stage = 0; phase ^= 1; }
+                        poll_norm();
+                    }
+                    if (elect_one()) umma_commit(&hempty_bar[hs]);
+                    __syncwarp();
+                    if (++hs == p.halo_slots) { hs = 0; hphase ^= 1; }
+                }
+            } else {
                 const int nk = p.ntaps[tc.ph] * p.kchunks;
                 for (int k = 0; k < nk; ++k) {
                     mbar_wait(&full_bar[stage], phase);
@@ -194,18 +331,30 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     const uint64_t ah = sdesc_sw128(st);
                     const uint64_t al = sdesc_sw128(st + a_bytes);
                     const uint64_t bd = sdesc_sw128(st + a_bytes * p.split);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk) {
-                        // +32 bytes per 16-element K step inside the 128-byte swizzle row
-                        umma_f16(d, ah + 2 * kk, bd + 2 * kk, idesc, (k | kk) != 0);
-                        if (p.split == 2) umma_f16(d, al + 2 * kk, bd + 2 * kk, idesc, 1u);
+                        for (int kk = 0; kk < kBK / 16; ++kk) {
+                            // +32 bytes per 16-element K step inside the 128-byte swizzle row
+                            umma_f16(d, ah + 2 * kk, bd + 2 * kk, idesc, (k | kk) != 0);
+                            if (p.split == 2) umma_f16(d, al + 2 * kk, bd + 2 * kk, idesc, 1u);
+                        }
+                        umma_commit(&empty_bar[stage]);
                     }
-                    umma_commit(&empty_bar[stage]);
+                    __syncwarp();
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    poll_norm();
                 }
-                umma_commit(&tfull_bar[buf]);
+            }
+            if (elect_one()) umma_commit(&tfull_bar[buf]);
+            __syncwarp();
+            if (kGdn) {
+                // the previous tile's norm must be issued before this one becomes pending
+                if (pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; issue_norm(); }
+                pend = 1;
+                pend_dcol = (uint32_t)(buf * p.acc_stride);
             }
         }
+        if (kGdn && pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; issue_norm(); }
     } else if (warp >= 4) {
         // ====================== epilogue ======================
         const int q = warp & 3;                     // TMEM lane quadrant
@@ -213,14 +362,16 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         const int r = q * 32 + lane;                // tile row (pixel) of this thread
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         uint32_t norm_phase = 0;
-        bool gamma_ready = false;
         int it = 0;
         int sat = 0;
         for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
             TileCoord tc = decode_tile(p, t);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
             const uint32_t use = (p.n_accbuf == 2) ? (uint32_t)(it >> 1) : (uint32_t)it;
-            mbar_wait(&tfull_bar[buf], use & 1);
+            // one lane waits on the mbarrier, the other epilogue warps sleep in a hardware
+            // named barrier (no polling: keeps the SYNCS unit and the issue slots free)
+            if (threadIdx.x == 128) mbar_wait(&tfull_bar[buf], use & 1);
+            named_bar_sync(2, 32 * kEpiWarps);
             tc_fence_after();
             const uint32_t dcol = (uint32_t)(buf * p.acc_stride);
             const uint32_t taddr = tmem_base + lane_off + dcol;
@@ -266,25 +417,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 }
                 tmem_st_wait();
                 tc_fence_before();
-                named_bar_sync(1, 32 * kEpiWarps);
-                if (threadIdx.x == 128) {
-                    if (!gamma_ready) { mbar_wait(gamma_bar, 0); gamma_ready = true; }
-                    tc_fence_after();
-                    const uint32_t ncol = tmem_base + dcol + (uint32_t)p.BN;
-                    const uint32_t gbase = smem_u32(smem + p.off_gamma);
-#pragma unroll
-                    for (int kk = 0; kk < 4 * GC; ++kk) {           // K = BN in steps of 16
-                        const int k0 = 16 * kk, gg = k0 / G, o = k0 - gg * G;
-                        const uint32_t ahi = tmem_base + dcol + gg * G + o / 2;
-                        const uint32_t alo = ahi + G / 2;
-                        const uint64_t bd = sdesc_sw128(gbase + (k0 / 64) * b_bytes) + 2 * (kk & 3);
-                        umma_f16_ts(ncol, ahi, bd, idesc, kk != 0);
-                        umma_f16_ts(ncol, alo, bd, idesc, 1u);
-                    }
-                    umma_commit(norm_bar);
-                }
-                mbar_wait(norm_bar, norm_phase);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(xsq_bar);       // the MMA warp issues the norm MMAs
+                if (threadIdx.x == 128) mbar_wait(norm_bar, norm_phase);
                 norm_phase ^= 1;
+                named_bar_sync(3, 32 * kEpiWarps);
                 tc_fence_after();
                 __half* out = reinterpret_cast<__half*>(p.out_act);
 #pragma unroll

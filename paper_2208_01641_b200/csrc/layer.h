@@ -44,6 +44,14 @@ struct ConvParams {
     // ---- kernel resources (host-computed)
     int stages;
     uint32_t stage_bytes, off_gamma, off_bar, off_par, smem_bytes;
+    // halo mode (stride-1 layers: 3x3 convs, sub-pixel deconv phases, packed g_s L4):
+    // per 64-channel chunk the (Ht+2) x (Wt+2) input halo (hi + lo) is loaded once into a
+    // 2-slot ring and every tap reads its A operand as a shifted window of it; the stage
+    // ring then carries only weight tiles.  Tile fixed at Wt = 8, Ht = 16.
+    int halo, halo_slots;
+    uint32_t off_halo, halo_plane_bytes;
+    int wres;                         // all weight tiles resident in smem (loaded once per CTA)
+    uint32_t off_wres;
     int tmem_cols, acc_stride, n_accbuf;
     // ---- epilogue
     int ep;
