@@ -51,3 +51,36 @@ def test_open_without_gpu_fails_loudly():
         assert e.status == lic.LIC_ECUDA
     else:
         raise AssertionError("lic_open succeeded without a GPU")
+
+
+def test_invalid_weights_rejected_before_device():
+    """SPEC.md:102 (beta > 0, gamma >= 0 validated at load) and a malformed container are
+    rejected by lic_open's parser, before any device work."""
+    import numpy as np
+    from lic_synth import ModelSpec, generate_weights, write_licw
+    from paper_2208_01641_b200 import lic
+    spec = ModelSpec(kind=1, N=128, M=192)
+    w = generate_weights(spec, 0)
+    w["ga2.beta"] = w["ga2.beta"].copy()
+    w["ga2.beta"][3] = 0.0
+    try:
+        lic.Codec(write_licw(spec, w), 128, 128)
+    except lic.LicError as e:
+        assert e.status == lic.LIC_EINVAL
+    else:
+        raise AssertionError("beta = 0 accepted")
+    w = generate_weights(spec, 0)
+    w["gs1.gamma"] = w["gs1.gamma"].copy()
+    w["gs1.gamma"][0, 5] = -0.01
+    try:
+        lic.Codec(write_licw(spec, w), 128, 128)
+    except lic.LicError as e:
+        assert e.status == lic.LIC_EINVAL
+    blob = write_licw(spec, generate_weights(spec, 0))
+    for bad in (blob[:-4], b"LICX" + blob[4:], blob + b"\0"):
+        try:
+            lic.Codec(bad, 128, 128)
+        except lic.LicError as e:
+            assert e.status == lic.LIC_EDIGEST
+        else:
+            raise AssertionError("malformed container accepted")
