@@ -174,6 +174,8 @@ struct lic_codec {
     // measurement
     uint64_t launches = 0;
     int profiling = 0;
+    int trace_layer = -1;
+    unsigned long long* d_trace = nullptr;   // 256 tiles x 8 events
     std::vector<cudaEvent_t> ev;            // [2 * kProfSlots]
     std::vector<int> ev_layer;              // layer of each recorded pair
     int ev_used = 0;
@@ -268,6 +270,11 @@ static void choose_tile(int Hg, int Wg, int* Wt, int* Ht) {
     }
 }
 
+// mbarrier area: full/empty[<= 8] + tfull/tempty[2] + norm + gamma + hfull/hempty[4] + xsq +
+// wres (34 x 8 B) + the TMEM base slot
+static constexpr uint32_t kBarBytes = 512;
+static_assert(kBarBytes >= (2 * 8 + 2 * 2 + 2 + 2 * 4 + 2) * 8 + 4, "barrier area too small");
+
 static int pow2_cols(int n) {
     int c = 32;
     while (c < n) c <<= 1;
@@ -332,18 +339,23 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)P.BN * 64 * 2;
     const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
     const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64) * 4;
-    const uint32_t fixed = gamma_bytes + 256 + par_bytes + 1024;
+    const uint32_t fixed = gamma_bytes + kBarBytes + par_bytes + 1024;
     const uint32_t budget = 227u * 1024u;
     // halo mode: every stride-1 layer whose taps stay inside a 3x3 neighbourhood
     const bool stride1 = !gemm_l1 && (Ly.deconv || (Ly.k == 3 && Ly.s == 1));
-    const uint32_t hpb = ((10 * 18 * 128) + 1023) / 1024 * 1024;      // (Wt+2) x (Ht+2) rows
+    int halo_w = 10;                                                   // Wt + 2
+    if (const char* e = std::getenv("LIC_HALO_W")) halo_w = std::max(10, std::min(32, atoi(e)));
+    const uint32_t hpb = ((uint32_t)(halo_w * 18 * 128) + 1023) / 1024 * 1024;   // halo_w x (Ht+2) rows
     if (stride1 && fixed + 2 * P.split * hpb + 2 * b_bytes <= budget && c->halo_enabled) {
         P.halo = 1;
         P.Wt = 8; P.Ht = 16;
         P.halo_plane_bytes = hpb;
+        P.halo_w = halo_w;
         P.stage_bytes = b_bytes;
-        // deepest halo ring (<= 4 slots) that leaves room for >= 3 weight stages
-        int slots = 4;
+        // halo ring depth: env LIC_HALO_SLOTS (2..4, default 2: a halo chunk is reused by all
+        // its taps, while every tap needs a fresh weight tile, so smem goes to the weight ring)
+        int slots = 2;
+        if (const char* e = std::getenv("LIC_HALO_SLOTS")) slots = std::max(2, std::min(4, atoi(e)));
         while (slots > 2 && fixed + slots * P.split * hpb + 3 * b_bytes > budget) --slots;
         P.halo_slots = slots;
         // small weight sets (packed g_s L4: 9 taps x 2 chunks x 2 KB) stay resident
@@ -375,7 +387,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.tiles_x = (P.Wg + P.Wt - 1) / P.Wt;
     P.tiles_y = (P.Hg + P.Ht - 1) / P.Ht;
     P.off_bar = P.off_gamma + gamma_bytes;
-    P.off_par = P.off_bar + 256;
+    P.off_par = P.off_bar + kBarBytes;
     P.smem_bytes = P.off_par + par_bytes + 1024;
     if (P.smem_bytes < 120 * 1024) P.smem_bytes = 120 * 1024;     // one CTA per SM (TMEM)
     // TMEM plan: accumulator (+ GDN norm) per buffer, double-buffered when it fits
@@ -389,7 +401,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     const int cout_pad = P.BN * P.n_ntiles;
     if (!encode_act_map(&Ly.mapA, Ly.in_buf, P.Cin, Ly.deconv ? Ly.Win : (gemm_l1 ? Ly.Wout : Ly.Win),
                         Ly.deconv ? Ly.Hin : (gemm_l1 ? Ly.Hout : Ly.Hin), c->max_batch, P.split, Ly.in_plane,
-                        P.halo ? P.Wt + 2 : P.Wt, P.halo ? P.Ht + 2 : P.Ht, P.stride))
+                        P.halo ? P.halo_w : P.Wt, P.halo ? P.Ht + 2 : P.Ht, P.stride))
         return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (activations) failed");
     if (!encode_w_map(&Ly.mapB, Ly.w, P.Cin, cout_pad, ntaps_w, P.BN))
         return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (weights) failed");
@@ -418,6 +430,11 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
     P.total_tiles = batch * P.nphase * P.tiles_y * P.tiles_x * P.n_ntiles;
     const int grid = std::min(P.total_tiles, c->num_sms);
     const int lid = (int)(&Ly - c->layers);
+    if (c->trace_layer == lid && c->d_trace) {
+        P.trace = c->d_trace;
+        if (const char* e = std::getenv("LIC_DBG_NOSTORE")) P.dbg_nostore = atoi(e);
+        CK(cudaMemsetAsync(c->d_trace, 0, 256 * 8 * 8, st));
+    }
     if (c->profiling) {
         if (c->ev_used == kProfSlots) prof_flush(c);
         CK(cudaEventRecord(c->ev[2 * c->ev_used], st));
@@ -1023,5 +1040,23 @@ size_t lic_internal_frame_pixels(const lic_codec* c) { return c ? (size_t)c->H *
 extern "C" lic_status lic_set_zero_copy(lic_codec* c, int on) {
     if (!c) return LIC_EINVAL;
     c->zero_copy = on ? 1 : 0;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_trace(lic_codec* c, int layer_id, int on) {
+    if (!c || layer_id < 0 || layer_id >= NLAYER) return LIC_EINVAL;
+    if (on && !c->d_trace) {
+        lic_status r = dalloc(c, &c->d_trace, 256 * 8 * 8);
+        if (r) return r;
+    }
+    c->trace_layer = on ? layer_id : -1;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_trace_read(lic_codec* c, uint64_t* out, size_t n) {
+    if (!c || !out || !c->d_trace) return LIC_EINVAL;
+    cudaSetDevice(c->device);
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(out, c->d_trace, std::min<size_t>(n, 256 * 8) * 8, cudaMemcpyDeviceToHost));
     return LIC_OK;
 }

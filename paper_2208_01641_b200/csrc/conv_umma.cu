@@ -41,9 +41,13 @@ struct TileCoord { int b, ph, gy0, gx0, nt; };
 
 // Tile order: sub-pixel phase fastest, then N tile, x, y, frame -- the 4 phase tiles (and
 // the N tiles) of one location run on neighbouring CTAs and share their input via L2.
+// The phase is rotated by the location index: with a persistent grid whose size is a multiple
+// of 4, CTA c would otherwise always get phase c % 4 (9, 6, 6 or 4 taps) and the kernel
+// would run at the speed of its phase-0 CTAs.
 __device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t) {
     TileCoord c;
     c.ph = t % p.nphase;    t /= p.nphase;
+    if (p.nphase == 4) c.ph = (c.ph + t) & 3;
     c.nt = t % p.n_ntiles;  t /= p.n_ntiles;
     int tx = t % p.tiles_x; t /= p.tiles_x;
     int ty = t % p.tiles_y;
@@ -79,6 +83,17 @@ __device__ __forceinline__ int round_clamp(float v, int L, int& sat) {
     if (r < (float)-L) { r = (float)-L; ++sat; }
     return (int)r;
 }
+
+// test-only timeline: event e of the it-th tile of CTA 0 (kTraceEv slots per tile)
+constexpr int kTraceEv = 8;
+constexpr int kTraceTiles = 256;
+enum TraceEv { T_MMA_START = 0, T_MMA_END = 1, T_NORM_ISSUE = 2, T_EPI_START = 3, T_EPI_XSQ = 4,
+               T_EPI_NORM = 5, T_EPI_END = 6, T_PROD_START = 7 };
+#define LIC_TRACE(it, ev)                                                                         \
+    do {                                                                                          \
+        if (p.trace && blockIdx.x == 0 && (it) < kTraceTiles)                                     \
+            p.trace[(size_t)(it) * kTraceEv + (ev)] = (unsigned long long)clock64();              \
+    } while (0)
 
 // GC: GDN/IGDN layers only -- 16-column chunks per epilogue group (BN = 64*GC); 0 otherwise
 template <int GC>
@@ -173,9 +188,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         }
         int stage = 0;
         uint32_t phase = 0;
-        for (int t = blockIdx.x; t < p.total_tiles && !p.wres; t += gridDim.x) {
+        int pit = 0;
+        for (int t = blockIdx.x; t < p.total_tiles && !p.wres; t += gridDim.x, ++pit) {
             TileCoord tc = decode_tile(p, t);
             const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
+            if (lane == 0) LIC_TRACE(pit, T_PROD_START);
             if (p.halo) {
                 // chunk-outer, tap-inner weight tiles (halos come from warp 3)
                 for (int c = 0; c < p.kchunks; ++c)
@@ -215,7 +232,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         if (p.halo) {
             int hs = 0;
             uint32_t hphase = 0;
-            const uint32_t hbytes = (uint32_t)(p.Wt + 2) * (p.Ht + 2) * 128 * p.split;
+            const uint32_t hbytes = (uint32_t)p.halo_w * (p.Ht + 2) * 128 * p.split;
             for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
                 TileCoord tc = decode_tile(p, t);
                 for (int c = 0; c < p.kchunks; ++c) {
@@ -247,6 +264,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         int it = 0;
         int pend = 0;                       // a tile's norm MMAs are outstanding
         uint32_t pend_dcol = 0, xsq_phase = 0;
+        int pend_it = 0;
         bool gamma_ready = false;
         auto issue_norm = [&]() {
             if (!gamma_ready) { mbar_wait(gamma_bar, 0); gamma_ready = true; }
@@ -267,6 +285,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 umma_commit(norm_bar);
             }
             __syncwarp();
+            if (lane == 0) LIC_TRACE(pend_it, T_NORM_ISSUE);
             pend = 0;
         };
         int poll_ctr = 0;
@@ -284,10 +303,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (kGdn && pend && p.n_accbuf == 1) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; issue_norm(); }
             mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
             tc_fence_after();
+            if (lane == 0) LIC_TRACE(it, T_MMA_START);
             const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
             if (p.halo) {
                 const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
-                const uint32_t sbo = (uint32_t)(p.Wt + 2) * 128;
+                const uint32_t sbo = (uint32_t)p.halo_w * 128;
                 for (int c = 0; c < p.kchunks; ++c) {
                     mbar_wait(&hfull_bar[hs], hphase);
                     tc_fence_after();
@@ -302,7 +322,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             bsm = smem_u32(smem + stage * p.stage_bytes);
                         }
                         // window of this tap: halo row (dy+1)*(Wt+2) + (dx+1), 8-row groups every Wt+2 rows
-                        const uint32_t row0 = (uint32_t)((p.tap_dy[t0 + ti] + 1) * (p.Wt + 2) + p.tap_dx[t0 + ti] + 1);
+                        const uint32_t row0 = (uint32_t)((p.tap_dy[t0 + ti] + 1) * p.halo_w + p.tap_dx[t0 + ti] + 1);
                         const uint64_t ah = sdesc_sw128_sbo(hb + row0 * 128, sbo);
                         const uint64_t al = sdesc_sw128_sbo(hb + p.halo_plane_bytes + row0 * 128, sbo);
                         const uint64_t bd = sdesc_sw128(bsm);
@@ -347,10 +367,12 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             }
             if (elect_one()) umma_commit(&tfull_bar[buf]);
             __syncwarp();
+            if (lane == 0) LIC_TRACE(it, T_MMA_END);
             if (kGdn) {
                 // the previous tile's norm must be issued before this one becomes pending
                 if (pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; issue_norm(); }
                 pend = 1;
+                pend_it = it;
                 pend_dcol = (uint32_t)(buf * p.acc_stride);
             }
         }
@@ -373,6 +395,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (threadIdx.x == 128) mbar_wait(&tfull_bar[buf], use & 1);
             named_bar_sync(2, 32 * kEpiWarps);
             tc_fence_after();
+            if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_START);
             const uint32_t dcol = (uint32_t)(buf * p.acc_stride);
             const uint32_t taddr = tmem_base + lane_off + dcol;
 
@@ -419,10 +442,12 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(xsq_bar);       // the MMA warp issues the norm MMAs
+                if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_XSQ);
                 if (threadIdx.x == 128) mbar_wait(norm_bar, norm_phase);
                 norm_phase ^= 1;
                 named_bar_sync(3, 32 * kEpiWarps);
                 tc_fence_after();
+                if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_NORM);
                 __half* out = reinterpret_cast<__half*>(p.out_act);
 #pragma unroll
                 for (int j = 0; j < GC; ++j) {
@@ -448,7 +473,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                             for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(cb + i) * HWo] = x[j][i];
                         }
-                        if (out) {
+                        if (out && !p.dbg_nostore) {
 #pragma unroll
                             for (int qq = 0; qq < 2; ++qq)
                                 split_store8(out + pix * p.Cout + cb + qq * 8,
@@ -573,6 +598,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+            if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_END);
         }
         if (p.sat_count) {
             for (int o = 16; o > 0; o >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, o);

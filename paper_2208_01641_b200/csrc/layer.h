@@ -48,7 +48,7 @@ struct ConvParams {
     // per 64-channel chunk the (Ht+2) x (Wt+2) input halo (hi + lo) is loaded once into a
     // 2-slot ring and every tap reads its A operand as a shifted window of it; the stage
     // ring then carries only weight tiles.  Tile fixed at Wt = 8, Ht = 16.
-    int halo, halo_slots;
+    int halo, halo_slots, halo_w;      // halo_w: halo row pitch in pixels (>= Wt + 2)
     uint32_t off_halo, halo_plane_bytes;
     int wres;                         // all weight tiles resident in smem (loaded once per CTA)
     uint32_t off_wres;
@@ -71,6 +71,8 @@ struct ConvParams {
                                       // phases packed into N: column j = phase (j>>2), channel (j&3)
     int crop_top, crop_left, crop_H, crop_W;
     unsigned long long* sat_count;    // saturation counter (nullable)
+    unsigned long long* trace;        // test-only: per-tile clock64 events of CTA 0 (nullable)
+    int dbg_nostore;                  // test-only experiment switch: skip activation stores
 };
 
 }  // namespace lic

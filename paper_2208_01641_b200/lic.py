@@ -73,6 +73,8 @@ _L.lic_profile.argtypes = [_P, _i]
 _L.lic_profile_read.argtypes = [_P, _i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
 _L.lic_launch_count.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64)]
 _L.lic_set_zero_copy.argtypes = [_P, _i]
+_L.lic_trace.argtypes = [_P, _i, _i]
+_L.lic_trace_read.argtypes = [_P, _P, _sz]
 
 
 
@@ -324,6 +326,15 @@ class Codec:
             if _L.lic_profile_read(self._h, i, ctypes.byref(ms), ctypes.byref(n)) == 0 and n.value:
                 out[name] = (ms.value, n.value)
         return out
+
+    def trace(self, layer, on=True):
+        lid = LAYERS.index(layer) if isinstance(layer, str) else layer
+        self._chk(_L.lic_trace(self._h, lid, int(on)), "lic_trace")
+
+    def trace_read(self):
+        out = np.zeros(256 * 8, np.uint64)
+        self._chk(_L.lic_trace_read(self._h, _ptr(out), out.size), "lic_trace_read")
+        return out.reshape(256, 8)
 
     def launch_count(self):
         n = ctypes.c_uint64()
