@@ -28,8 +28,8 @@
 #include "layer.h"
 
 namespace lic {
-cudaError_t launch_conv_umma(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const ConvParams&, int,
-                             cudaStream_t);
+cudaError_t launch_conv_umma(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                             const CUtensorMap&, const ConvParams&, int, cudaStream_t);
 cudaError_t launch_ingest(const void*, int, int, int, int, int, int, int, int, __half*, size_t, int, cudaStream_t);
 cudaError_t launch_sym_ingest(const int8_t*, const float*, int, int, int, int, __half*, size_t, int, cudaStream_t);
 cudaError_t launch_pack_chw(const float*, int, int, int, int, __half*, size_t, int, cudaStream_t);
@@ -136,7 +136,7 @@ struct Layer {
     __half* out_buf = nullptr;
     size_t out_plane = 0;
     ConvParams prm{};
-    CUtensorMap mapA{}, mapB{}, mapG{};
+    CUtensorMap mapA{}, mapB{}, mapG{}, mapOH{}, mapOL{};
 };
 
 struct lic_codec {
@@ -163,6 +163,7 @@ struct lic_codec {
     int debug = 0;
     int zero_copy = 0;
     int halo_enabled = 1;          // LIC_NO_HALO=1 in the environment disables halo mode
+    int tma_out_enabled = 1;       // LIC_TMA_OUT=0 disables the TMA-store epilogue
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
     std::vector<void*> allocs;          // device allocations to free
@@ -260,6 +261,32 @@ static bool encode_w_map(CUtensorMap* m, const __half* base, int K, int rows, in
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// TMA-store maps of an NHWC fp16 plane, box = one epilogue warp's 32 px x 16 ch
+static bool encode_out_conv_map(CUtensorMap* m, const __half* base, int C, int W, int H, int B, int bw, int bh) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+    cuuint64_t str[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {16, (cuuint32_t)bw, (cuuint32_t)bh, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, (void*)base, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// sub-pixel phase view of a stride-2 transposed conv output (NHWC, H = 2 Hin, W = 2 Win):
+// dims (C, px, qx = x/2, py, qyb = b*Hin + y/2)
+static bool encode_out_phase_map(CUtensorMap* m, const __half* base, int C, int W, int H, int B, int bw, int bh) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[5] = {(cuuint64_t)C, 2, (cuuint64_t)(W / 2), 2, (cuuint64_t)B * (H / 2)};
+    cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)2 * C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)2 * W * C * 2};
+    cuuint32_t box[5] = {16, 1, (cuuint32_t)bw, 1, (cuuint32_t)bh};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, (void*)base, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // choose Wt x Ht = 128 minimising padded tiles over the grid
 static void choose_tile(int Hg, int Wg, int* Wt, int* Ht) {
     static const int opts[5][2] = {{16, 8}, {32, 4}, {8, 16}, {64, 2}, {128, 1}};
@@ -339,8 +366,19 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)P.BN * 64 * 2;
     const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
     const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64) * 4;
-    const uint32_t fixed = gamma_bytes + kBarBytes + par_bytes + 1024;
     const uint32_t budget = 227u * 1024u;
+    // TMA-store epilogue: 16 warps x 2 KB staging, when the layer writes an activation and the
+    // pipeline keeps >= 3 stages with it (env LIC_TMA_OUT=0 disables)
+    const bool has_act = Ly.out_buf != nullptr && Ly.ep != EP_SIGMA && Ly.ep != EP_FINAL;
+    bool tma_out = has_act && c->tma_out_enabled;
+    const uint32_t ostage_bytes = 16 * 2048;
+    {
+        const uint32_t fx = gamma_bytes + kBarBytes + par_bytes + 1024 + ostage_bytes;
+        const uint32_t st_b = a_bytes * P.split + b_bytes;     // per-tap stage (non-halo)
+        const bool stride1_ = !gemm_l1 && (Ly.deconv || (Ly.k == 3 && Ly.s == 1));
+        if (!stride1_ && fx + 3 * st_b > budget) tma_out = false;
+    }
+    const uint32_t fixed = gamma_bytes + kBarBytes + par_bytes + 1024 + (tma_out ? ostage_bytes : 0);
     // halo mode: every stride-1 layer whose taps stay inside a 3x3 neighbourhood
     const bool stride1 = !gemm_l1 && (Ly.deconv || (Ly.k == 3 && Ly.s == 1));
     int halo_w = 10;                                                   // Wt + 2
@@ -388,7 +426,9 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.tiles_y = (P.Hg + P.Ht - 1) / P.Ht;
     P.off_bar = P.off_gamma + gamma_bytes;
     P.off_par = P.off_bar + kBarBytes;
-    P.smem_bytes = P.off_par + par_bytes + 1024;
+    P.tma_out = tma_out ? 1 : 0;
+    P.off_ostage = (P.off_par + par_bytes + 1023) / 1024 * 1024;
+    P.smem_bytes = (tma_out ? P.off_ostage + ostage_bytes : P.off_par + par_bytes) + 1024;
     if (P.smem_bytes < 120 * 1024) P.smem_bytes = 120 * 1024;     // one CTA per SM (TMEM)
     // TMEM plan: accumulator (+ GDN norm) per buffer, double-buffered when it fits
     int per = std::max(32, P.BN) + (gdn ? P.BN : 0);
@@ -410,6 +450,19 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
             return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (gamma) failed");
     } else {
         Ly.mapG = Ly.mapB;
+    }
+    Ly.mapOH = Ly.mapB;
+    Ly.mapOL = Ly.mapB;
+    if (P.tma_out) {
+        const int bw = P.Wt < 32 ? P.Wt : 32, bh = 32 / bw;
+        bool ok;
+        if (P.nphase == 1)
+            ok = encode_out_conv_map(&Ly.mapOH, Ly.out_buf, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh) &&
+                 encode_out_conv_map(&Ly.mapOL, Ly.out_buf + Ly.out_plane, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh);
+        else
+            ok = encode_out_phase_map(&Ly.mapOH, Ly.out_buf, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh) &&
+                 encode_out_phase_map(&Ly.mapOL, Ly.out_buf + Ly.out_plane, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh);
+        if (!ok) return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (output) failed");
     }
     // epilogue constants
     P.ep = Ly.ep;
@@ -439,7 +492,7 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
         if (c->ev_used == kProfSlots) prof_flush(c);
         CK(cudaEventRecord(c->ev[2 * c->ev_used], st));
     }
-    CK(launch_conv_umma(Ly.mapA, Ly.mapB, Ly.mapG, P, grid, st));
+    CK(launch_conv_umma(Ly.mapA, Ly.mapB, Ly.mapG, Ly.mapOH, Ly.mapOL, P, grid, st));
     ++c->launches;
     if (c->profiling) {
         CK(cudaEventRecord(c->ev[2 * c->ev_used + 1], st));
@@ -561,6 +614,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(LIC_ECUDA);
     c->split = precision == LIC_PREC_SPLIT ? 2 : 1;
     if (const char* e = std::getenv("LIC_NO_HALO")) c->halo_enabled = (e[0] == '0');
+    if (const char* e = std::getenv("LIC_TMA_OUT")) c->tma_out_enabled = (e[0] != '0');
     c->max_batch = (int)max_batch;
     c->H = (int)height; c->W = (int)width;
     const int P = c->kind == 1 ? 64 : 16;

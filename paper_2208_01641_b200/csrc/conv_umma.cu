@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                  const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ CUtensorMap mapG,
+                 const __grid_constant__ CUtensorMap mapOH,
+                 const __grid_constant__ CUtensorMap mapOL,
                  const __grid_constant__ ConvParams p)
 {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -408,6 +410,53 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const size_t HWo = (size_t)p.Hout * p.Wout;
             const size_t chw0 = (size_t)tc.b * p.Cout * HWo + (size_t)oy * p.Wout + ox;
             const int co0 = tc.nt * p.BN;
+            // this warp's 32 pixels form a bw x bh box at tile offset (tx0, ty0)
+            const int bw = p.Wt < 32 ? p.Wt : 32, bh = 32 / bw;
+            const int ty0 = (q * 32) / p.Wt, tx0 = (q * 32) % p.Wt;
+            const bool tma_ok = p.tma_out && (p.nphase == 1 || tc.gy0 + ty0 + bh <= p.Hg);
+            uint8_t* ostage = smem + p.off_ostage + (warp - 4) * 2048;
+            // 16 channels [cb, cb+16) of this thread's pixel -> fp16 hi/lo NHWC activation
+            auto emit16 = [&](const float* v16, int cb) {
+                __half* out = reinterpret_cast<__half*>(p.out_act);
+                if (tma_ok) {
+                    if (lane == 0) bulk_wait_read0();        // previous store has read the stage
+                    __syncwarp();
+                    uint4 h0, h1, l0, l1;
+                    h0.x = h2_bits(v16[0], v16[1]);   h0.y = h2_bits(v16[2], v16[3]);
+                    h0.z = h2_bits(v16[4], v16[5]);   h0.w = h2_bits(v16[6], v16[7]);
+                    h1.x = h2_bits(v16[8], v16[9]);   h1.y = h2_bits(v16[10], v16[11]);
+                    h1.z = h2_bits(v16[12], v16[13]); h1.w = h2_bits(v16[14], v16[15]);
+                    float lv[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) lv[i] = v16[i] - hround(v16[i]);
+                    l0.x = h2_bits(lv[0], lv[1]);   l0.y = h2_bits(lv[2], lv[3]);
+                    l0.z = h2_bits(lv[4], lv[5]);   l0.w = h2_bits(lv[6], lv[7]);
+                    l1.x = h2_bits(lv[8], lv[9]);   l1.y = h2_bits(lv[10], lv[11]);
+                    l1.z = h2_bits(lv[12], lv[13]); l1.w = h2_bits(lv[14], lv[15]);
+                    reinterpret_cast<uint4*>(ostage)[2 * lane] = h0;
+                    reinterpret_cast<uint4*>(ostage)[2 * lane + 1] = h1;
+                    reinterpret_cast<uint4*>(ostage + 1024)[2 * lane] = l0;
+                    reinterpret_cast<uint4*>(ostage + 1024)[2 * lane + 1] = l1;
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (p.nphase == 1) {
+                            tma_store_4d(&mapOH, ostage, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b);
+                            if (p.split == 2) tma_store_4d(&mapOL, ostage + 1024, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b);
+                        } else {
+                            const int qyb = tc.b * p.Hg + tc.gy0 + ty0;
+                            tma_store_5d(&mapOH, ostage, cb, px, tc.gx0 + tx0, py, qyb);
+                            if (p.split == 2) tma_store_5d(&mapOL, ostage + 1024, cb, px, tc.gx0 + tx0, py, qyb);
+                        }
+                        bulk_commit();
+                    }
+                    __syncwarp();
+                } else if (valid) {
+                    split_store8(out + pix * p.Cout + cb, p.split == 2 ? out + p.act_plane + pix * p.Cout + cb : nullptr, v16);
+                    split_store8(out + pix * p.Cout + cb + 8, p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + 8 : nullptr,
+                                 v16 + 8);
+                }
+            };
 
             if constexpr (kGdn) {
                 constexpr int G = 16 * GC;                   // channels of this group
@@ -468,19 +517,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             x[j][i] = (p.ep == EP_GDN) ? x[j][i] * rs : x[j][i] * (nn * rs);
                         }
                     }
-                    if (valid) {
-                        if (p.out_f32) {
+                    if (valid && p.out_f32) {
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(cb + i) * HWo] = x[j][i];
-                        }
-                        if (out && !p.dbg_nostore) {
-#pragma unroll
-                            for (int qq = 0; qq < 2; ++qq)
-                                split_store8(out + pix * p.Cout + cb + qq * 8,
-                                             p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + qq * 8 : nullptr,
-                                             x[j] + qq * 8);
-                        }
+                        for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(cb + i) * HWo] = x[j][i];
                     }
+                    if (out && !p.dbg_nostore) emit16(x[j], cb);
                 }
             } else {
                 const int ncol16 = (p.BN + 15) / 16;
@@ -489,109 +530,102 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     __syncwarp();
                     tmem_ld16(taddr + c * 16, v);
                     const int cb = co0 + c * 16;
-                    if (valid && cb < p.Cout) {
-                        const int nj = p.pack4 ? 16 : min(16, p.Cout - cb);
-                        if (p.pack4) {
+                    if (cb >= p.Cout) continue;                       // warp-uniform
+                    const int nj = p.pack4 ? 16 : min(16, p.Cout - cb);
+                    if (p.pack4) {
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) v[j] += s_bias[j & 3];
-                        } else {
-                            const float4* b4 = reinterpret_cast<const float4*>(s_bias + cb);
+                        for (int j = 0; j < 16; ++j) v[j] += s_bias[j & 3];
+                    } else {
+                        const float4* b4 = reinterpret_cast<const float4*>(s_bias + cb);
 #pragma unroll
-                            for (int i4 = 0; i4 < 4; ++i4) {
-                                const float4 bb = b4[i4];
-                                v[4 * i4 + 0] += bb.x; v[4 * i4 + 1] += bb.y; v[4 * i4 + 2] += bb.z; v[4 * i4 + 3] += bb.w;
-                            }
+                        for (int i4 = 0; i4 < 4; ++i4) {
+                            const float4 bb = b4[i4];
+                            v[4 * i4 + 0] += bb.x; v[4 * i4 + 1] += bb.y; v[4 * i4 + 2] += bb.z; v[4 * i4 + 3] += bb.w;
                         }
-                        switch (p.ep) {
-                        case EP_F32: {
+                    }
+                    switch (p.ep) {
+                    case EP_F32: {
+                        if (valid) {
 #pragma unroll
                             for (int j = 0; j < 16; ++j)
                                 if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
-                            break;
                         }
-                        case EP_RELU: {
-                            __half* out = reinterpret_cast<__half*>(p.out_act);
+                        break;
+                    }
+                    case EP_RELU: {
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.0f);
-                            if (p.out_f32) {
+                        for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.0f);
+                        if (valid && p.out_f32) {
 #pragma unroll
-                                for (int j = 0; j < 16; ++j)
-                                    if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
-                            }
-#pragma unroll
-                            for (int qq = 0; qq < 2; ++qq)
-                                split_store8(out + pix * p.Cout + cb + qq * 8,
-                                             p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + qq * 8 : nullptr,
-                                             v + qq * 8);
-                            break;
+                            for (int j = 0; j < 16; ++j)
+                                if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
                         }
-                        case EP_YQUANT:
-                        case EP_ZQUANT: {
-                            int8_t* sym = reinterpret_cast<int8_t*>(p.out_sym);
-                            float av[16];
+                        emit16(v, cb);
+                        break;
+                    }
+                    case EP_YQUANT:
+                    case EP_ZQUANT: {
+                        int8_t* sym = reinterpret_cast<int8_t*>(p.out_sym);
+                        float av[16];
+                        int vsat = 0;
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                const float m = s_mu[cb + j];
-                                const int s = (j < nj) ? round_clamp(v[j] - m, p.L, sat) : 0;
-                                if (j < nj) sym[chw0 + (size_t)(cb + j) * HWo] = (int8_t)s;
-                                av[j] = (p.ep == EP_YQUANT) ? fabsf(v[j]) : (float)s + m;
-                            }
-                            if (p.out_f32) {
-#pragma unroll
-                                for (int j = 0; j < 16; ++j)
-                                    if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
-                            }
-                            if (p.out_act && (p.ep == EP_ZQUANT || p.abs_out)) {
-                                __half* out = reinterpret_cast<__half*>(p.out_act);
-#pragma unroll
-                                for (int qq = 0; qq < 2; ++qq)
-                                    split_store8(out + pix * p.Cout + cb + qq * 8,
-                                                 p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + qq * 8 : nullptr,
-                                                 av + qq * 8);
-                            }
-                            break;
+                        for (int j = 0; j < 16; ++j) {
+                            const float m = s_mu[cb + j];
+                            const int s = round_clamp(v[j] - m, p.L, vsat);
+                            if (valid && j < nj) sym[chw0 + (size_t)(cb + j) * HWo] = (int8_t)s;
+                            av[j] = (p.ep == EP_YQUANT) ? fabsf(v[j]) : (float)s + m;
                         }
-                        case EP_SIGMA: {
-                            uint8_t* idx = reinterpret_cast<uint8_t*>(p.out_sym);
+                        if (valid) sat += vsat;
+                        if (valid && p.out_f32) {
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                if (j >= nj) continue;
-                                float s = fmaxf(v[j], 0.0f);
-                                if (p.out_f32) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = s;
-                                s = fmaxf(s, 0.11f);
-                                // #{ j in [0, 62] : table_j < s }: binary search over the sorted table
-                                int lo_i = 0, hi_i = 63;
+                            for (int j = 0; j < 16; ++j)
+                                if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = v[j];
+                        }
+                        if (p.out_act && (p.ep == EP_ZQUANT || p.abs_out)) emit16(av, cb);
+                        break;
+                    }
+                    case EP_SIGMA: {
+                        if (!valid) break;
+                        uint8_t* idx = reinterpret_cast<uint8_t*>(p.out_sym);
 #pragma unroll
-                                for (int step = 0; step < 6; ++step) {
-                                    const int mid = (lo_i + hi_i) >> 1;
-                                    if (s_tab[mid] < s) lo_i = mid + 1; else hi_i = mid;
-                                }
-                                idx[chw0 + (size_t)(cb + j) * HWo] = (uint8_t)lo_i;
+                        for (int j = 0; j < 16; ++j) {
+                            if (j >= nj) continue;
+                            float s = fmaxf(v[j], 0.0f);
+                            if (p.out_f32) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = s;
+                            s = fmaxf(s, 0.11f);
+                            // #{ j in [0, 62] : table_j < s }: binary search over the sorted table
+                            int lo_i = 0, hi_i = 63;
+#pragma unroll
+                            for (int step = 0; step < 6; ++step) {
+                                const int mid = (lo_i + hi_i) >> 1;
+                                if (s_tab[mid] < s) lo_i = mid + 1; else hi_i = mid;
                             }
-                            break;
+                            idx[chw0 + (size_t)(cb + j) * HWo] = (uint8_t)lo_i;
                         }
-                        case EP_FINAL: {
+                        break;
+                    }
+                    case EP_FINAL: {
+                        if (!valid) break;
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                if (j >= nj) continue;
-                                // packed phases: column j -> sub-pixel (j>>2) of grid pixel (gy, gx), channel j&3
-                                const int ch = p.pack4 ? (j & 3) : cb + j;
-                                if (p.pack4 && ch >= 3) continue;
-                                const int yy = p.pack4 ? 2 * gy + ((j >> 3) & 1) : oy;
-                                const int xx = p.pack4 ? 2 * gx + ((j >> 2) & 1) : ox;
-                                const int ry = yy - p.crop_top, rx = xx - p.crop_left;
-                                if (ry < 0 || ry >= p.crop_H || rx < 0 || rx >= p.crop_W) continue;
-                                const float xv = fminf(fmaxf(v[j], 0.0f), 1.0f);
-                                if (p.out_f32)
-                                    p.out_f32[(((size_t)tc.b * 3 + ch) * p.crop_H + ry) * p.crop_W + rx] = xv;
-                                if (p.out_u8)
-                                    p.out_u8[(((size_t)tc.b * p.crop_H + ry) * p.crop_W + rx) * 3 + ch] =
-                                        (uint8_t)roundf(xv * 255.0f);
-                            }
-                            break;
+                        for (int j = 0; j < 16; ++j) {
+                            if (j >= nj) continue;
+                            // packed phases: column j -> sub-pixel (j>>2) of grid pixel (gy, gx), channel j&3
+                            const int ch = p.pack4 ? (j & 3) : cb + j;
+                            if (p.pack4 && ch >= 3) continue;
+                            const int yy = p.pack4 ? 2 * gy + ((j >> 3) & 1) : oy;
+                            const int xx = p.pack4 ? 2 * gx + ((j >> 2) & 1) : ox;
+                            const int ry = yy - p.crop_top, rx = xx - p.crop_left;
+                            if (ry < 0 || ry >= p.crop_H || rx < 0 || rx >= p.crop_W) continue;
+                            const float xv = fminf(fmaxf(v[j], 0.0f), 1.0f);
+                            if (p.out_f32)
+                                p.out_f32[(((size_t)tc.b * 3 + ch) * p.crop_H + ry) * p.crop_W + rx] = xv;
+                            if (p.out_u8)
+                                p.out_u8[(((size_t)tc.b * p.crop_H + ry) * p.crop_W + rx) * 3 + ch] =
+                                    (uint8_t)roundf(xv * 255.0f);
                         }
-                        default: break;
-                        }
+                        break;
+                    }
+                    default: break;
                     }
                 }
             }
@@ -600,6 +634,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (lane == 0) mbar_arrive(&tempty_bar[buf]);
             if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_END);
         }
+        if (p.tma_out && lane == 0) bulk_wait0();
         if (p.sat_count) {
             for (int o = 16; o > 0; o >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, o);
             if (lane == 0 && sat) atomicAdd(p.sat_count, (unsigned long long)sat);
@@ -616,7 +651,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 
 template <int GC>
 static cudaError_t launch_t(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
-                            const ConvParams& p, int grid, cudaStream_t stream) {
+                            const CUtensorMap& mapOH, const CUtensorMap& mapOL, const ConvParams& p, int grid,
+                            cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -624,17 +660,18 @@ static cudaError_t launch_t(const CUtensorMap& mapA, const CUtensorMap& mapB, co
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    conv_umma_kernel<GC><<<grid, kThreads, p.smem_bytes, stream>>>(mapA, mapB, mapG, p);
+    conv_umma_kernel<GC><<<grid, kThreads, p.smem_bytes, stream>>>(mapA, mapB, mapG, mapOH, mapOL, p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_conv_umma(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
-                             const ConvParams& p, int grid, cudaStream_t stream) {
+                             const CUtensorMap& mapOH, const CUtensorMap& mapOL, const ConvParams& p, int grid,
+                             cudaStream_t stream) {
     const bool gdn = (p.ep == EP_GDN || p.ep == EP_IGDN);
-    if (!gdn) return launch_t<0>(mapA, mapB, mapG, p, grid, stream);
+    if (!gdn) return launch_t<0>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
     switch (p.BN) {      // GDN channel counts of the configs: N = 128, 192
-    case 128: return launch_t<2>(mapA, mapB, mapG, p, grid, stream);
-    case 192: return launch_t<3>(mapA, mapB, mapG, p, grid, stream);
+    case 128: return launch_t<2>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+    case 192: return launch_t<3>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -73,6 +73,11 @@ struct ConvParams {
     unsigned long long* sat_count;    // saturation counter (nullable)
     unsigned long long* trace;        // test-only: per-tile clock64 events of CTA 0 (nullable)
     int dbg_nostore;                  // test-only experiment switch: skip activation stores
+    // TMA-store epilogue: each epilogue warp stages 32 px x 16 ch (hi, lo: 1 KB each) in smem and
+    // writes it with a bulk tensor store; out maps: conv (C, W, H, B), deconv phase view
+    // (C, px, W/2, py, B*H/2) of the NHWC output, one map per plane
+    int tma_out;
+    uint32_t off_ostage;
 };
 
 }  // namespace lic
