@@ -164,6 +164,7 @@ struct lic_codec {
     int zero_copy = 0;
     int halo_enabled = 1;          // LIC_NO_HALO=1 in the environment disables halo mode
     int tma_out_enabled = 1;       // LIC_TMA_OUT=0 disables the TMA-store epilogue
+    int cg_enabled = 1;            // LIC_CG=1 forces one CTA per tile (no cta_group::2 pairs)
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
     std::vector<void*> allocs;          // device allocations to free
@@ -362,8 +363,11 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
             P.ntaps[ph] = ntap - P.tap0[ph];
         }
     }
+    // CTA pair (cta_group::2, M = 256) unless disabled (env LIC_CG=1); B / gamma split by rows
+    // (N tiles >= 64 only: the packed N = 16 g_s L4 stays on one CTA per tile)
+    P.cg = (c->cg_enabled && P.BN % 16 == 0 && P.BN >= 64) ? 2 : 1;
     // shared memory plan: stage ring | halo ring (halo mode) | gamma (GDN) | mbarriers | constants
-    const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)P.BN * 64 * 2;
+    const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)(P.BN / P.cg) * 64 * 2;
     const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
     const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64) * 4;
     const uint32_t budget = 227u * 1024u;
@@ -427,9 +431,30 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.off_bar = P.off_gamma + gamma_bytes;
     P.off_par = P.off_bar + kBarBytes;
     P.tma_out = tma_out ? 1 : 0;
+    P.ostage_slots = 1;
     P.off_ostage = (P.off_par + par_bytes + 1023) / 1024 * 1024;
     P.smem_bytes = (tma_out ? P.off_ostage + ostage_bytes : P.off_par + par_bytes) + 1024;
+    // double-buffered staging when it fits without losing pipeline depth below 3 (halo: 2) stages
+    if (tma_out && P.smem_bytes + ostage_bytes <= budget) {
+        const bool keep = P.halo ? (P.wres || P.stages >= 2) : P.stages >= 3;
+        if (keep) { P.ostage_slots = 2; P.smem_bytes += ostage_bytes; }
+    } else if (tma_out && P.halo && !P.wres && P.stage_bytes) {
+        // trade weight stages (keeping >= 2) for the second staging slot
+        const int drop = (int)((ostage_bytes + P.stage_bytes - 1) / P.stage_bytes);
+        if (P.stages - drop >= 2) {
+            const uint32_t sh = (uint32_t)drop * P.stage_bytes;
+            P.stages -= drop;
+            P.off_halo -= sh;
+            P.off_gamma -= sh;
+            P.off_bar -= sh;
+            P.off_par -= sh;
+            P.off_ostage = (P.off_par + par_bytes + 1023) / 1024 * 1024;
+            P.ostage_slots = 2;
+            P.smem_bytes = P.off_ostage + 2 * ostage_bytes + 1024;
+        }
+    }
     if (P.smem_bytes < 120 * 1024) P.smem_bytes = 120 * 1024;     // one CTA per SM (TMEM)
+    if (P.smem_bytes > budget) return fail(c, LIC_EINVAL, "layer plan exceeds shared memory (%u)", P.smem_bytes);
     // TMEM plan: accumulator (+ GDN norm) per buffer, double-buffered when it fits
     int per = std::max(32, P.BN) + (gdn ? P.BN : 0);
     P.n_accbuf = (2 * per <= 512) ? 2 : 1;
@@ -443,10 +468,10 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
                         Ly.deconv ? Ly.Hin : (gemm_l1 ? Ly.Hout : Ly.Hin), c->max_batch, P.split, Ly.in_plane,
                         P.halo ? P.halo_w : P.Wt, P.halo ? P.Ht + 2 : P.Ht, P.stride))
         return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (activations) failed");
-    if (!encode_w_map(&Ly.mapB, Ly.w, P.Cin, cout_pad, ntaps_w, P.BN))
+    if (!encode_w_map(&Ly.mapB, Ly.w, P.Cin, cout_pad, ntaps_w, P.BN / P.cg))
         return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (weights) failed");
     if (gdn) {
-        if (!encode_w_map(&Ly.mapG, Ly.gamma, Ly.Cout, Ly.Cout, 1, Ly.Cout))
+        if (!encode_w_map(&Ly.mapG, Ly.gamma, Ly.Cout, Ly.Cout, 1, Ly.Cout / P.cg))
             return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (gamma) failed");
     } else {
         Ly.mapG = Ly.mapB;
@@ -480,8 +505,9 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
 static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int batch, cudaStream_t st) {
     ConvParams P = P0;
     P.batch = batch;
-    P.total_tiles = batch * P.nphase * P.tiles_y * P.tiles_x * P.n_ntiles;
-    const int grid = std::min(P.total_tiles, c->num_sms);
+    const int txs = (P.tiles_x + P.cg - 1) / P.cg;          // tiles (or CTA-pair tiles) along x
+    P.total_tiles = batch * P.nphase * P.tiles_y * txs * P.n_ntiles;
+    const int grid = P.cg * std::min(P.total_tiles, c->num_sms / P.cg);
     const int lid = (int)(&Ly - c->layers);
     if (c->trace_layer == lid && c->d_trace) {
         P.trace = c->d_trace;
@@ -492,7 +518,12 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
         if (c->ev_used == kProfSlots) prof_flush(c);
         CK(cudaEventRecord(c->ev[2 * c->ev_used], st));
     }
-    CK(launch_conv_umma(Ly.mapA, Ly.mapB, Ly.mapG, Ly.mapOH, Ly.mapOL, P, grid, st));
+    {
+        const cudaError_t e = launch_conv_umma(Ly.mapA, Ly.mapB, Ly.mapG, Ly.mapOH, Ly.mapOL, P, grid, st);
+        if (e != cudaSuccess)
+            return fail(c, LIC_ECUDA, "launch of layer %d (grid %d, cg %d, smem %u, tiles %d, stages %d, halo %d): %s",
+                        lid, grid, P.cg, P.smem_bytes, P.total_tiles, P.stages, P.halo, cudaGetErrorString(e));
+    }
     ++c->launches;
     if (c->profiling) {
         CK(cudaEventRecord(c->ev[2 * c->ev_used + 1], st));
@@ -615,6 +646,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     c->split = precision == LIC_PREC_SPLIT ? 2 : 1;
     if (const char* e = std::getenv("LIC_NO_HALO")) c->halo_enabled = (e[0] == '0');
     if (const char* e = std::getenv("LIC_TMA_OUT")) c->tma_out_enabled = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_CG")) c->cg_enabled = (e[0] != '1');
     c->max_batch = (int)max_batch;
     c->H = (int)height; c->W = (int)width;
     const int P = c->kind == 1 ? 64 : 16;

@@ -44,12 +44,14 @@ struct TileCoord { int b, ph, gy0, gx0, nt; };
 // The phase is rotated by the location index: with a persistent grid whose size is a multiple
 // of 4, CTA c would otherwise always get phase c % 4 (9, 6, 6 or 4 taps) and the kernel
 // would run at the speed of its phase-0 CTAs.
-__device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t) {
+// CTA pairs (p.cg = 2) take two horizontally adjacent tiles: rank r gets tile 2*txp + r.
+__device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t, int rank) {
     TileCoord c;
     c.ph = t % p.nphase;    t /= p.nphase;
     if (p.nphase == 4) c.ph = (c.ph + t) & 3;
     c.nt = t % p.n_ntiles;  t /= p.n_ntiles;
-    int tx = t % p.tiles_x; t /= p.tiles_x;
+    const int txs = (p.tiles_x + p.cg - 1) / p.cg;
+    int tx = (t % txs) * p.cg + rank; t /= txs;
     int ty = t % p.tiles_y;
     c.b = t / p.tiles_y;
     c.gx0 = tx * p.Wt;
@@ -95,8 +97,11 @@ enum TraceEv { T_MMA_START = 0, T_MMA_END = 1, T_NORM_ISSUE = 2, T_EPI_START = 3
             p.trace[(size_t)(it) * kTraceEv + (ev)] = (unsigned long long)clock64();              \
     } while (0)
 
-// GC: GDN/IGDN layers only -- 16-column chunks per epilogue group (BN = 64*GC); 0 otherwise
-template <int GC>
+// GC: GDN/IGDN layers only -- 16-column chunks per epilogue group (BN = 64*GC); 0 otherwise.
+// CG: 1 = one CTA per 128-pixel tile; 2 = CTA pair (cluster of 2, tcgen05 cta_group::2, M = 256):
+//     each CTA loads its own A (or halo) and half of B / gamma, the leader issues the MMAs and
+//     commits to both CTAs' barriers, the peer's epilogue arrives remotely on the leader's.
+template <int GC, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                  const __grid_constant__ CUtensorMap mapB,
@@ -119,6 +124,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     uint64_t* xsq_bar = hempty_bar + 4;             // epilogue -> MMA warp: x^2 written to TMEM
     uint64_t* wres_bar = xsq_bar + 1;               // resident weights landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wres_bar + 1);
+    uint32_t* xsq_cnt = tmem_slot + 1;              // epilogue warps that wrote x^2 (cumulative)
     float* s_bias = reinterpret_cast<float*>(smem + p.off_par);   // [cout_pad]
     float* s_beta = s_bias + p.BN * p.n_ntiles;                     // [cout_pad]
     float* s_mu = s_beta + p.BN * p.n_ntiles;                       // [cout_pad]
@@ -127,15 +133,21 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     constexpr bool kGdn = GC > 0;
+    const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
+    const bool leader = rank == 0;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;     // pair (or CTA) index and count
+    // barrier address the TMA / epilogue arrivals target: the leader CTA's copy
+    auto lbar = [&](uint64_t* b) -> uint32_t { return CG == 2 ? mapa_shared(smem_u32(b), 0) : smem_u32(b); };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], kEpiWarps); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], kEpiWarps * CG); }
         mbar_init(norm_bar, 1);
         mbar_init(gamma_bar, 1);
         for (int i = 0; i < 4; ++i) { mbar_init(&hfull_bar[i], 1); mbar_init(&hempty_bar[i], 1); }
-        mbar_init(xsq_bar, kEpiWarps);
+        mbar_init(xsq_bar, kEpiWarps * CG);
         mbar_init(wres_bar, 1);
+        *xsq_cnt = 0;
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -143,7 +155,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         tma_prefetch_desc(&mapB);
         if (kGdn) tma_prefetch_desc(&mapG);
     }
-    if (warp == 2) tmem_alloc(tmem_slot, (uint32_t)p.tmem_cols);
+    if (warp == 2) {
+        if constexpr (CG == 2) tmem_alloc_cg2(tmem_slot, (uint32_t)p.tmem_cols);
+        else tmem_alloc(tmem_slot, (uint32_t)p.tmem_cols);
+    }
     if (warp >= 4) {
         // per-channel epilogue constants, staged once per CTA
         const int np = p.BN * p.n_ntiles;
@@ -156,13 +171,34 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         for (int i = threadIdx.x - 128; i < 64; i += 32 * kEpiWarps) s_tab[i] = p.table ? p.table[i] : 0.0f;
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     const uint32_t a_bytes = kBM * kBK * 2;          // 16 KB per activation plane
-    const uint32_t b_bytes = (uint32_t)p.BN * kBK * 2;
-    const uint32_t idesc = idesc_f16_f32(kBM, (uint32_t)p.BN);
+    const int bnc = p.BN / CG;                        // B (and gamma) rows held by this CTA
+    const uint32_t b_bytes = (uint32_t)bnc * kBK * 2;
+    const uint32_t idesc = idesc_f16_f32(kBM * CG, (uint32_t)p.BN);
+    // TMA into this CTA's smem, completing bytes on the leader's barrier (CG = 2)
+    auto ld3 = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+        if constexpr (CG == 2) tma_load_3d_cg2(dst, m, lbar(bar), c0, c1, c2);
+        else tma_load_3d(dst, m, bar, c0, c1, c2);
+    };
+    auto ld5 = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3, int c4) {
+        if constexpr (CG == 2) tma_load_5d_cg2(dst, m, lbar(bar), c0, c1, c2, c3, c4);
+        else tma_load_5d(dst, m, bar, c0, c1, c2, c3, c4);
+    };
+    // the leader expects the bytes of both CTAs; the peer's loads only complete_tx
+    auto expect = [&](uint64_t* bar, uint32_t bytes) { if (leader) mbar_arrive_expect_tx(bar, bytes * CG); };
+    auto commit = [&](uint64_t* bar) {
+        if constexpr (CG == 2) umma_commit_pair(bar); else umma_commit(bar);
+    };
+    auto mma_ss = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+        if constexpr (CG == 2) umma_f16_cg2(d, a, b, idesc, acc); else umma_f16(d, a, b, idesc, acc);
+    };
+    auto mma_ts = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t acc) {
+        if constexpr (CG == 2) umma_f16_ts_cg2(d, a, b, idesc, acc); else umma_f16_ts(d, a, b, idesc, acc);
+    };
 
     if (warp == 0) {
         // ====================== TMA producer (weights; activations unless halo mode) ======================
@@ -170,9 +206,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         if (kGdn) {
             // gamma (Cout x Cout fp16, K-major rows; BN/64 = GC chunks of 64 columns), resident
             if (elect_one()) {
-                mbar_arrive_expect_tx(gamma_bar, (uint32_t)GC * b_bytes);
-                for (int c = 0; c < GC; ++c)
-                    tma_load_3d(smem + p.off_gamma + c * b_bytes, &mapG, gamma_bar, c * kBK, 0, 0);
+                expect(gamma_bar, (uint32_t)GC * b_bytes);
+                for (int c = 0; c < GC; ++c)         // this CTA's half of gamma's rows (CG = 2)
+                    ld3(smem + p.off_gamma + c * b_bytes, &mapG, gamma_bar, c * kBK, rank * bnc, 0);
             }
             __syncwarp();
         }
@@ -180,10 +216,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             // every (tap, chunk) weight tile, once per CTA: tile (w, c) at (w * kchunks + c) * b_bytes
             if (elect_one()) {
                 const int nw = p.ntaps[0];
-                mbar_arrive_expect_tx(wres_bar, (uint32_t)(nw * p.kchunks) * b_bytes);
+                expect(wres_bar, (uint32_t)(nw * p.kchunks) * b_bytes);
                 for (int w = 0; w < nw; ++w)
                     for (int c = 0; c < p.kchunks; ++c)
-                        tma_load_3d(smem + p.off_wres + (w * p.kchunks + c) * b_bytes, &mapB, wres_bar, c * kBK, 0,
+                        ld3(smem + p.off_wres + (w * p.kchunks + c) * b_bytes, &mapB, wres_bar, c * kBK, rank * bnc,
                                     p.tap_w[w]);
             }
             __syncwarp();
@@ -191,8 +227,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         int stage = 0;
         uint32_t phase = 0;
         int pit = 0;
-        for (int t = blockIdx.x; t < p.total_tiles && !p.wres; t += gridDim.x, ++pit) {
-            TileCoord tc = decode_tile(p, t);
+        for (int t = cid; t < p.total_tiles && !p.wres; t += ncl, ++pit) {
+            TileCoord tc = decode_tile(p, t, rank);
             const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
             if (lane == 0) LIC_TRACE(pit, T_PROD_START);
             if (p.halo) {
@@ -201,9 +237,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     for (int ti = 0; ti < nt; ++ti) {
                         mbar_wait(&empty_bar[stage], phase ^ 1);
                         if (elect_one()) {
-                            mbar_arrive_expect_tx(&full_bar[stage], b_bytes);
-                            tma_load_3d(smem + stage * p.stage_bytes, &mapB, &full_bar[stage], c * kBK,
-                                        tc.nt * p.BN, p.tap_w[t0 + ti]);
+                            expect(&full_bar[stage], b_bytes);
+                            ld3(smem + stage * p.stage_bytes, &mapB, &full_bar[stage], c * kBK,
+                                tc.nt * p.BN + rank * bnc, p.tap_w[t0 + ti]);
                         }
                         __syncwarp();
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
@@ -218,11 +254,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* st = smem + stage * p.stage_bytes;
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(&full_bar[stage], a_bytes * p.split + b_bytes);
-                        tma_load_5d(st, &mapA, &full_bar[stage], c * kBK, x0, y0, tc.b, 0);
-                        if (p.split == 2)
-                            tma_load_5d(st + a_bytes, &mapA, &full_bar[stage], c * kBK, x0, y0, tc.b, 1);
-                        tma_load_3d(st + a_bytes * p.split, &mapB, &full_bar[stage], c * kBK, tc.nt * p.BN, wt);
+                        expect(&full_bar[stage], a_bytes * p.split + b_bytes);
+                        ld5(st, &mapA, &full_bar[stage], c * kBK, x0, y0, tc.b, 0);
+                        if (p.split == 2) ld5(st + a_bytes, &mapA, &full_bar[stage], c * kBK, x0, y0, tc.b, 1);
+                        ld3(st + a_bytes * p.split, &mapB, &full_bar[stage], c * kBK, tc.nt * p.BN + rank * bnc, wt);
                     }
                     __syncwarp();
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
@@ -235,16 +270,16 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             int hs = 0;
             uint32_t hphase = 0;
             const uint32_t hbytes = (uint32_t)p.halo_w * (p.Ht + 2) * 128 * p.split;
-            for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-                TileCoord tc = decode_tile(p, t);
+            for (int t = cid; t < p.total_tiles; t += ncl) {
+                TileCoord tc = decode_tile(p, t, rank);
                 for (int c = 0; c < p.kchunks; ++c) {
                     mbar_wait(&hempty_bar[hs], hphase ^ 1);
                     uint8_t* hb = smem + p.off_halo + hs * (2 * p.halo_plane_bytes);
                     if (elect_one()) {
-                        mbar_arrive_expect_tx(&hfull_bar[hs], hbytes);
-                        tma_load_5d(hb, &mapA, &hfull_bar[hs], c * kBK, tc.gx0 - 1, tc.gy0 - 1, tc.b, 0);
+                        expect(&hfull_bar[hs], hbytes);
+                        ld5(hb, &mapA, &hfull_bar[hs], c * kBK, tc.gx0 - 1, tc.gy0 - 1, tc.b, 0);
                         if (p.split == 2)
-                            tma_load_5d(hb + p.halo_plane_bytes, &mapA, &hfull_bar[hs], c * kBK, tc.gx0 - 1,
+                            ld5(hb + p.halo_plane_bytes, &mapA, &hfull_bar[hs], c * kBK, tc.gx0 - 1,
                                         tc.gy0 - 1, tc.b, 1);
                     }
                     __syncwarp();
@@ -281,28 +316,30 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     const uint32_t ahi = tmem_base + pend_dcol + gg * G + o / 2;
                     const uint32_t alo = ahi + G / 2;
                     const uint64_t bd = sdesc_sw128(gbase + (k0 / 64) * b_bytes) + 2 * (kk & 3);
-                    umma_f16_ts(ncol, ahi, bd, idesc, kk != 0);
-                    umma_f16_ts(ncol, alo, bd, idesc, 1u);
+                    mma_ts(ncol, ahi, bd, kk != 0);
+                    mma_ts(ncol, alo, bd, 1u);
                 }
-                umma_commit(norm_bar);
+                commit(norm_bar);
             }
             __syncwarp();
             if (lane == 0) LIC_TRACE(pend_it, T_NORM_ISSUE);
             pend = 0;
         };
-        int poll_ctr = 0;
-        auto poll_norm = [&]() {       // every 4th K step: test_wait is ~150 cycles
-            if (kGdn && pend && (++poll_ctr & 3) == 0 && mbar_test(xsq_bar, xsq_phase)) {
+        int xsq_seen = 0;              // tiles whose x^2 the MMA warp has consumed
+        auto poll_norm = [&]() {       // cheap volatile smem read; the mbarrier wait then completes at once
+            if (kGdn && pend && *reinterpret_cast<volatile uint32_t*>(xsq_cnt) >= (uint32_t)(kEpiWarps * CG * (xsq_seen + 1))) {
+                mbar_wait(xsq_bar, xsq_phase);
                 xsq_phase ^= 1;
+                ++xsq_seen;
                 issue_norm();
             }
         };
         if (p.wres) mbar_wait(wres_bar, 0);
-        for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
-            TileCoord tc = decode_tile(p, t);
+        for (int t = cid; t < p.total_tiles && leader; t += ncl, ++it) {
+            TileCoord tc = decode_tile(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
             const uint32_t use = (p.n_accbuf == 2) ? (uint32_t)(it >> 1) : (uint32_t)it;
-            if (kGdn && pend && p.n_accbuf == 1) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; issue_norm(); }
+            if (kGdn && pend && p.n_accbuf == 1) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(); }
             mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
             tc_fence_after();
             if (lane == 0) LIC_TRACE(it, T_MMA_START);
@@ -331,16 +368,16 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         if (elect_one()) {
 #pragma unroll
                             for (int kk = 0; kk < kBK / 16; ++kk) {
-                                umma_f16(d, ah + 2 * kk, bd + 2 * kk, idesc, (c | ti | kk) != 0);
-                                if (p.split == 2) umma_f16(d, al + 2 * kk, bd + 2 * kk, idesc, 1u);
+                                mma_ss(d, ah + 2 * kk, bd + 2 * kk, (c | ti | kk) != 0);
+                                if (p.split == 2) mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
                             }
-                            if (!p.wres) umma_commit(&empty_bar[stage]);
+                            if (!p.wres) commit(&empty_bar[stage]);
                         }
                         __syncwarp();
                         if (!p.wres && ++stage == p.stages) { stage = 0; phase ^= 1; }
                         poll_norm();
                     }
-                    if (elect_one()) umma_commit(&hempty_bar[hs]);
+                    if (elect_one()) commit(&hempty_bar[hs]);
                     __syncwarp();
                     if (++hs == p.halo_slots) { hs = 0; hphase ^= 1; }
                 }
@@ -357,28 +394,28 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                         for (int kk = 0; kk < kBK / 16; ++kk) {
                             // +32 bytes per 16-element K step inside the 128-byte swizzle row
-                            umma_f16(d, ah + 2 * kk, bd + 2 * kk, idesc, (k | kk) != 0);
-                            if (p.split == 2) umma_f16(d, al + 2 * kk, bd + 2 * kk, idesc, 1u);
+                            mma_ss(d, ah + 2 * kk, bd + 2 * kk, (k | kk) != 0);
+                            if (p.split == 2) mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
                         }
-                        umma_commit(&empty_bar[stage]);
+                        commit(&empty_bar[stage]);
                     }
                     __syncwarp();
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     poll_norm();
                 }
             }
-            if (elect_one()) umma_commit(&tfull_bar[buf]);
+            if (elect_one()) commit(&tfull_bar[buf]);
             __syncwarp();
             if (lane == 0) LIC_TRACE(it, T_MMA_END);
             if (kGdn) {
                 // the previous tile's norm must be issued before this one becomes pending
-                if (pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; issue_norm(); }
+                if (pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(); }
                 pend = 1;
                 pend_it = it;
                 pend_dcol = (uint32_t)(buf * p.acc_stride);
             }
         }
-        if (kGdn && pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; issue_norm(); }
+        if (kGdn && pend && leader) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(); }
     } else if (warp >= 4) {
         // ====================== epilogue ======================
         const int q = warp & 3;                     // TMEM lane quadrant
@@ -388,8 +425,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         uint32_t norm_phase = 0;
         int it = 0;
         int sat = 0;
-        for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
-            TileCoord tc = decode_tile(p, t);
+        int ost_i = 0;                              // staging slot counter
+        for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
+            TileCoord tc = decode_tile(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
             const uint32_t use = (p.n_accbuf == 2) ? (uint32_t)(it >> 1) : (uint32_t)it;
             // one lane waits on the mbarrier, the other epilogue warps sleep in a hardware
@@ -414,12 +452,16 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const int bw = p.Wt < 32 ? p.Wt : 32, bh = 32 / bw;
             const int ty0 = (q * 32) / p.Wt, tx0 = (q * 32) % p.Wt;
             const bool tma_ok = p.tma_out && (p.nphase == 1 || tc.gy0 + ty0 + bh <= p.Hg);
-            uint8_t* ostage = smem + p.off_ostage + (warp - 4) * 2048;
+            uint8_t* ostage_base = smem + p.off_ostage + (warp - 4) * 2048 * p.ostage_slots;
             // 16 channels [cb, cb+16) of this thread's pixel -> fp16 hi/lo NHWC activation
             auto emit16 = [&](const float* v16, int cb) {
                 __half* out = reinterpret_cast<__half*>(p.out_act);
                 if (tma_ok) {
-                    if (lane == 0) bulk_wait_read0();        // previous store has read the stage
+                    uint8_t* ostage = ostage_base + (p.ostage_slots == 2 ? (ost_i & 1) * 2048 : 0);
+                    ++ost_i;
+                    if (lane == 0) {                         // the store that last used this slot has read it
+                        if (p.ostage_slots == 2) bulk_wait_read1(); else bulk_wait_read0();
+                    }
                     __syncwarp();
                     uint4 h0, h1, l0, l1;
                     h0.x = h2_bits(v16[0], v16[1]);   h0.y = h2_bits(v16[2], v16[3]);
@@ -490,7 +532,16 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(xsq_bar);       // the MMA warp issues the norm MMAs
+                if (lane == 0) {
+                    // the (leader's) MMA warp issues the norm MMAs
+                    if constexpr (CG == 2) {
+                        mbar_arrive_cluster(lbar(xsq_bar));
+                        atom_add_cluster(mapa_shared(smem_u32(xsq_cnt), 0), 1u);
+                    } else {
+                        mbar_arrive(xsq_bar);
+                        atomicAdd(xsq_cnt, 1u);
+                    }
+                }
                 if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_XSQ);
                 if (threadIdx.x == 128) mbar_wait(norm_bar, norm_phase);
                 norm_phase ^= 1;
@@ -631,7 +682,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+            if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_cluster(lbar(&tempty_bar[buf]));
+                else mbar_arrive(&tempty_bar[buf]);
+            }
             if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_END);
         }
         if (p.tma_out && lane == 0) bulk_wait0();
@@ -642,36 +696,62 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     }
 
     tc_fence_before();
-    __syncthreads();
+    // CG = 2: the leader's MMAs read the peer's smem and write its TMEM -- nobody leaves early
+    if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
+        if constexpr (CG == 2) tmem_dealloc_cg2(tmem_base, (uint32_t)p.tmem_cols);
+        else tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
     }
 }
 
-template <int GC>
+template <int GC, int CG>
 static cudaError_t launch_t(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
                             const CUtensorMap& mapOH, const CUtensorMap& mapOL, const ConvParams& p, int grid,
                             cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<GC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<GC, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    conv_umma_kernel<GC><<<grid, kThreads, p.smem_bytes, stream>>>(mapA, mapB, mapG, mapOH, mapOL, p);
-    return cudaGetLastError();
+    if constexpr (CG == 1) {
+        conv_umma_kernel<GC, 1><<<grid, kThreads, p.smem_bytes, stream>>>(mapA, mapB, mapG, mapOH, mapOL, p);
+        return cudaGetLastError();
+    } else {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = p.smem_bytes;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, conv_umma_kernel<GC, 2>, mapA, mapB, mapG, mapOH, mapOL, p);
+    }
 }
 
 cudaError_t launch_conv_umma(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
                              const CUtensorMap& mapOH, const CUtensorMap& mapOL, const ConvParams& p, int grid,
                              cudaStream_t stream) {
     const bool gdn = (p.ep == EP_GDN || p.ep == EP_IGDN);
-    if (!gdn) return launch_t<0>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+    if (p.cg == 2) {
+        if (!gdn) return launch_t<0, 2>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+        switch (p.BN) {
+        case 128: return launch_t<2, 2>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+        case 192: return launch_t<3, 2>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+        default: return cudaErrorInvalidValue;
+        }
+    }
+    if (!gdn) return launch_t<0, 1>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
     switch (p.BN) {      // GDN channel counts of the configs: N = 128, 192
-    case 128: return launch_t<2>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
-    case 192: return launch_t<3>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+    case 128: return launch_t<2, 1>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+    case 192: return launch_t<3, 1>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -40,6 +40,7 @@ struct ConvParams {
     int ntaps[4], tap0[4];
     int tap_dy[kMaxTaps], tap_dx[kMaxTaps], tap_w[kMaxTaps];
     int split;                        // 2: activations are fp16 hi + lo planes; 1: hi only
+    int cg;                           // 1: one CTA per tile; 2: CTA pair (cta_group::2, M = 256)
     int total_tiles;
     // ---- kernel resources (host-computed)
     int stages;
@@ -76,7 +77,7 @@ struct ConvParams {
     // TMA-store epilogue: each epilogue warp stages 32 px x 16 ch (hi, lo: 1 KB each) in smem and
     // writes it with a bulk tensor store; out maps: conv (C, W, H, B), deconv phase view
     // (C, px, W/2, py, B*H/2) of the NHWC output, one map per plane
-    int tma_out;
+    int tma_out, ostage_slots;        // staging buffers per warp (1 or 2, 2 KB each)
     uint32_t off_ostage;
 };
 
