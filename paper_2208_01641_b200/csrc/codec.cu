@@ -165,6 +165,8 @@ struct lic_codec {
     int halo_enabled = 1;          // LIC_NO_HALO=1 in the environment disables halo mode
     int tma_out_enabled = 1;       // LIC_TMA_OUT=0 disables the TMA-store epilogue
     int cg_enabled = 1;            // LIC_CG=1 forces one CTA per tile (no cta_group::2 pairs)
+    int gs4_bn = 32;               // packed g_s L4 N tile (env LIC_GS4_BN=16|32)
+    int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
     std::vector<void*> allocs;          // device allocations to free
@@ -317,7 +319,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.Cin = Ly.Cin_eff;
     P.kchunks = Ly.Cin_eff / 64;
     P.Cout = Ly.Cout;
-    if (Ly.ep == EP_FINAL && Ly.deconv) { P.BN = 16; P.n_ntiles = 1; }
+    if (Ly.ep == EP_FINAL && Ly.deconv) { P.BN = c->gs4_bn; P.n_ntiles = 1; }
     else if (Ly.Cout <= 256) { P.BN = (Ly.Cout + 15) / 16 * 16; P.n_ntiles = 1; }
     else { P.n_ntiles = (Ly.Cout + 255) / 256; P.BN = ((Ly.Cout + P.n_ntiles - 1) / P.n_ntiles + 15) / 16 * 16; }
     const bool gdn = (Ly.ep == EP_GDN || Ly.ep == EP_IGDN);
@@ -365,7 +367,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     }
     // CTA pair (cta_group::2, M = 256) unless disabled (env LIC_CG=1); B / gamma split by rows
     // (N tiles >= 64 only: the packed N = 16 g_s L4 stays on one CTA per tile)
-    P.cg = (c->cg_enabled && P.BN % 16 == 0 && P.BN >= 64) ? 2 : 1;
+    P.cg = (c->cg_enabled && P.BN % 16 == 0 && P.BN >= 32) ? 2 : 1;
     // shared memory plan: stage ring | halo ring (halo mode) | gamma (GDN) | mbarriers | constants
     const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)(P.BN / P.cg) * 64 * 2;
     const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
@@ -402,7 +404,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.halo_slots = slots;
         // small weight sets (packed g_s L4: 9 taps x 2 chunks x 2 KB) stay resident
         const uint32_t wtot = (uint32_t)P.ntaps[0] * P.kchunks * b_bytes;
-        if (P.nphase == 1 && fixed + slots * P.split * hpb + wtot <= budget && wtot <= 64 * 1024) {
+        if (c->wres_enabled && P.nphase == 1 && fixed + slots * P.split * hpb + wtot <= budget && wtot <= 64 * 1024) {
             P.wres = 1;
             P.stages = 1;
             P.stage_bytes = 0;
@@ -647,6 +649,8 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_NO_HALO")) c->halo_enabled = (e[0] == '0');
     if (const char* e = std::getenv("LIC_TMA_OUT")) c->tma_out_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_CG")) c->cg_enabled = (e[0] != '1');
+    if (const char* e = std::getenv("LIC_GS4_BN")) c->gs4_bn = (atoi(e) == 16) ? 16 : 32;
+    if (const char* e = std::getenv("LIC_NO_WRES")) c->wres_enabled = (e[0] != '1');
     c->max_batch = (int)max_batch;
     c->H = (int)height; c->W = (int)width;
     const int P = c->kind == 1 ? 64 : 16;
@@ -730,7 +734,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
         int bn = d.cout <= 256 ? (d.cout + 15) / 16 * 16 : 0;
         if (!bn) { int nt = (d.cout + 255) / 256; bn = ((d.cout + nt - 1) / nt + 15) / 16 * 16 * nt; }
         const bool pack4 = d.id == GS4;
-        const int cout_pad = pack4 ? 16 : bn;
+        const int cout_pad = pack4 ? c->gs4_bn : bn;
         const int taps = d.id == GA1 ? 1 : (pack4 ? 9 : d.k * d.k);
         std::vector<__half> wp((size_t)taps * cout_pad * Ly.Cin_eff, __float2half(0.0f));
         if (pack4) {
@@ -741,7 +745,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
                     if (ky < 0 || ky > 4 || kx < 0 || kx > 4) continue;
                     for (int co = 0; co < 3; ++co)
                         for (int ci = 0; ci < d.cin; ++ci)
-                            wp[((size_t)t * 16 + ph * 4 + co) * Ly.Cin_eff + ci] =
+                            wp[((size_t)t * cout_pad + ph * 4 + co) * Ly.Cin_eff + ci] =
                                 __float2half_rn(w[(((size_t)co * d.cin + ci) * 5 + ky) * 5 + kx]);
                 }
             }

@@ -334,7 +334,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 issue_norm();
             }
         };
-        if (p.wres) mbar_wait(wres_bar, 0);
+        if (p.wres && leader) mbar_wait(wres_bar, 0);      // the peer's bytes land on the leader's barrier
         for (int t = cid; t < p.total_tiles && leader; t += ncl, ++it) {
             TileCoord tc = decode_tile(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
