@@ -30,7 +30,6 @@
 namespace lic {
 cudaError_t launch_conv_umma(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                              const CUtensorMap&, const ConvParams&, int, cudaStream_t);
-cudaError_t launch_ingest(const void*, int, int, int, int, int, int, int, int, __half*, size_t, int, cudaStream_t);
 cudaError_t launch_sym_ingest(const int8_t*, const float*, int, int, int, int, __half*, size_t, int, cudaStream_t);
 cudaError_t launch_pack_chw(const float*, int, int, int, int, __half*, size_t, int, cudaStream_t);
 cudaError_t launch_sigma_index(const float*, size_t, const float*, uint8_t*, cudaStream_t);
@@ -149,8 +148,8 @@ struct lic_codec {
     bool sticky = false;
     Layer layers[NLAYER];
     // device buffers
-    __half *bufI = nullptr, *bufA = nullptr, *bufB = nullptr, *bufY = nullptr, *bufZ = nullptr;
-    size_t planeI = 0, planeA = 0, planeY = 0, planeZ = 0;
+    __half *bufA = nullptr, *bufB = nullptr, *bufY = nullptr, *bufZ = nullptr;
+    size_t planeA = 0, planeY = 0, planeZ = 0;
     float *mu_y = nullptr, *mu_z = nullptr, *table = nullptr;
     unsigned long long* d_sat = nullptr;
     void* d_frames = nullptr;           // staging for host frames (f32 CHW size)
@@ -158,6 +157,7 @@ struct lic_codec {
     uint8_t* d_yidx = nullptr;
     int8_t* d_zsym = nullptr;
     float* d_dbg = nullptr;             // test-layer / debug scratch
+    float* d_dbg_in = nullptr;          // test-layer input copy for the fused g_a L1
     size_t dbg_elems = 0;
     float *dbg_y = nullptr, *dbg_z = nullptr, *dbg_s = nullptr;
     int debug = 0;
@@ -305,6 +305,18 @@ static void choose_tile(int Hg, int Wg, int* Wt, int* Ht) {
 static constexpr uint32_t kBarBytes = 512;
 static_assert(kBarBytes >= (2 * 8 + 2 * 2 + 2 + 2 * 4 + 2) * 8 + 4, "barrier area too small");
 
+// q = (umulhi(n, m) + n) >> s == n / d for 0 <= n < 2^31 (round-up magic, d >= 1)
+static void fast_div(int d, uint32_t* m, int* s) {
+    int l = 0;
+    while ((1ll << l) < d) ++l;
+    *s = l;
+    *m = (uint32_t)(((1ull << 32) * ((1ull << l) - (uint64_t)d)) / (uint64_t)d + 1);
+}
+static int ilog2_exact(int v) {
+    for (int l = 0; l < 31; ++l) if ((1 << l) == v) return l;
+    return -1;
+}
+
 static int pow2_cols(int n) {
     int c = 32;
     while (c < n) c <<= 1;
@@ -390,7 +402,24 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     int halo_w = 10;                                                   // Wt + 2
     if (const char* e = std::getenv("LIC_HALO_W")) halo_w = std::max(10, std::min(32, atoi(e)));
     const uint32_t hpb = ((uint32_t)(halo_w * 18 * 128) + 1023) / 1024 * 1024;   // halo_w x (Ht+2) rows
-    if (stride1 && fixed + 2 * P.split * hpb + 2 * b_bytes <= budget && c->halo_enabled) {
+    if (gemm_l1) {
+        // fused g_a L1: stage s = A chunk s (hi, lo) built by warps 0/2/3; resident weights;
+        // double-buffered fp32 input patch; k -> patch offset table + u8 LUT
+        P.fuse_l1 = 1;
+        P.halo = 0;
+        P.halo_slots = 0;
+        P.Wt = 16; P.Ht = 8;
+        P.stage_bytes = a_bytes * P.split;
+        P.stages = P.kchunks;
+        P.wres = 1;
+        P.off_wres = P.stages * P.stage_bytes;
+        P.off_patch = P.off_wres + P.kchunks * b_bytes;
+        const uint32_t patch_bytes = 2u * 19u * 112u * 2u;           // hi + lo planes
+        P.off_lut = P.off_patch + 2 * patch_bytes;
+        P.off_halo = 0;
+        P.off_raw = (P.off_lut + 257 * 4 + 15) / 16 * 16;
+        P.off_gamma = (P.off_raw + 2 * 19 * 112 + 1023) / 1024 * 1024;
+    } else if (stride1 && fixed + 2 * P.split * hpb + 2 * b_bytes <= budget && c->halo_enabled) {
         P.halo = 1;
         P.Wt = 8; P.Ht = 16;
         P.halo_plane_bytes = hpb;
@@ -430,6 +459,13 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     }
     P.tiles_x = (P.Wg + P.Wt - 1) / P.Wt;
     P.tiles_y = (P.Hg + P.Ht - 1) / P.Ht;
+    P.txs = (P.tiles_x + P.cg - 1) / P.cg;
+    fast_div(P.n_ntiles, &P.fd_nt_m, &P.fd_nt_s);
+    fast_div(P.txs, &P.fd_txs_m, &P.fd_txs_s);
+    fast_div(P.tiles_y, &P.fd_ty_m, &P.fd_ty_s);
+    P.wt_log2 = ilog2_exact(P.Wt);
+    P.nph_log2 = ilog2_exact(P.nphase);
+    if (P.wt_log2 < 0 || P.nph_log2 < 0) return fail(c, LIC_EINVAL, "tile width / phase count must be powers of two");
     P.off_bar = P.off_gamma + gamma_bytes;
     P.off_par = P.off_bar + kBarBytes;
     P.tma_out = tma_out ? 1 : 0;
@@ -438,7 +474,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.smem_bytes = (tma_out ? P.off_ostage + ostage_bytes : P.off_par + par_bytes) + 1024;
     // double-buffered staging when it fits without losing pipeline depth below 3 (halo: 2) stages
     if (tma_out && P.smem_bytes + ostage_bytes <= budget) {
-        const bool keep = P.halo ? (P.wres || P.stages >= 2) : P.stages >= 3;
+        const bool keep = P.fuse_l1 || (P.halo ? (P.wres || P.stages >= 2) : P.stages >= 3);
         if (keep) { P.ostage_slots = 2; P.smem_bytes += ostage_bytes; }
     } else if (tma_out && P.halo && !P.wres && P.stage_bytes) {
         // trade weight stages (keeping >= 2) for the second staging slot
@@ -466,7 +502,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     // tensor maps
     const int ntaps_w = gemm_l1 ? 1 : (P.pack4 ? 9 : Ly.k * Ly.k);
     const int cout_pad = P.BN * P.n_ntiles;
-    if (!encode_act_map(&Ly.mapA, Ly.in_buf, P.Cin, Ly.deconv ? Ly.Win : (gemm_l1 ? Ly.Wout : Ly.Win),
+    if (!P.fuse_l1 && !encode_act_map(&Ly.mapA, Ly.in_buf, P.Cin, Ly.deconv ? Ly.Win : (gemm_l1 ? Ly.Wout : Ly.Win),
                         Ly.deconv ? Ly.Hin : (gemm_l1 ? Ly.Hout : Ly.Hin), c->max_batch, P.split, Ly.in_plane,
                         P.halo ? P.halo_w : P.Wt, P.halo ? P.Ht + 2 : P.Ht, P.stride))
         return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (activations) failed");
@@ -514,7 +550,7 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
     if (c->trace_layer == lid && c->d_trace) {
         P.trace = c->d_trace;
         if (const char* e = std::getenv("LIC_DBG_NOSTORE")) P.dbg_nostore = atoi(e);
-        CK(cudaMemsetAsync(c->d_trace, 0, 256 * 8 * 8, st));
+        CK(cudaMemsetAsync(c->d_trace, 0, 256 * 16 * 8, st));
     }
     if (c->profiling) {
         if (c->ev_used == kProfSlots) prof_flush(c);
@@ -678,12 +714,11 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     }
 
     // ---- activation buffers (planes of fp16 NHWC)
-    c->planeI = (size_t)B * H2 * W2 * 128;
     c->planeA = (size_t)B * H2 * W2 * N;
     c->planeY = (size_t)B * Hy * Wy * M;
     c->planeZ = (size_t)B * std::max(1, Hz) * std::max(1, Wz) * N;
     lic_status st;
-    if ((st = dalloc(c, &c->bufI, c->planeI * S * 2)) || (st = dalloc(c, &c->bufA, c->planeA * S * 2)) ||
+    if ((st = dalloc(c, &c->bufA, c->planeA * S * 2)) ||
         (st = dalloc(c, &c->bufB, c->planeA * S * 2)) || (st = dalloc(c, &c->bufY, c->planeY * S * 2)) ||
         (st = dalloc(c, &c->bufZ, c->planeZ * S * 2)) || (st = dalloc(c, &c->table, 64 * 4)) ||
         (st = dalloc(c, &c->mu_y, (size_t)M * 4)) || (st = dalloc(c, &c->mu_z, (size_t)N * 4)) ||
@@ -699,7 +734,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     struct Def { int id; bool deconv; int k, s, p, cin, cout, hin, win, hout, wout; EpKind ep; __half* in; size_t inpl;
                  __half* out; size_t outpl; };
     std::vector<Def> defs = {
-        {GA1, false, 5, 2, 2, 3, N, c->Hp, c->Wp, H2, W2, EP_GDN, c->bufI, c->planeI, c->bufA, c->planeA},
+        {GA1, false, 5, 2, 2, 3, N, c->Hp, c->Wp, H2, W2, EP_GDN, nullptr, 0, c->bufA, c->planeA},
         {GA2, false, 5, 2, 2, N, N, H2, W2, H2 / 2, W2 / 2, EP_GDN, c->bufA, c->planeA, c->bufB, c->planeA},
         {GA3, false, 5, 2, 2, N, N, H2 / 2, W2 / 2, H2 / 4, W2 / 4, EP_GDN, c->bufB, c->planeA, c->bufA, c->planeA},
         {GA4, false, 5, 2, 2, N, M, H2 / 4, W2 / 4, Hy, Wy, EP_YQUANT, c->bufA, c->planeA, c->bufY, c->planeY},
@@ -756,7 +791,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
                     for (int kx = 0; kx < d.k; ++kx) {
                         const float v = w[(((size_t)co * d.cin + ci) * d.k + ky) * d.k + kx];
                         size_t o;
-                        if (d.id == GA1) o = (size_t)co * 128 + (ky * 5 + kx) * 3 + ci;     // im2col K order
+                        if (d.id == GA1) o = (size_t)co * 128 + ky * 16 + kx * 3 + ci;      // fused im2col K order
                         else o = ((size_t)(ky * d.k + kx) * cout_pad + co) * Ly.Cin_eff + ci;
                         wp[o] = __float2half_rn(v);
                     }
@@ -911,10 +946,12 @@ static lic_status encode_impl(lic_codec* c, const void* frames, int hwc, uint32_
     OutBuf oi = hyper ? route_out(c, y_idx, c->d_yidx, ny) : OutBuf{nullptr, nullptr, 0};
     OutBuf oz = hyper ? route_out(c, z_sym, c->d_zsym, nz) : OutBuf{nullptr, nullptr, 0};
     CK(cudaMemsetAsync(c->d_sat, 0, 8, st));
-    CK(launch_ingest(fdev, hwc, B, c->H, c->W, c->top, c->left, c->Hp / 2, c->Wp / 2, c->bufI, c->planeI,
-                     c->split, st));
-    ++c->launches;
-    for (int id : {GA1, GA2, GA3})
+    {
+        ConvParams p = c->layers[GA1].prm;             // fused im2col: reads the frames directly
+        p.frame = fdev; p.fr_u8 = hwc; p.fr_H = c->H; p.fr_W = c->W; p.fr_top = c->top; p.fr_left = c->left;
+        if ((r = run_layer(c, c->layers[GA1], p, B, st))) return r;
+    }
+    for (int id : {GA2, GA3})
         if ((r = run_layer(c, c->layers[id], c->layers[id].prm, B, st))) return r;
     {
         ConvParams p = c->layers[GA4].prm;
@@ -1060,11 +1097,18 @@ extern "C" lic_status lic_test_layer(lic_codec* c, int id, const float* in, uint
         CK(cudaMemcpyAsync(c->d_dbg, in, nin * 4, cudaMemcpyHostToDevice, st));
         ind = c->d_dbg;
     }
-    if (id == GA1)
-        CK(launch_ingest(ind, 0, B, Ly.Hin, Ly.Win, 0, 0, Ly.Hout, Ly.Wout, c->bufI, c->planeI, c->split, st));
-    else
-        CK(launch_pack_chw(ind, B, Ly.Cin, Ly.Hin, Ly.Win, Ly.in_buf, Ly.in_plane, c->split, st));
     ConvParams p = Ly.prm;
+    if (id == GA1) {
+        // the fused L1 reads its input during the launch: keep it apart from the output scratch
+        if (ind == c->d_dbg) {
+            if (!c->d_dbg_in && (r = dalloc(c, &c->d_dbg_in, c->dbg_elems * 4))) return r;
+            CK(cudaMemcpyAsync(c->d_dbg_in, ind, nin * 4, cudaMemcpyDeviceToDevice, st));
+            ind = c->d_dbg_in;
+        }
+        p.frame = ind; p.fr_u8 = 0; p.fr_H = Ly.Hin; p.fr_W = Ly.Win; p.fr_top = 0; p.fr_left = 0;
+    } else {
+        CK(launch_pack_chw(ind, B, Ly.Cin, Ly.Hin, Ly.Win, Ly.in_buf, Ly.in_plane, c->split, st));
+    }
     OutBuf o = route_out(c, out, c->d_dbg, nout * 4);
     p.out_f32 = (float*)o.dev;
     p.sat_count = nullptr;
@@ -1136,7 +1180,7 @@ extern "C" lic_status lic_set_zero_copy(lic_codec* c, int on) {
 extern "C" lic_status lic_trace(lic_codec* c, int layer_id, int on) {
     if (!c || layer_id < 0 || layer_id >= NLAYER) return LIC_EINVAL;
     if (on && !c->d_trace) {
-        lic_status r = dalloc(c, &c->d_trace, 256 * 8 * 8);
+        lic_status r = dalloc(c, &c->d_trace, 256 * 16 * 8);
         if (r) return r;
     }
     c->trace_layer = on ? layer_id : -1;
@@ -1147,6 +1191,6 @@ extern "C" lic_status lic_trace_read(lic_codec* c, uint64_t* out, size_t n) {
     if (!c || !out || !c->d_trace) return LIC_EINVAL;
     cudaSetDevice(c->device);
     CK(cudaStreamSynchronize(c->stream));
-    CK(cudaMemcpy(out, c->d_trace, std::min<size_t>(n, 256 * 8) * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, c->d_trace, std::min<size_t>(n, 256 * 16) * 8, cudaMemcpyDeviceToHost));
     return LIC_OK;
 }

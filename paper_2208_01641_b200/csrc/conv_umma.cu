@@ -45,15 +45,20 @@ struct TileCoord { int b, ph, gy0, gx0, nt; };
 // of 4, CTA c would otherwise always get phase c % 4 (9, 6, 6 or 4 taps) and the kernel
 // would run at the speed of its phase-0 CTAs.
 // CTA pairs (p.cg = 2) take two horizontally adjacent tiles: rank r gets tile 2*txp + r.
+__device__ __forceinline__ int fdiv(int n, uint32_t m, int s) {
+    return (int)((__umulhi((uint32_t)n, m) + (uint32_t)n) >> s);
+}
 __device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t, int rank) {
     TileCoord c;
-    c.ph = t % p.nphase;    t /= p.nphase;
+    c.ph = t & (p.nphase - 1);  t >>= p.nph_log2;
     if (p.nphase == 4) c.ph = (c.ph + t) & 3;
-    c.nt = t % p.n_ntiles;  t /= p.n_ntiles;
-    const int txs = (p.tiles_x + p.cg - 1) / p.cg;
-    int tx = (t % txs) * p.cg + rank; t /= txs;
-    int ty = t % p.tiles_y;
-    c.b = t / p.tiles_y;
+    int q = fdiv(t, p.fd_nt_m, p.fd_nt_s);
+    c.nt = t - q * p.n_ntiles;  t = q;
+    q = fdiv(t, p.fd_txs_m, p.fd_txs_s);
+    const int tx = (t - q * p.txs) * p.cg + rank;  t = q;
+    q = fdiv(t, p.fd_ty_m, p.fd_ty_s);
+    const int ty = t - q * p.tiles_y;
+    c.b = q;
     c.gx0 = tx * p.Wt;
     c.gy0 = ty * p.Ht;
     return c;
@@ -63,20 +68,84 @@ __device__ __forceinline__ uint32_t h2_bits(float a, float b) {
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
 }
+// shared-memory vector load (the aligned dynamic-smem base is a generic pointer, so plain
+// dereferences compile to generic LD)
+__device__ __forceinline__ float4 lds4(const float* ptr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_u32(ptr)));
+    return v;
+}
+__device__ __forceinline__ float ldsf(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint4 ldsu4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldsu(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldsb(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+// 4-byte global -> shared async copy; src_size 0 zero-fills without reading
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t src_size) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(dst), "l"(src), "r"(src_size) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void stsh(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" :: "r"(addr), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void stsf(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" :: "r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void stsu4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+// fused g_a L1 geometry: 16 x 8 output tile -> 19 x 35 x 3 input patch
+constexpr int kL1Wt = 16, kL1Ht = 8;
+constexpr int kL1PH = 2 * kL1Ht + 3, kL1PW = (2 * kL1Wt + 3) * 3;    // patch rows, values per row (105)
+constexpr int kL1Pitch = 112;                                        // halves per patch row (>= 6*15 + 16)
+constexpr uint32_t kL1PlaneBytes = kL1PH * kL1Pitch * 2;             // one fp16 plane of a patch
+constexpr int kL1K = 80;                                             // K = 16*ky + 3*kx + c, 5 rows of 16
+constexpr int kL1Builders = 96;                                      // warps 0, 2, 3
+constexpr int kL1RawWords = 28;                                      // >= (3 + 105) / 4 words per raw row
+constexpr uint32_t kL1RawBytes = kL1PH * kL1RawWords * 4;           // one raw u8 patch
+static_assert(kL1Wt == 16, "build_l1 decodes r -> (r >> 4, r & 15)");
+
+// MUFU.RSQ without the denormal-input fix-up (GDN/IGDN: beta + n >= beta > 0, normal)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float hround(float v) { return __half2float(__float2half_rn(v)); }
+// (a, b) -> packed fp16 hi = rn(a, b) and lo = rn(a - hi, b - hi): one pack per plane, the hi
+// values unpacked from the pack itself (no second rounding of a and b)
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = h2_bits(a - hf.x, b - hf.y);
+}
 
 // 8 consecutive channels -> one 16-byte fp16 hi vector (+ one lo vector)
 __device__ __forceinline__ void split_store8(__half* hi, __half* lo, const float* v) {
     uint4 h, l;
-    h.x = h2_bits(v[0], v[1]); h.y = h2_bits(v[2], v[3]); h.z = h2_bits(v[4], v[5]); h.w = h2_bits(v[6], v[7]);
+    split2(v[0], v[1], h.x, l.x); split2(v[2], v[3], h.y, l.y);
+    split2(v[4], v[5], h.z, l.z); split2(v[6], v[7], h.w, l.w);
     *reinterpret_cast<uint4*>(hi) = h;
-    if (lo) {
-        l.x = h2_bits(v[0] - hround(v[0]), v[1] - hround(v[1]));
-        l.y = h2_bits(v[2] - hround(v[2]), v[3] - hround(v[3]));
-        l.z = h2_bits(v[4] - hround(v[4]), v[5] - hround(v[5]));
-        l.w = h2_bits(v[6] - hround(v[6]), v[7] - hround(v[7]));
-        *reinterpret_cast<uint4*>(lo) = l;
-    }
+    if (lo) *reinterpret_cast<uint4*>(lo) = l;
 }
 
 __device__ __forceinline__ int round_clamp(float v, int L, int& sat) {
@@ -87,10 +156,11 @@ __device__ __forceinline__ int round_clamp(float v, int L, int& sat) {
 }
 
 // test-only timeline: event e of the it-th tile of CTA 0 (kTraceEv slots per tile)
-constexpr int kTraceEv = 8;
+constexpr int kTraceEv = 16;
 constexpr int kTraceTiles = 256;
 enum TraceEv { T_MMA_START = 0, T_MMA_END = 1, T_NORM_ISSUE = 2, T_EPI_START = 3, T_EPI_XSQ = 4,
-               T_EPI_NORM = 5, T_EPI_END = 6, T_PROD_START = 7 };
+               T_EPI_NORM = 5, T_EPI_END = 6, T_PROD_START = 7,
+               T_B_PATCH = 8, T_B_C0_READY = 9, T_B_C0_DONE = 10, T_B_C1_READY = 11, T_B_C1_DONE = 12 };
 #define LIC_TRACE(it, ev)                                                                         \
     do {                                                                                          \
         if (p.trace && blockIdx.x == 0 && (it) < kTraceTiles)                                     \
@@ -140,7 +210,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     auto lbar = [&](uint64_t* b) -> uint32_t { return CG == 2 ? mapa_shared(smem_u32(b), 0) : smem_u32(b); };
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < p.stages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+        // fused L1: the 3 builder warps of each CTA arrive on the leader's full barrier
+        const uint32_t full_cnt = p.fuse_l1 ? 3u * CG : 1u;
+        for (int s = 0; s < p.stages; ++s) { mbar_init(&full_bar[s], full_cnt); mbar_init(&empty_bar[s], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], kEpiWarps * CG); }
         mbar_init(norm_bar, 1);
         mbar_init(gamma_bar, 1);
@@ -151,7 +223,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&mapA);
+        if (!p.fuse_l1) tma_prefetch_desc(&mapA);
         tma_prefetch_desc(&mapB);
         if (kGdn) tma_prefetch_desc(&mapG);
     }
@@ -169,6 +241,22 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             s_mu[i] = (in && p.mu) ? p.mu[i] : 0.0f;
         }
         for (int i = threadIdx.x - 128; i < 64; i += 32 * kEpiWarps) s_tab[i] = p.table ? p.table[i] : 0.0f;
+    }
+    if (p.fuse_l1) {
+        // zero the A stages (K columns >= 80 are never rewritten) and both patch buffers (the
+        // row padding halves 105..111 are never rewritten); u8 -> (hi | lo << 16) of u8 / 255
+        // (IEEE division, as the oracle), entry 256 = 0 for samples outside the frame
+        for (uint32_t i = threadIdx.x; i < p.stages * p.stage_bytes / 16; i += kThreads)
+            stsu4(smem_u32(smem) + 16 * i, make_uint4(0, 0, 0, 0));
+        for (uint32_t i = threadIdx.x; i < 4 * kL1PlaneBytes / 16; i += kThreads)
+            stsu4(smem_u32(smem + p.off_patch) + 16 * i, make_uint4(0, 0, 0, 0));
+        uint32_t* lut = reinterpret_cast<uint32_t*>(smem + p.off_lut);
+        for (int u = threadIdx.x; u < 257; u += kThreads) {
+            uint32_t h = 0, l = 0;
+            if (u < 256) { const float v = __fdiv_rn((float)u, 255.0f); split2(v, 0.0f, h, l); }
+            lut[u] = (h & 0xffffu) | (l << 16);
+        }
+        fence_proxy_async_smem();
     }
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
@@ -200,7 +288,158 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         if constexpr (CG == 2) umma_f16_ts_cg2(d, a, b, idesc, acc); else umma_f16_ts(d, a, b, idesc, acc);
     };
 
-    if (warp == 0) {
+    // ====================== fused g_a L1: im2col A-tile builders (warps 0, 2, 3) ======================
+    // K order of the L1 GEMM: k = 16*ky + 3*kx + c (15 values per kernel row + one slot whose
+    // weight is zero; 80 used of 128).  Per tile the 19 x 35 x 3 input patch is written to smem
+    // already split (fp16 hi and lo planes, rows of 112 halves, zero outside the frame); a K
+    // row segment (ky, 8 values from 8h) of pixel (ty, tx) is then 16 contiguous bytes of patch
+    // row 2ty + ky at half 6tx + 8h, copied (4 x LDS.32 per plane) into the SW128 A tile.
+    auto build_l1 = [&](int bw) {
+        const int bt = bw * 32 + lane;
+        const uint32_t lut_s = smem_u32(smem + p.off_lut);
+        const uint32_t patch_s = smem_u32(smem + p.off_patch);
+        const uint32_t raw_s = smem_u32(smem + p.off_raw);
+        // u8 frames with 4-byte aligned rows (W % 4 == 0): the patch bytes arrive by cp.async
+        // (4-byte words, zero-filled outside the frame -- the frame edges are word boundaries),
+        // one tile ahead of the build; otherwise per-sample loads.
+        const bool fast = p.fr_u8 && (p.fr_W & 3) == 0;
+        auto raw_issue = [&](int tt, int buf) {
+            const TileCoord tn = decode_tile(p, tt, rank);
+            const uint8_t* fr = reinterpret_cast<const uint8_t*>(p.frame);
+            const int rowb = 3 * p.fr_W;
+            const int iyn = 2 * tn.gy0 - 2 - p.fr_top, ws = (3 * (2 * tn.gx0 - 2 - p.fr_left)) >> 2;   // floor
+            const uint32_t rb = raw_s + (uint32_t)buf * kL1RawBytes;
+            for (int q = bt; q < kL1PH * kL1RawWords; q += kL1Builders) {
+                const int r = q / kL1RawWords, w = q - kL1RawWords * r;
+                const int iy = iyn + r, gw = 4 * (ws + w);
+                const bool ok = iy >= 0 && iy < p.fr_H && gw >= 0 && gw < rowb;
+                const uint8_t* src = ok ? fr + ((size_t)tn.b * p.fr_H + iy) * rowb + gw : fr;
+                cp_async4(rb + 4u * q, src, ok ? 4u : 0u);
+            }
+            cp_async_commit();
+        };
+        if (fast && cid < p.total_tiles) raw_issue(cid, 0);
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
+            const TileCoord tc = decode_tile(p, t, rank);
+            const uint32_t pbh = patch_s + (uint32_t)((it & 1) * 2 * kL1PlaneBytes), pbl = pbh + kL1PlaneBytes;
+            const int iy0 = 2 * tc.gy0 - 2 - p.fr_top, ix0 = 2 * tc.gx0 - 2 - p.fr_left;
+            // ---- patch (double-buffered by tile parity; the named barrier of tile it+1 orders
+            // every builder's reads of buffer it&1 before anyone rewrites it at tile it+2).
+            // All global loads first (independent, in flight together), then split + stores;
+            // a thread owns patch columns e0 = bt and e1 = bt + 96 (< 105 for bt < 9).
+            const int e0 = bt, e1 = bt + kL1Builders;
+            const bool has1 = e1 < kL1PW;
+            if (fast) {
+                cp_async_wait_all();
+                named_bar_sync(4, kL1Builders);                          // raw[it & 1] complete
+                const uint32_t rb = raw_s + (uint32_t)(it & 1) * kL1RawBytes + (uint32_t)((3 * ix0) & 3);
+#pragma unroll
+                for (int r = 0; r < kL1PH; ++r) {
+                    const uint32_t w0 = ldsu(lut_s + 4u * ldsb(rb + r * (4 * kL1RawWords) + e0));
+                    stsh(pbh + 2u * (r * kL1Pitch + e0), w0);
+                    stsh(pbl + 2u * (r * kL1Pitch + e0), w0 >> 16);
+                    if (has1) {
+                        const uint32_t w1 = ldsu(lut_s + 4u * ldsb(rb + r * (4 * kL1RawWords) + e1));
+                        stsh(pbh + 2u * (r * kL1Pitch + e1), w1);
+                        stsh(pbl + 2u * (r * kL1Pitch + e1), w1 >> 16);
+                    }
+                }
+            } else if (p.fr_u8) {
+                const uint8_t* fr = reinterpret_cast<const uint8_t*>(p.frame);
+                const int rowb = 3 * p.fr_W;
+                const int gb0 = 3 * ix0 + e0, gb1 = 3 * ix0 + e1;
+                const bool c0 = gb0 >= 0 && gb0 < rowb, c1 = has1 && gb1 >= 0 && gb1 < rowb;
+                uint32_t u0[kL1PH], u1[kL1PH];
+#pragma unroll
+                for (int r = 0; r < kL1PH; ++r) {
+                    const int iy = iy0 + r;
+                    const bool rok = iy >= 0 && iy < p.fr_H;
+                    const uint8_t* row = fr + ((size_t)tc.b * p.fr_H + iy) * rowb;
+                    u0[r] = (rok && c0) ? (uint32_t)__ldg(row + gb0) : 256u;     // lut[256] = 0
+                    u1[r] = (rok && c1) ? (uint32_t)__ldg(row + gb1) : 256u;
+                }
+#pragma unroll
+                for (int r = 0; r < kL1PH; ++r) {
+                    const uint32_t w0 = ldsu(lut_s + 4u * u0[r]);                 // hi | lo << 16
+                    stsh(pbh + 2u * (r * kL1Pitch + e0), w0);
+                    stsh(pbl + 2u * (r * kL1Pitch + e0), w0 >> 16);
+                    if (has1) {
+                        const uint32_t w1 = ldsu(lut_s + 4u * u1[r]);
+                        stsh(pbh + 2u * (r * kL1Pitch + e1), w1);
+                        stsh(pbl + 2u * (r * kL1Pitch + e1), w1 >> 16);
+                    }
+                }
+            } else {
+                const float* fr = reinterpret_cast<const float*>(p.frame);
+                const int px0 = e0 / 3, ch0 = e0 - 3 * px0, px1 = e1 / 3, ch1 = e1 - 3 * px1;
+                const bool c0 = ix0 + px0 >= 0 && ix0 + px0 < p.fr_W;
+                const bool c1 = has1 && ix0 + px1 >= 0 && ix0 + px1 < p.fr_W;
+                float v0[kL1PH], v1[kL1PH];
+#pragma unroll
+                for (int r = 0; r < kL1PH; ++r) {
+                    const int iy = iy0 + r;
+                    const bool rok = iy >= 0 && iy < p.fr_H;
+                    v0[r] = (rok && c0) ? __ldg(fr + (((size_t)tc.b * 3 + ch0) * p.fr_H + iy) * p.fr_W + ix0 + px0) : 0.0f;
+                    v1[r] = (rok && c1) ? __ldg(fr + (((size_t)tc.b * 3 + ch1) * p.fr_H + iy) * p.fr_W + ix0 + px1) : 0.0f;
+                }
+#pragma unroll
+                for (int r = 0; r < kL1PH; ++r) {
+                    uint32_t h, l;
+                    split2(v0[r], v1[r], h, l);
+                    stsh(pbh + 2u * (r * kL1Pitch + e0), h);
+                    stsh(pbl + 2u * (r * kL1Pitch + e0), l);
+                    if (has1) {
+                        stsh(pbh + 2u * (r * kL1Pitch + e1), h >> 16);
+                        stsh(pbl + 2u * (r * kL1Pitch + e1), l >> 16);
+                    }
+                }
+            }
+            named_bar_sync(4, kL1Builders);
+            if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_PATCH);
+            // next tile's raw bytes (its buffer was last read converting tile it-1, before the
+            // raw barrier of this tile)
+            if (fast && t + ncl < p.total_tiles) raw_issue(t + ncl, (it + 1) & 1);
+            // ---- A tiles, one stage per 64-column K chunk
+            for (int c = 0; c < p.kchunks; ++c) {
+                const int kc = c * 64;
+                const int nj = max(0, min(8, (kL1K - kc) / 8));             // 16-byte columns with k < 80
+                mbar_wait(&empty_bar[stage], phase ^ 1);
+                if (bw == 0 && lane == 0) LIC_TRACE(it, c ? T_B_C1_READY : T_B_C0_READY);
+                const uint32_t ah = smem_u32(smem + stage * p.stage_bytes), al = ah + a_bytes;
+                if (nj > 0) {
+                    const int j = bt % nj;                                   // fixed column (96 % nj == 0)
+                    const int ky = (kc + 8 * j) >> 4, h8 = (j & 1) * 16;     // kernel row, byte offset in it
+                    const int rstep = kL1Builders / nj;
+                    for (int r = bt / nj; r < kBM; r += rstep) {
+                        const int ty = r >> 4, tx = r & 15;
+                        const uint32_t so = (uint32_t)((2 * ty + ky) * (2 * kL1Pitch) + 12 * tx + h8);
+                        uint4 hv, lv;
+                        hv.x = ldsu(pbh + so); hv.y = ldsu(pbh + so + 4); hv.z = ldsu(pbh + so + 8); hv.w = ldsu(pbh + so + 12);
+                        lv.x = ldsu(pbl + so); lv.y = ldsu(pbl + so + 4); lv.z = ldsu(pbl + so + 8); lv.w = ldsu(pbl + so + 12);
+                        const uint32_t o = (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4));
+                        stsu4(ah + o, hv);
+                        if (p.split == 2) stsu4(al + o, lv);
+                    }
+                }
+                fence_proxy_async_smem();                             // generic writes -> tensor core
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2) mbar_arrive_cluster(lbar(&full_bar[stage]));
+                    else mbar_arrive(&full_bar[stage]);
+                    if (bw == 0) LIC_TRACE(it, c ? T_B_C1_DONE : T_B_C0_DONE);
+                }
+                if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            }
+            if (bw == 0 && lane == 0) LIC_TRACE(it, T_PROD_START);     // fused L1: tile built
+        }
+    };
+
+    if (warp == 2 && p.fuse_l1) {
+        build_l1(1);
+    } else if (warp == 0) {
         // ====================== TMA producer (weights; activations unless halo mode) ======================
         // warp-uniform loop; one elected lane issues (keeps coordinates in uniform registers)
         if (kGdn) {
@@ -264,8 +503,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 }
             }
         }
+        if (p.fuse_l1) build_l1(0);
     } else if (warp == 3) {
         // ====================== halo producer (halo mode) ======================
+        if (p.fuse_l1) build_l1(2);
         if (p.halo) {
             int hs = 0;
             uint32_t hphase = 0;
@@ -334,13 +575,27 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 issue_norm();
             }
         };
+        // blocking waits of the MMA warp keep polling for a pending norm (GDN), so that the
+        // norm of tile i is not held back while the warp waits for tile i+1's operands
+        auto wait_poll = [&](uint64_t* bar, uint32_t par) {
+            if constexpr (kGdn) {
+                if (mbar_test(bar, par)) return;
+                const long long t0 = clock64();
+                while (!mbar_test(bar, par)) {
+                    poll_norm();
+                    if (clock64() - t0 > (1ll << 35)) __trap();      // protocol bug: fail loudly
+                }
+            } else {
+                mbar_wait(bar, par);
+            }
+        };
         if (p.wres && leader) mbar_wait(wres_bar, 0);      // the peer's bytes land on the leader's barrier
         for (int t = cid; t < p.total_tiles && leader; t += ncl, ++it) {
             TileCoord tc = decode_tile(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
             const uint32_t use = (p.n_accbuf == 2) ? (uint32_t)(it >> 1) : (uint32_t)it;
             if (kGdn && pend && p.n_accbuf == 1) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(); }
-            mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
+            wait_poll(&tempty_bar[buf], (use & 1) ^ 1);
             tc_fence_after();
             if (lane == 0) LIC_TRACE(it, T_MMA_START);
             const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
@@ -348,7 +603,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
                 const uint32_t sbo = (uint32_t)p.halo_w * 128;
                 for (int c = 0; c < p.kchunks; ++c) {
-                    mbar_wait(&hfull_bar[hs], hphase);
+                    wait_poll(&hfull_bar[hs], hphase);
                     tc_fence_after();
                     const uint32_t hb = smem_u32(smem + p.off_halo + hs * (2 * p.halo_plane_bytes));
                     for (int ti = 0; ti < nt; ++ti) {
@@ -356,7 +611,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         if (p.wres) {
                             bsm = smem_u32(smem + p.off_wres + ((t0 + ti) * p.kchunks + c) * b_bytes);
                         } else {
-                            mbar_wait(&full_bar[stage], phase);
+                            wait_poll(&full_bar[stage], phase);
                             tc_fence_after();
                             bsm = smem_u32(smem + stage * p.stage_bytes);
                         }
@@ -383,13 +638,15 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 }
             } else {
                 const int nk = p.ntaps[tc.ph] * p.kchunks;
+                const int t0k = p.tap0[tc.ph] * p.kchunks;            // resident weights: tile (tap, chunk)
                 for (int k = 0; k < nk; ++k) {
-                    mbar_wait(&full_bar[stage], phase);
+                    wait_poll(&full_bar[stage], phase);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + stage * p.stage_bytes);
                     const uint64_t ah = sdesc_sw128(st);
                     const uint64_t al = sdesc_sw128(st + a_bytes);
-                    const uint64_t bd = sdesc_sw128(st + a_bytes * p.split);
+                    const uint64_t bd = p.wres ? sdesc_sw128(smem_u32(smem + p.off_wres + (t0k + k) * b_bytes))
+                                               : sdesc_sw128(st + a_bytes * p.split);
                     if (elect_one()) {
 #pragma unroll
                         for (int kk = 0; kk < kBK / 16; ++kk) {
@@ -425,7 +682,6 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         uint32_t norm_phase = 0;
         int it = 0;
         int sat = 0;
-        int ost_i = 0;                              // staging slot counter
         for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
             TileCoord tc = decode_tile(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
@@ -439,7 +695,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const uint32_t dcol = (uint32_t)(buf * p.acc_stride);
             const uint32_t taddr = tmem_base + lane_off + dcol;
 
-            const int gy = tc.gy0 + r / p.Wt, gx = tc.gx0 + r % p.Wt;
+            const int gy = tc.gy0 + (r >> p.wt_log2), gx = tc.gx0 + (r & (p.Wt - 1));
             const bool valid = (gy < p.Hg) && (gx < p.Wg);
             const int py = (p.nphase == 4) ? (tc.ph >> 1) : 0;
             const int px = (p.nphase == 4) ? (tc.ph & 1) : 0;
@@ -450,49 +706,56 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const int co0 = tc.nt * p.BN;
             // this warp's 32 pixels form a bw x bh box at tile offset (tx0, ty0)
             const int bw = p.Wt < 32 ? p.Wt : 32, bh = 32 / bw;
-            const int ty0 = (q * 32) / p.Wt, tx0 = (q * 32) % p.Wt;
+            const int ty0 = (q * 32) >> p.wt_log2, tx0 = (q * 32) & (p.Wt - 1);
             const bool tma_ok = p.tma_out && (p.nphase == 1 || tc.gy0 + ty0 + bh <= p.Hg);
             uint8_t* ostage_base = smem + p.off_ostage + (warp - 4) * 2048 * p.ostage_slots;
-            // 16 channels [cb, cb+16) of this thread's pixel -> fp16 hi/lo NHWC activation
+            // 16 channels [cb, cb+16) of this thread's pixel -> fp16 hi/lo NHWC activation.
+            // TMA path: chunks are staged per warp (32 px x 16 ch, hi + lo: 2 KB) into the
+            // warp's ostage_slots slots and flushed together -- one proxy fence and one bulk
+            // group per batch; the first chunk of a batch waits until the previous batch's
+            // stores have read their staging.
+            int npend = 0, pcb0 = 0, pcb1 = 0;
+            auto flush = [&]() {
+                if (npend == 0) return;                       // warp-uniform
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    for (int k = 0; k < npend; ++k) {
+                        uint8_t* os = ostage_base + k * 2048;
+                        const int cb = k ? pcb1 : pcb0;
+                        if (p.nphase == 1) {
+                            tma_store_4d(&mapOH, os, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b);
+                            if (p.split == 2) tma_store_4d(&mapOL, os + 1024, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b);
+                        } else {
+                            const int qyb = tc.b * p.Hg + tc.gy0 + ty0;
+                            tma_store_5d(&mapOH, os, cb, px, tc.gx0 + tx0, py, qyb);
+                            if (p.split == 2) tma_store_5d(&mapOL, os + 1024, cb, px, tc.gx0 + tx0, py, qyb);
+                        }
+                    }
+                    bulk_commit();
+                }
+                __syncwarp();
+                npend = 0;
+            };
             auto emit16 = [&](const float* v16, int cb) {
                 __half* out = reinterpret_cast<__half*>(p.out_act);
                 if (tma_ok) {
-                    uint8_t* ostage = ostage_base + (p.ostage_slots == 2 ? (ost_i & 1) * 2048 : 0);
-                    ++ost_i;
-                    if (lane == 0) {                         // the store that last used this slot has read it
-                        if (p.ostage_slots == 2) bulk_wait_read1(); else bulk_wait_read0();
+                    if (npend == 0) {
+                        if (lane == 0) bulk_wait_read0();
+                        __syncwarp();
                     }
-                    __syncwarp();
+                    uint8_t* ostage = ostage_base + npend * 2048;
                     uint4 h0, h1, l0, l1;
-                    h0.x = h2_bits(v16[0], v16[1]);   h0.y = h2_bits(v16[2], v16[3]);
-                    h0.z = h2_bits(v16[4], v16[5]);   h0.w = h2_bits(v16[6], v16[7]);
-                    h1.x = h2_bits(v16[8], v16[9]);   h1.y = h2_bits(v16[10], v16[11]);
-                    h1.z = h2_bits(v16[12], v16[13]); h1.w = h2_bits(v16[14], v16[15]);
-                    float lv[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) lv[i] = v16[i] - hround(v16[i]);
-                    l0.x = h2_bits(lv[0], lv[1]);   l0.y = h2_bits(lv[2], lv[3]);
-                    l0.z = h2_bits(lv[4], lv[5]);   l0.w = h2_bits(lv[6], lv[7]);
-                    l1.x = h2_bits(lv[8], lv[9]);   l1.y = h2_bits(lv[10], lv[11]);
-                    l1.z = h2_bits(lv[12], lv[13]); l1.w = h2_bits(lv[14], lv[15]);
+                    split2(v16[0], v16[1], h0.x, l0.x);   split2(v16[2], v16[3], h0.y, l0.y);
+                    split2(v16[4], v16[5], h0.z, l0.z);   split2(v16[6], v16[7], h0.w, l0.w);
+                    split2(v16[8], v16[9], h1.x, l1.x);   split2(v16[10], v16[11], h1.y, l1.y);
+                    split2(v16[12], v16[13], h1.z, l1.z); split2(v16[14], v16[15], h1.w, l1.w);
                     reinterpret_cast<uint4*>(ostage)[2 * lane] = h0;
                     reinterpret_cast<uint4*>(ostage)[2 * lane + 1] = h1;
                     reinterpret_cast<uint4*>(ostage + 1024)[2 * lane] = l0;
                     reinterpret_cast<uint4*>(ostage + 1024)[2 * lane + 1] = l1;
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (p.nphase == 1) {
-                            tma_store_4d(&mapOH, ostage, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b);
-                            if (p.split == 2) tma_store_4d(&mapOL, ostage + 1024, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b);
-                        } else {
-                            const int qyb = tc.b * p.Hg + tc.gy0 + ty0;
-                            tma_store_5d(&mapOH, ostage, cb, px, tc.gx0 + tx0, py, qyb);
-                            if (p.split == 2) tma_store_5d(&mapOL, ostage + 1024, cb, px, tc.gx0 + tx0, py, qyb);
-                        }
-                        bulk_commit();
-                    }
-                    __syncwarp();
+                    if (npend == 0) pcb0 = cb; else pcb1 = cb;
+                    if (++npend == p.ostage_slots) flush();
                 } else if (valid) {
                     split_store8(out + pix * p.Cout + cb, p.split == 2 ? out + p.act_plane + pix * p.Cout + cb : nullptr, v16);
                     split_store8(out + pix * p.Cout + cb + 8, p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + 8 : nullptr,
@@ -513,18 +776,16 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                 for (int j = 0; j < GC; ++j) {
                     uint32_t hi[8], lo[8];
-                    const float4* b4 = reinterpret_cast<const float4*>(s_bias + g * G + j * 16);
 #pragma unroll
                     for (int i4 = 0; i4 < 4; ++i4) {
-                        const float4 bb = b4[i4];
+                        const float4 bb = lds4(s_bias + g * G + j * 16 + 4 * i4);
                         x[j][4 * i4 + 0] += bb.x; x[j][4 * i4 + 1] += bb.y;
                         x[j][4 * i4 + 2] += bb.z; x[j][4 * i4 + 3] += bb.w;
                     }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const float a2 = x[j][2 * i] * x[j][2 * i], b2 = x[j][2 * i + 1] * x[j][2 * i + 1];
-                        hi[i] = h2_bits(a2, b2);
-                        lo[i] = h2_bits(a2 - hround(a2), b2 - hround(b2));
+                        split2(a2, b2, hi[i], lo[i]);
                     }
                     tmem_st8(taddr + g * G + j * 8, hi);
                     tmem_st8(taddr + g * G + G / 2 + j * 8, lo);
@@ -553,18 +814,22 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 for (int j = 0; j < GC; ++j) {
                     float n[16];
                     __syncwarp();
-                    tmem_ld16(taddr + p.BN + g * G + j * 16, n);
+                    if (p.dbg_nostore & 4) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) n[i] = x[j][i];
+                    } else {
+                        tmem_ld16(taddr + p.BN + g * G + j * 16, n);
+                    }
                     const int cb = g * G + j * 16;
-                    const float4* be4 = reinterpret_cast<const float4*>(s_beta + cb);
 #pragma unroll
                     for (int i4 = 0; i4 < 4; ++i4) {
-                        const float4 be = be4[i4];
+                        const float4 be = lds4(s_beta + cb + 4 * i4);
                         const float bv[4] = {be.x, be.y, be.z, be.w};
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int i = 4 * i4 + u;
                             const float nn = bv[u] + n[i];
-                            const float rs = rsqrtf(nn);           // MUFU; sqrt(nn) = nn * rsqrt(nn)
+                            const float rs = (p.dbg_nostore & 2) ? nn : rsqrt_ftz(nn);   // MUFU; sqrt(nn) = nn * rsqrt(nn)
                             x[j][i] = (p.ep == EP_GDN) ? x[j][i] * rs : x[j][i] * (nn * rs);
                         }
                     }
@@ -572,7 +837,27 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                         for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(cb + i) * HWo] = x[j][i];
                     }
-                    if (out && !p.dbg_nostore) emit16(x[j], cb);
+                    if (out && !(p.dbg_nostore & 1)) emit16(x[j], cb);
+                }
+            } else if (p.pack4) {
+                // packed g_s L4: channel group g takes sub-pixel phase g (columns 4g .. 4g+2), so
+                // all 16 epilogue warps share the 12 outputs of each grid pixel
+                float v[16];
+                __syncwarp();
+                tmem_ld16(taddr, v);
+                float c3[3] = {v[0], v[1], v[2]};
+#pragma unroll
+                for (int ph = 1; ph < 4; ++ph)
+                    if (g == ph) { c3[0] = v[4 * ph]; c3[1] = v[4 * ph + 1]; c3[2] = v[4 * ph + 2]; }
+                const int ry = 2 * gy + (g >> 1) - p.crop_top, rx = 2 * gx + (g & 1) - p.crop_left;
+                if (valid && ry >= 0 && ry < p.crop_H && rx >= 0 && rx < p.crop_W) {
+                    const size_t o = ((size_t)tc.b * p.crop_H + ry) * p.crop_W + rx;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const float xv = fminf(fmaxf(c3[ch] + s_bias[ch], 0.0f), 1.0f);
+                        if (p.out_f32) p.out_f32[((size_t)tc.b * 3 + ch) * p.crop_H * p.crop_W + (size_t)ry * p.crop_W + rx] = xv;
+                        if (p.out_u8) p.out_u8[o * 3 + ch] = (uint8_t)roundf(xv * 255.0f);
+                    }
                 }
             } else {
                 const int ncol16 = (p.BN + 15) / 16;
@@ -587,10 +872,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                         for (int j = 0; j < 16; ++j) v[j] += s_bias[j & 3];
                     } else {
-                        const float4* b4 = reinterpret_cast<const float4*>(s_bias + cb);
 #pragma unroll
                         for (int i4 = 0; i4 < 4; ++i4) {
-                            const float4 bb = b4[i4];
+                            const float4 bb = lds4(s_bias + cb + 4 * i4);
                             v[4 * i4 + 0] += bb.x; v[4 * i4 + 1] += bb.y; v[4 * i4 + 2] += bb.z; v[4 * i4 + 3] += bb.w;
                         }
                     }
@@ -686,6 +970,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 if constexpr (CG == 2) mbar_arrive_cluster(lbar(&tempty_bar[buf]));
                 else mbar_arrive(&tempty_bar[buf]);
             }
+            flush();                                     // after releasing the accumulator
             if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_END);
         }
         if (p.tma_out && lane == 0) bulk_wait0();

@@ -42,6 +42,11 @@ struct ConvParams {
     int split;                        // 2: activations are fp16 hi + lo planes; 1: hi only
     int cg;                           // 1: one CTA per tile; 2: CTA pair (cta_group::2, M = 256)
     int total_tiles;
+    // tile-index decode without hardware division: q = (umulhi(n, m) + n) >> s (host-computed
+    // magic numbers, exact for n < 2^31); Wt and nphase are powers of two
+    uint32_t fd_nt_m, fd_txs_m, fd_ty_m;
+    int fd_nt_s, fd_txs_s, fd_ty_s;
+    int txs, wt_log2, nph_log2;
     // ---- kernel resources (host-computed)
     int stages;
     uint32_t stage_bytes, off_gamma, off_bar, off_par, smem_bytes;
@@ -74,6 +79,17 @@ struct ConvParams {
     unsigned long long* sat_count;    // saturation counter (nullable)
     unsigned long long* trace;        // test-only: per-tile clock64 events of CTA 0 (nullable)
     int dbg_nostore;                  // test-only experiment switch: skip activation stores
+    // fused g_a L1 (im2col GEMM, K = 75 padded to 128): warps 0, 2 and 3 build the A tiles
+    // (hi, lo) in shared memory straight from the frame -- u8 HWC (x = u8 / 255) or f32 CHW --
+    // through a per-tile input patch; no ingest kernel and no im2col tensor in HBM.  Tile fixed
+    // at Wt = 16, Ht = 8 (patch 19 rows x 35 px x 3 ch fp32, double-buffered); stage s holds K
+    // chunk s; the weights stay resident.
+    int fuse_l1;
+    const void* frame;                // u8 [B][H][W][3] or f32 [B][3][H][W] (device)
+    int fr_u8, fr_H, fr_W, fr_top, fr_left;   // frame size and its offset in the padded grid
+    uint32_t off_patch;               // split patch [2][hi, lo][19][112] fp16
+    uint32_t off_lut;                 // u8 LUT [257] (hi | lo << 16; entry 256 = 0)
+    uint32_t off_raw;                 // raw u8 patch [2][19][112] (cp.async, u8 frames)
     // TMA-store epilogue: each epilogue warp stages 32 px x 16 ch (hi, lo: 1 KB each) in smem and
     // writes it with a bulk tensor store; out maps: conv (C, W, H, B), deconv phase view
     // (C, px, W/2, py, B*H/2) of the NHWC output, one map per plane

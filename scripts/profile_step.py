@@ -2,7 +2,7 @@
 decode) at the bench workload, in a fixed kernel order for ncu:
 
   conv_umma launches per pass: ga1 ga2 ga3 ga4 ha1 ha2 ha3 hs1 hs2 hs3 | hs1 hs2 hs3 | gs1 gs2 gs3 gs4
-  (plus ingest_im2col before ga1 and sym_ingest before each decoder stage)
+  (plus sym_ingest before each decoder stage; frame ingest is fused into ga1)
 
     ncu --set full -k regex:conv_umma -s 17 -c 17 -o prof python scripts/profile_step.py
 """
