@@ -12,9 +12,12 @@
 // B200 design: the calling thread is the GPU control thread; it services three GPU task
 // kinds (ENC, IDX = decoder GPU1, DEC = decoder GPU2) from a ready queue, oldest-batch
 // and latest-stage first.  Worker threads run the per-frame coder tasks (C1: rANS encode
-// y and z, then decode z; C2: decode y).  Batches live in `inflight` pinned, device-mapped
-// slots: encode kernels write symbol planes straight into them (zero-copy)
-// and the decoder kernels read the decoded planes from them.
+// y and z, then decode z; C2: decode y).  Batches live in `inflight` slots, each with pinned
+// host planes (what the coder reads / writes) and device planes (what the kernels read /
+// write).  Three streams: kernels on `stream`, host->device copies on `cstream`,
+// device->host copies on `dstream` (symbol planes, and frames when the caller's frames are
+// in host memory), ordered by events, so the copies of one batch overlap the kernels of the
+// next and the two copy engines run concurrently.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,8 +42,13 @@ enum GpuKind { G_ENC = 0, G_IDX = 1, G_DEC = 2 };
 enum CpuKind { C_ONE = 0, C_TWO = 1 };
 
 struct Slot {
+    // pinned host planes (coder side)
     int8_t* y_sym = nullptr;  uint8_t* y_idx = nullptr;  int8_t* z_sym = nullptr;
     int8_t* z_dec = nullptr;  uint8_t* idx_dec = nullptr; int8_t* y_dec = nullptr;
+    // device planes (kernel side) and frame staging (host frames only)
+    int8_t* d_ysym = nullptr; uint8_t* d_yidx = nullptr; int8_t* d_zsym = nullptr;
+    int8_t* d_zdec = nullptr; uint8_t* d_idxdec = nullptr; int8_t* d_ydec = nullptr;
+    uint8_t* d_fin = nullptr; uint8_t* d_fout = nullptr;
     std::vector<std::vector<uint8_t>> ystr, zstr;
     std::vector<size_t> ylen, zlen;
     int batch = -1;
@@ -68,7 +76,11 @@ struct lic_pipeline {
     lic_rans_tables* tab_z = nullptr;
     std::vector<Slot> slots;
     std::vector<void*> pinned;
-    cudaStream_t stream = nullptr;          // all GPU stages, in issue order
+    std::vector<void*> dev;                 // device slot planes
+    cudaStream_t stream = nullptr;          // kernels, in issue order
+    cudaStream_t cstream = nullptr;         // host -> device copies
+    cudaStream_t dstream = nullptr;         // device -> host copies (the other copy engine)
+    bool in_host = false, out_host = false; // caller's frames in host memory (staged per slot)
     std::vector<cudaEvent_t> events;        // completion events, recycled
     std::deque<Pending> pending;            // issued, not yet completed (FIFO)
     // threading
@@ -156,9 +168,14 @@ extern "C" void lic_pipeline_close(lic_pipeline* p) {
     p->cv_cpu.notify_all();
     for (auto& t : p->workers) t.join();
     if (p->stream) cudaStreamSynchronize(p->stream);
+    if (p->cstream) cudaStreamSynchronize(p->cstream);
+    if (p->dstream) cudaStreamSynchronize(p->dstream);
     for (cudaEvent_t e : p->events) cudaEventDestroy(e);
     if (p->stream) cudaStreamDestroy(p->stream);
+    if (p->cstream) cudaStreamDestroy(p->cstream);
+    if (p->dstream) cudaStreamDestroy(p->dstream);
     for (void* q : p->pinned) cudaFreeHost(q);
+    for (void* q : p->dev) cudaFree(q);
     lic_rans_tables_free(p->tab_y);
     lic_rans_tables_free(p->tab_z);
     delete p;
@@ -203,8 +220,30 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
         p->pinned.push_back(q);
         return q;
     };
+    auto dalloc = [&](size_t bytes) -> void* {
+        void* q = nullptr;
+        if (cudaMalloc(&q, bytes ? bytes : 16) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        p->dev.push_back(q);
+        return q;
+    };
+    const size_t fbytes = B * lic_internal_frame_pixels(codec) * 3 * (cfg->u8 ? 1 : 4);
     p->slots.resize(p->cfg.inflight);
     for (Slot& s : p->slots) {
+        s.d_ysym = (int8_t*)dalloc(B * p->ny);
+        s.d_ydec = (int8_t*)dalloc(B * p->ny);
+        s.d_yidx = (uint8_t*)dalloc(p->hyper ? B * p->ny : 16);
+        s.d_idxdec = (uint8_t*)dalloc(p->hyper ? B * p->ny : 16);
+        s.d_zsym = (int8_t*)dalloc(p->hyper ? B * p->nz : 16);
+        s.d_zdec = (int8_t*)dalloc(p->hyper ? B * p->nz : 16);
+        s.d_fin = (uint8_t*)dalloc(fbytes);
+        s.d_fout = (uint8_t*)dalloc(fbytes);
+        if (!s.d_ysym || !s.d_ydec || !s.d_yidx || !s.d_idxdec || !s.d_zsym || !s.d_zdec || !s.d_fin || !s.d_fout) {
+            lic_pipeline_close(p);
+            return LIC_ENOMEM;
+        }
         s.y_sym = (int8_t*)pin(B * p->ny);
         s.y_dec = (int8_t*)pin(B * p->ny);
         s.y_idx = (uint8_t*)pin(p->hyper ? B * p->ny : 16);
@@ -220,12 +259,14 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
         s.ylen.assign(B, 0);
         s.zlen.assign(B, 0);
     }
-    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p->cstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p->dstream, cudaStreamNonBlocking) != cudaSuccess) {
         cudaGetLastError();
         lic_pipeline_close(p);
         return LIC_ECUDA;
     }
-    p->events.resize(8);
+    p->events.resize(32);
     for (auto& e : p->events)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
             cudaGetLastError();
@@ -237,27 +278,74 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
     return LIC_OK;
 }
 
-static lic_status gpu_call(lic_pipeline* p, const GpuTask& t) {
+// cstream -> stream -> cstream ordering through recycled events (a wait captures the event's
+// state when it is enqueued, so re-recording an event later is harmless)
+static cudaEvent_t next_event(lic_pipeline* p, size_t& ev_next) { return p->events[ev_next++ % p->events.size()]; }
+static bool join(lic_pipeline* p, cudaStream_t from, cudaStream_t to, size_t& ev_next) {
+    cudaEvent_t e = next_event(p, ev_next);
+    return cudaEventRecord(e, from) == cudaSuccess && cudaStreamWaitEvent(to, e, 0) == cudaSuccess;
+}
+
+// Issues one GPU task: H2D inputs (cstream), kernels (stream), D2H outputs (cstream); returns
+// with `done` recorded after the last step.
+static lic_status gpu_call(lic_pipeline* p, const GpuTask& t, cudaEvent_t done, size_t& ev_next) {
     Slot& s = p->slots[t.slot];
     const uint32_t B = p->cfg.batch;
     const size_t b = (size_t)s.batch;
+    const size_t fb = (size_t)B * p->in_bytes;
+    lic_status st = LIC_OK;
+    auto cp = [&](void* dst, const void* src, size_t n, cudaMemcpyKind k) {
+        cudaStream_t cs = k == cudaMemcpyHostToDevice ? p->cstream : p->dstream;
+        if (!st && cudaMemcpyAsync(dst, src, n, k, cs) != cudaSuccess) st = LIC_ECUDA;
+    };
+    auto to_k = [&]() { if (!st && !join(p, p->cstream, p->stream, ev_next)) st = LIC_ECUDA; };
+    auto to_c = [&]() { if (!st && !join(p, p->stream, p->dstream, ev_next)) st = LIC_ECUDA; };
     switch (t.kind) {
     case G_ENC: {
-        const uint8_t* fr = p->in + b * B * p->in_bytes;
-        return p->cfg.u8 ? lic_encode_u8(p->codec, fr, B, s.y_sym, p->hyper ? s.y_idx : nullptr,
-                                         p->hyper ? s.z_sym : nullptr, nullptr, p->stream)
-                         : lic_encode(p->codec, (const float*)fr, B, s.y_sym, p->hyper ? s.y_idx : nullptr,
-                                      p->hyper ? s.z_sym : nullptr, nullptr, p->stream);
+        const uint8_t* fr = p->in + b * fb;
+        if (p->in_host) { cp(s.d_fin, fr, fb, cudaMemcpyHostToDevice); to_k(); fr = s.d_fin; }
+        if (!st)
+            st = p->cfg.u8 ? lic_encode_u8(p->codec, fr, B, s.d_ysym, p->hyper ? s.d_yidx : nullptr,
+                                           p->hyper ? s.d_zsym : nullptr, nullptr, p->stream)
+                           : lic_encode(p->codec, (const float*)fr, B, s.d_ysym, p->hyper ? s.d_yidx : nullptr,
+                                        p->hyper ? s.d_zsym : nullptr, nullptr, p->stream);
+        to_c();
+        cp(s.y_sym, s.d_ysym, B * p->ny, cudaMemcpyDeviceToHost);
+        if (p->hyper) {
+            cp(s.y_idx, s.d_yidx, B * p->ny, cudaMemcpyDeviceToHost);
+            cp(s.z_sym, s.d_zsym, B * p->nz, cudaMemcpyDeviceToHost);
+        }
+        break;
     }
     case G_IDX:
-        return lic_hyper_indexes(p->codec, s.z_dec, B, s.idx_dec, p->stream);
+        cp(s.d_zdec, s.z_dec, B * p->nz, cudaMemcpyHostToDevice);
+        to_k();
+        if (!st) st = lic_hyper_indexes(p->codec, s.d_zdec, B, s.d_idxdec, p->stream);
+        to_c();
+        cp(s.idx_dec, s.d_idxdec, B * p->ny, cudaMemcpyDeviceToHost);
+        break;
     case G_DEC: {
-        uint8_t* fr = p->out + b * B * p->out_bytes;
-        return p->cfg.u8 ? lic_decode_u8(p->codec, s.y_dec, B, fr, p->stream)
-                         : lic_decode(p->codec, s.y_dec, B, (float*)fr, p->stream);
+        cp(s.d_ydec, s.y_dec, B * p->ny, cudaMemcpyHostToDevice);
+        to_k();
+        uint8_t* fr = p->out + b * fb;
+        uint8_t* dst = p->out_host ? s.d_fout : fr;
+        if (!st)
+            st = p->cfg.u8 ? lic_decode_u8(p->codec, s.d_ydec, B, dst, p->stream)
+                           : lic_decode(p->codec, s.d_ydec, B, (float*)dst, p->stream);
+        to_c();
+        if (p->out_host) cp(fr, s.d_fout, fb, cudaMemcpyDeviceToHost);
+        break;
     }
     }
-    return LIC_EINVAL;
+    // every task ends with kernels -> dstream (possibly no copies after them)
+    if (!st && cudaEventRecord(done, p->dstream) != cudaSuccess) st = LIC_ECUDA;
+    return st;
+}
+
+static bool is_host(const void* q) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, q) != cudaSuccess) { cudaGetLastError(); return true; }
+    return a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged;
 }
 
 extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, uint32_t nframes, void* frames_out,
@@ -271,6 +359,8 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         std::lock_guard<std::mutex> g(p->mu);
         p->in = (const uint8_t*)frames_in;
         p->out = (uint8_t*)frames_out;
+        p->in_host = is_host(frames_in);
+        p->out_host = is_host(frames_out);
         p->nbatches = (int)(nframes / B);
         p->next_enc = 0;
         p->done = 0;
@@ -293,7 +383,7 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
     // kMaxPending in flight) so the device never idles while ready work exists; the
     // oldest issued task is retired by waiting on its event, which then releases its
     // coder tasks (ENC, IDX) or its slot (DEC).
-    constexpr size_t kMaxPending = 2;
+    constexpr size_t kMaxPending = 3;
     size_t ev_next = 0;
     for (;;) {
         GpuTask t{};
@@ -331,9 +421,8 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         }
         if (issue) {
             const double g0 = now_s();
-            lic_status st = gpu_call(p, t);
-            cudaEvent_t ev = p->events[ev_next++ % p->events.size()];
-            if (!st && cudaEventRecord(ev, p->stream) != cudaSuccess) st = LIC_ECUDA;
+            cudaEvent_t ev = next_event(p, ev_next);
+            lic_status st = gpu_call(p, t, ev, ev_next);
             std::lock_guard<std::mutex> g(p->mu);
             if (st) { p->err = st; break; }
             p->pending.push_back({t, ev, g0});
@@ -373,8 +462,10 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
             ++p->done;
         }
     }
-    // leave nothing running on the stream
+    // leave nothing running on the streams
     cudaStreamSynchronize(p->stream);
+    cudaStreamSynchronize(p->cstream);
+    cudaStreamSynchronize(p->dstream);
     const double t_run1 = now_s();
     // error path: drop queued coder work and wait for tasks already running
     std::unique_lock<std::mutex> g(p->mu);
