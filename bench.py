@@ -170,6 +170,8 @@ def main():
     ap.add_argument("--batch", type=int, default=4, help="frames per step (per GPU)")
     ap.add_argument("--coder-threads", type=int, default=0, help="0: derived from the host cores")
     ap.add_argument("--inflight", type=int, default=8)
+    ap.add_argument("--substreams", type=int, default=8,
+                    help="y string as K channel-slab rANS substreams (DESIGN.md R21); 1 = one string")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--serial", action="store_true", help="serial reference pipeline (no overlap)")
     ap.add_argument("--zero-copy", action="store_true", help="kernels touch pinned host planes in place")
@@ -200,7 +202,7 @@ def main():
     codec = lic.Codec(blob, H, W, max_batch=B, device=local)
     codec.set_zero_copy(args.zero_copy)
     pipe = lic.Pipeline(codec, coder_threads=threads, batch=B, inflight=args.inflight, u8=True,
-                        serial=args.serial)
+                        serial=args.serial, substreams=args.substreams)
 
     # synthetic stream: 8 distinct frames per rank, looped (the paper loops one image)
     base = torch.from_numpy(synth_frames_u8(8, H, W, seed=1000 + rank))
@@ -297,6 +299,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": WORKLOAD, "batch_per_gpu": B, "frames_per_gpu": nfr,
                    "coder_threads_per_gpu": threads, "inflight": args.inflight,
+                   "y_substreams": args.substreams,
                    "l2": "inputs larger than L2 (activations ~0.36 GB per frame, frame set > 126 MB)",
                    "pipeline": "serial" if args.serial else "overlapped"},
         "latency_ms": {"p50": round(st["latency_p50_ms"], 3), "p95": round(st["latency_p95_ms"], 3),
@@ -318,7 +321,8 @@ def main():
     # ---- end-of-run bitstream gather (off the timed loop): every rank's per-frame strings
     # for its first frames, ordered by global frame index on rank 0
     from paper_2208_01641_b200.dist import gather_bitstreams, stream_digest
-    vp = lic.Pipeline(codec, coder_threads=threads, batch=B, inflight=2, u8=True, keep_bitstreams=True)
+    vp = lic.Pipeline(codec, coder_threads=threads, batch=B, inflight=2, u8=True, keep_bitstreams=True,
+                      substreams=args.substreams)
     vst = vp.run(dev_in, dev_out, 2 * B)
     local = {rank + world * i: vp.bitstream(i) for i in range(2 * B)}
     vp.close()

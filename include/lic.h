@@ -208,6 +208,7 @@ typedef struct {
     int u8;                   /* frames are u8 [H][W][3] (1) or f32 [3][H][W] (0) */
     int serial;               /* 1: no overlap between stages (reference) */
     int keep_bitstreams;      /* 1: keep every frame's strings for lic_pipeline_bitstream */
+    uint32_t substreams;      /* y string as K channel-slab substreams (lic_rans_encode_slabs); 0 or 1: one string */
 } lic_pipeline_config;
 typedef struct {
     uint64_t frames;          /* frames completed */
@@ -239,6 +240,21 @@ lic_status lic_rans_encode_fast(const lic_rans_tables* t, const int8_t* sym, con
                                 uint8_t* out, size_t cap, size_t* out_len);
 lic_status lic_rans_decode_fast(const lic_rans_tables* t, const uint8_t* in, size_t len, const uint8_t* row,
                                 lic_shape plane, int8_t* sym_out);
+
+/* Channel-slab substreams ("the entropy coding process
+ * is highly CPU-intensive", :195 faster coders as future work; reading R21).  The
+ * C x H x W plane is cut into K channel slabs, slab k = channels [floor(k*C/K),
+ * floor((k+1)*C/K)), and every slab is coded as an independent string in exactly the
+ * lic_rans_encode format (rows as there: row[i] per symbol, or the channel).
+ *   K == 1: the plain string (identical to lic_rans_encode_fast).
+ *   K >  1: K big-endian u32 string lengths, then the K strings in slab order.
+ * One call codes the K strings in lockstep on the calling thread (independent dependency
+ * chains overlap in the core).  1 <= K <= min(64, C).  Errors as lic_rans_encode /
+ * lic_rans_decode; a framing whose lengths do not add up to `len` is LIC_ECORRUPT. */
+lic_status lic_rans_encode_slabs(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row, lic_shape plane,
+                                 uint32_t K, uint8_t* out, size_t cap, size_t* out_len);
+lic_status lic_rans_decode_slabs(const lic_rans_tables* t, const uint8_t* in, size_t len, const uint8_t* row,
+                                 lic_shape plane, uint32_t K, int8_t* sym_out);
 
 /* Library version string. */
 const char* lic_version(void);

@@ -209,6 +209,57 @@ def rans_decode(data, rows, cdf, sym_min=None):
     return sym
 
 
+def slab_bounds(C, K):
+    """Channel slab k = [floor(k*C/K), floor((k+1)*C/K)) (R21)."""
+    return [(k * C // K, (k + 1) * C // K) for k in range(K)]
+
+
+def rans_encode_slabs(sym_chw, rows_chw, cdf, K):
+    """K channel-slab substreams (DESIGN.md R21): each slab an independent step-10 string;
+    K = 1 is the plain string, K > 1 is K big-endian u32 lengths followed by the strings.
+    rows_chw None: the row of a symbol is its channel."""
+    sym_chw = np.asarray(sym_chw)
+    C = sym_chw.shape[0]
+    if K == 1:
+        rows = channel_rows(sym_chw.shape) if rows_chw is None else np.asarray(rows_chw, np.int32).ravel()
+        return rans_encode(sym_chw, rows, cdf)
+    parts = []
+    for c0, c1 in slab_bounds(C, K):
+        sub = sym_chw[c0:c1]
+        if rows_chw is None:
+            rows = channel_rows(sub.shape) + c0
+        else:
+            rows = np.asarray(rows_chw[c0:c1], np.int32).ravel()
+        parts.append(rans_encode(sub, rows, cdf))
+    head = b"".join(len(p).to_bytes(4, "big") for p in parts)
+    return head + b"".join(parts)
+
+
+def rans_decode_slabs(data, shape, rows_chw, cdf, K):
+    """Inverse of rans_encode_slabs; CorruptStream on a bad framing."""
+    C, H, W = shape
+    if K == 1:
+        rows = channel_rows(shape) if rows_chw is None else np.asarray(rows_chw, np.int32).ravel()
+        return rans_decode(data, rows, cdf).reshape(shape)
+    data = bytes(data)
+    if len(data) < 4 * K:
+        raise CorruptStream()
+    lens = [int.from_bytes(data[4 * k:4 * k + 4], "big") for k in range(K)]
+    if 4 * K + sum(lens) != len(data):
+        raise CorruptStream()
+    out = np.empty(shape, np.int8)
+    pos = 4 * K
+    for (c0, c1), n in zip(slab_bounds(C, K), lens):
+        sub_shape = (c1 - c0, H, W)
+        if rows_chw is None:
+            rows = channel_rows(sub_shape) + c0
+        else:
+            rows = np.asarray(rows_chw[c0:c1], np.int32).ravel()
+        out[c0:c1] = rans_decode(data[pos:pos + n], rows, cdf).reshape(sub_shape)
+        pos += n
+    return out
+
+
 def channel_rows(shape):
     """Row index per symbol of a C x H x W plane coded with per-channel tables."""
     C, H, W = shape
@@ -244,21 +295,27 @@ def pad_chw(x, hyper):
 
 
 # ---------------------------------------------------------------- transforms
-def g_a(x, w):
-    """g_a: conv5s2 -> GDN x3 -> conv5s2 N->M."""
+def _norm(act):
+    """Activation of g_a / g_s: 0 GDN, 1 1DN (the paper's
+    implementation C)."""
+    return onedn if act == 1 else gdn
+
+
+def g_a(x, w, act=0):
+    """g_a: conv5s2 -> GDN (or 1DN) x3 -> conv5s2 N->M."""
     h = x
     for i in (1, 2, 3):
         h = conv2d(h, w[f"ga{i}.w"], w[f"ga{i}.b"], 2, 2)
-        h = gdn(h, w[f"ga{i}.beta"], w[f"ga{i}.gamma"], inverse=False)
+        h = _norm(act)(h, w[f"ga{i}.beta"], w[f"ga{i}.gamma"], inverse=False)
     return conv2d(h, w["ga4.w"], w["ga4.b"], 2, 2)
 
 
-def g_s(yhat, w):
-    """g_s: deconv5s2 (output_padding 1) -> IGDN x3 -> deconv N->3."""
+def g_s(yhat, w, act=0):
+    """g_s: deconv5s2 (output_padding 1) -> IGDN (or inverse 1DN) x3 -> deconv N->3."""
     h = yhat
     for i in (1, 2, 3):
         h = deconv2d(h, w[f"gs{i}.w"], w[f"gs{i}.b"], 2, 2, 1)
-        h = gdn(h, w[f"gs{i}.beta"], w[f"gs{i}.gamma"], inverse=True)
+        h = _norm(act)(h, w[f"gs{i}.beta"], w[f"gs{i}.gamma"], inverse=True)
     return deconv2d(h, w["gs4.w"], w["gs4.b"], 2, 2, 1)
 
 
@@ -292,9 +349,9 @@ def build_tables(w, hyper, L):
     return Tables(cdf_table(w["sigma_y"], L), None, None)
 
 
-def encode_planes(x_pad, w, hyper, L):
+def encode_planes(x_pad, w, hyper, L, act=0):
     """GPU half of encode: returns the latents and planes."""
-    y = g_a(x_pad, w)
+    y = g_a(x_pad, w, act)
     out = {"y": y}
     if not hyper:
         sym, yhat, nsat = quantize(y, w["mu_y"], L)
@@ -310,12 +367,13 @@ def encode_planes(x_pad, w, hyper, L):
     return out
 
 
-def code_planes(planes, tables, hyper):
-    """CPU half of encode: rANS strings."""
+def code_planes(planes, tables, hyper, substreams=1):
+    """CPU half of encode: rANS strings; the y string as `substreams`
+    channel slabs (R21; 1 = one plain string)."""
     ys = planes["y_sym"]
     if not hyper:
-        return rans_encode(ys, channel_rows(ys.shape), tables.fact_y), None
-    yb = rans_encode(ys, planes["y_idx"].astype(np.int32), tables.gauss)
+        return rans_encode_slabs(ys, None, tables.fact_y, substreams), None
+    yb = rans_encode_slabs(ys, planes["y_idx"], tables.gauss, substreams)
     zs = planes["z_sym"]
     zb = rans_encode(zs, channel_rows(zs.shape), tables.z)
     return yb, zb
@@ -327,21 +385,21 @@ def hyper_indexes(z_sym, w):
     return scale_index(h_s(zhat, w), w["scale_table"])
 
 
-def decode_frame(y_sym, w, hyper, crop, H, W):
+def decode_frame(y_sym, w, hyper, crop, H, W, act=0):
     """Decoder GPU2: y-hat = s + mu (hyper mu = 0), x-hat =
     clamp(g_s(y-hat), 0, 1), cropped by the pad offsets."""
     yhat = dequantize(y_sym, None if hyper else w["mu_y"])
-    xh = np.clip(g_s(yhat, w), np.float32(0.0), np.float32(1.0))
+    xh = np.clip(g_s(yhat, w, act), np.float32(0.0), np.float32(1.0))
     top, left = crop
     return np.ascontiguousarray(xh[:, top:top + H, left:left + W])
 
 
-def decode_strings(yb, zb, w, tables, hyper, y_shape, z_shape, crop, H, W):
+def decode_strings(yb, zb, w, tables, hyper, y_shape, z_shape, crop, H, W, substreams=1, act=0):
     """Full decode: CPU1 rANS(z) -> GPU1 h_s -> CPU2 rANS(y) -> GPU2 g_s."""
     if hyper:
         zs = rans_decode(zb, channel_rows(z_shape), tables.z).reshape(z_shape)
         idx = hyper_indexes(zs, w)
-        ys = rans_decode(yb, idx.astype(np.int32), tables.gauss).reshape(y_shape)
+        ys = rans_decode_slabs(yb, y_shape, idx, tables.gauss, substreams)
     else:
-        ys = rans_decode(yb, channel_rows(y_shape), tables.fact_y).reshape(y_shape)
-    return decode_frame(ys, w, hyper, crop, H, W), ys
+        ys = rans_decode_slabs(yb, y_shape, None, tables.fact_y, substreams)
+    return decode_frame(ys, w, hyper, crop, H, W, act), ys

@@ -637,7 +637,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     c->N = rd<uint16_t>(licw + 7);
     c->M = rd<uint16_t>(licw + 9);
     c->L = rd<uint16_t>(licw + 11);
-    if (c->kind > 1 || c->act != 0) return bail(LIC_EINVAL);      // 1DN: NEXT-1
+    if (c->kind > 1 || c->act > 1) return bail(LIC_EINVAL);       // act 0 GDN, 1 1DN
     if (c->N % 64 || c->M % 64 || c->N < 64 || c->N > 256 || c->M < 64 || c->M > 512 || c->L < 1 || c->L > 127)
         return bail(LIC_EINVAL);
     // ---- parse blocks
@@ -812,6 +812,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     }
     c->layers[GA4].prm.mu = c->kind == 0 ? c->mu_y : nullptr;
     c->layers[GA4].prm.abs_out = c->kind == 1;
+    for (int l : {GA1, GA2, GA3, GS1, GS2, GS3}) c->layers[l].prm.onedn = c->act == 1;
     if (c->kind == 1) c->layers[HA3].prm.mu = c->mu_z;
     c->layers[GS4].prm.crop_top = c->top;
     c->layers[GS4].prm.crop_left = c->left;

@@ -124,6 +124,11 @@ constexpr uint32_t kL1RawBytes = kL1PH * kL1RawWords * 4;           // one raw u
 static_assert(kL1Wt == 16, "build_l1 decodes r -> (r >> 4, r & 15)");
 
 // MUFU.RSQ without the denormal-input fix-up (GDN/IGDN: beta + n >= beta > 0, normal)
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float rsqrt_ftz(float x) {
     float y;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -782,10 +787,15 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         x[j][4 * i4 + 0] += bb.x; x[j][4 * i4 + 1] += bb.y;
                         x[j][4 * i4 + 2] += bb.z; x[j][4 * i4 + 3] += bb.w;
                     }
+                    if (p.onedn) {
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const float a2 = x[j][2 * i] * x[j][2 * i], b2 = x[j][2 * i + 1] * x[j][2 * i + 1];
-                        split2(a2, b2, hi[i], lo[i]);
+                        for (int i = 0; i < 8; ++i) split2(fabsf(x[j][2 * i]), fabsf(x[j][2 * i + 1]), hi[i], lo[i]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float a2 = x[j][2 * i] * x[j][2 * i], b2 = x[j][2 * i + 1] * x[j][2 * i + 1];
+                            split2(a2, b2, hi[i], lo[i]);
+                        }
                     }
                     tmem_st8(taddr + g * G + j * 8, hi);
                     tmem_st8(taddr + g * G + G / 2 + j * 8, lo);
@@ -825,12 +835,22 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     for (int i4 = 0; i4 < 4; ++i4) {
                         const float4 be = lds4(s_beta + cb + 4 * i4);
                         const float bv[4] = {be.x, be.y, be.z, be.w};
+                        if (p.onedn) {
+                            // 1DN: y = x / n (forward), x * n (inverse); n = beta + gamma |x|
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int i = 4 * i4 + u;
-                            const float nn = bv[u] + n[i];
-                            const float rs = (p.dbg_nostore & 2) ? nn : rsqrt_ftz(nn);   // MUFU; sqrt(nn) = nn * rsqrt(nn)
-                            x[j][i] = (p.ep == EP_GDN) ? x[j][i] * rs : x[j][i] * (nn * rs);
+                            for (int u = 0; u < 4; ++u) {
+                                const int i = 4 * i4 + u;
+                                const float nn = bv[u] + n[i];
+                                x[j][i] = (p.ep == EP_GDN) ? x[j][i] * rcp_ftz(nn) : x[j][i] * nn;
+                            }
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int i = 4 * i4 + u;
+                                const float nn = bv[u] + n[i];
+                                const float rs = (p.dbg_nostore & 2) ? nn : rsqrt_ftz(nn);   // MUFU; sqrt(nn) = nn * rsqrt(nn)
+                                x[j][i] = (p.ep == EP_GDN) ? x[j][i] * rs : x[j][i] * (nn * rs);
+                            }
                         }
                     }
                     if (valid && p.out_f32) {

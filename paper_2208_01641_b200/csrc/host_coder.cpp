@@ -284,3 +284,293 @@ extern "C" lic_status lic_rans_decode_fast(const lic_rans_tables* t, const uint8
     if (x != kRansLow || p != end) return LIC_ECORRUPT;
     return LIC_OK;
 }
+
+// ------------------------------------------------------------------ channel-slab substreams
+// NEXT-2 ("the entropy coding process is highly CPU-intensive",
+// :195 faster coders as future work; reading R21).  A C x H x W plane is cut into K
+// channel slabs [floor(kC/K), floor((k+1)C/K)); every slab is coded as an independent rANS string
+// in exactly the format above.  K = 1 is the plain string; K > 1 frames the strings as K big-endian
+// u32 lengths followed by the K strings.  One thread codes the K strings in lockstep (symbol i of
+// slab 0, of slab 1, ...): the per-string dependency chains (mulhi / table lookup / renormalise)
+// are independent, so they overlap in the core's pipelines instead of running back to back.
+namespace {
+
+struct SlabGeom {
+    uint32_t K;
+    size_t hw;
+    size_t begin[64], count[64];       // symbol range of slab k
+    uint32_t ch0[64];                   // first channel of slab k
+};
+
+bool slab_geom(lic_shape plane, uint32_t K, SlabGeom& g) {
+    if (K == 0 || K > 64 || K > (plane.c ? plane.c : 1)) return false;
+    g.K = K;
+    g.hw = (size_t)plane.h * plane.w;
+    for (uint32_t k = 0; k < K; ++k) {
+        const uint32_t c0 = (uint32_t)((uint64_t)k * plane.c / K), c1 = (uint32_t)((uint64_t)(k + 1) * plane.c / K);
+        g.ch0[k] = c0;
+        g.begin[k] = (size_t)c0 * g.hw;
+        g.count[k] = (size_t)(c1 - c0) * g.hw;
+    }
+    return true;
+}
+
+#define LIC_INLINE inline __attribute__((always_inline))
+
+// One encoder step (symbol idx) of one string.  kRow: row[idx] per symbol, else the channel,
+// tracked by a countdown (ch, rem) instead of a division.  Renormalisation emits at most two
+// bytes (x < 2^31, xmax >= 2^15) and is branch-free: the byte is always stored one below the
+// pointer, which only advances when it is emitted.
+// Table fields are passed by value (locals): the byte stores through uint8_t* may alias any
+// memory, so fields read through `t` would be reloaded after every store.
+struct EncCtx { const EncSym* enc; uint32_t nsym, nrows; int smin; };
+struct DecCtx { const uint32_t* cdf; const uint8_t* bucket; uint32_t row_len, nrows; int smin; };
+
+template <bool kRow>
+LIC_INLINE void enc_step(const EncCtx t, const int8_t* sym, const uint8_t* row, size_t hw, size_t idx,
+                         uint32_t& x, uint8_t*& ptr, uint32_t& ch, size_t& rem) {
+    uint32_t r;
+    if (kRow) {
+        r = row[idx];
+    } else {
+        r = ch;
+        if (--rem == 0) { --ch; rem = hw; }
+    }
+    const int s = (int)sym[idx] - t.smin;       // validated by the caller (validate_planes)
+    const EncSym e = t.enc[(size_t)r * t.nsym + s];
+    uint32_t xv = x;
+    uint8_t* pj = ptr;
+    pj[-1] = (uint8_t)xv;
+    const uint32_t e1 = xv >= e.xmax;
+    pj -= e1; xv >>= 8 * e1;
+    pj[-1] = (uint8_t)xv;
+    const uint32_t e2 = xv >= e.xmax;
+    pj -= e2; xv >>= 8 * e2;
+    const uint32_t q = (uint32_t)(((uint64_t)xv * e.rcp) >> 32) >> e.shift;
+    x = xv + e.bias + q * (uint32_t)e.cmpl;
+    ptr = pj;
+}
+
+// Encoder: G strings, last symbol to first.  String j writes backwards from hi[j] into a scratch
+// region of 2 * count + 8 bytes (<= 2 bytes per symbol + the 4-byte state, so it cannot
+// overflow).  Strings longer than the shortest first code their extra tail symbols alone, then
+// all G run in lockstep over the common prefix.
+template <int G, bool kRow>
+lic_status enc_group(const lic_rans_tables* tab, const int8_t* __restrict sym, const uint8_t* __restrict row,
+                     const SlabGeom& g, int k0, uint8_t* const* hi, uint8_t** ptr_out) {
+    const EncCtx t{tab->enc.data(), tab->nsym, tab->n_rows, tab->sym_min};
+    const size_t hw = g.hw ? g.hw : 1;
+    uint32_t x[G], ch[G];
+    uint8_t* ptr[G];
+    size_t rem[G], beg[G];
+    size_t nmin = ~size_t(0);
+    for (int j = 0; j < G; ++j) {
+        const size_t c = g.count[k0 + j];
+        x[j] = kRansLow; ptr[j] = hi[j]; beg[j] = g.begin[k0 + j];
+        ch[j] = g.ch0[k0 + j] + (uint32_t)(c ? (c - 1) / hw : 0);
+        rem[j] = c ? (c - 1) % hw + 1 : 0;
+        nmin = std::min(nmin, c);
+    }
+    for (int j = 0; j < G; ++j)
+        for (size_t i = g.count[k0 + j]; i-- > nmin;) enc_step<kRow>(t, sym, row, hw, beg[j] + i, x[j], ptr[j], ch[j], rem[j]);
+    for (size_t i = nmin; i-- > 0;) {
+#pragma GCC unroll 8
+        for (int j = 0; j < G; ++j) enc_step<kRow>(t, sym, row, hw, beg[j] + i, x[j], ptr[j], ch[j], rem[j]);
+    }
+    for (int j = 0; j < G; ++j) {
+        uint8_t* pj = ptr[j];
+        *--pj = (uint8_t)x[j];
+        *--pj = (uint8_t)(x[j] >> 8);
+        *--pj = (uint8_t)(x[j] >> 16);
+        *--pj = (uint8_t)(x[j] >> 24);
+        ptr_out[j] = pj;
+    }
+    return LIC_OK;
+}
+
+// One decoder step (symbol idx) of one string.  Branch-free renormalisation (at most two bytes:
+// x >= 2^7 after the coding step) while two input bytes remain, checked bytes near the end.
+// Returns false on a corrupt stream (exhausted input).
+template <bool kRow>
+LIC_INLINE int dec_step(const DecCtx t, const uint8_t* row, size_t hw, size_t idx, uint32_t& x,
+                        const uint8_t*& p, const uint8_t* end, uint32_t& ch, size_t& rem, int8_t* sym_out) {
+    uint32_t r;
+    if (kRow) {
+        r = row[idx];
+    } else {
+        r = ch;
+        if (--rem == 0) { ++ch; rem = hw; }
+    }
+    const uint32_t* c = t.cdf + (size_t)r * t.row_len;     // r validated by the caller
+    uint32_t xv = x;
+    const uint32_t slot = xv & (kProbScale - 1);
+    uint32_t s = t.bucket[(size_t)r * 4096 + (slot >> 4)];
+    while (c[s + 1] <= slot) ++s;
+    const uint32_t start = c[s], freq = c[s + 1] - start;
+    xv = freq * (xv >> kProbBits) + slot - start;
+    const uint8_t* pj = p;
+    if (end - pj >= 2) {
+        const uint32_t d1 = xv < kRansLow;
+        xv = d1 ? (xv << 8) | pj[0] : xv;
+        pj += d1;
+        const uint32_t d2 = xv < kRansLow;
+        xv = d2 ? (xv << 8) | pj[0] : xv;
+        pj += d2;
+    } else {
+        while (xv < kRansLow) {
+            if (pj >= end) return LIC_ECORRUPT;
+            xv = (xv << 8) | *pj++;
+        }
+    }
+    x = xv;
+    p = pj;
+    sym_out[idx] = (int8_t)((int)s + t.smin);
+    return LIC_OK;
+}
+
+// Decoder: G strings in lockstep over the common prefix, then each string's tail alone.
+template <int G, bool kRow>
+lic_status dec_group(const lic_rans_tables* tab, const uint8_t* const* in, const size_t* len,
+                     const uint8_t* __restrict row, const SlabGeom& g, int k0, int8_t* __restrict sym_out) {
+    const DecCtx t{tab->cdf.data(), tab->bucket.data(), tab->row_len, tab->n_rows, tab->sym_min};
+    const size_t hw = g.hw ? g.hw : 1;
+    uint32_t x[G], ch[G];
+    const uint8_t* p[G];
+    const uint8_t* end[G];
+    size_t rem[G], beg[G];
+    size_t nmin = ~size_t(0);
+    for (int j = 0; j < G; ++j) {
+        if (len[j] < 4) return LIC_ECORRUPT;
+        const uint8_t* q = in[j];
+        x[j] = ((uint32_t)q[0] << 24) | ((uint32_t)q[1] << 16) | ((uint32_t)q[2] << 8) | q[3];
+        p[j] = q + 4;
+        end[j] = q + len[j];
+        ch[j] = g.ch0[k0 + j]; rem[j] = hw; beg[j] = g.begin[k0 + j];
+        nmin = std::min(nmin, g.count[k0 + j]);
+    }
+    for (size_t i = 0; i < nmin; ++i) {
+        int st = 0;
+#pragma GCC unroll 8
+        for (int j = 0; j < G; ++j) st |= dec_step<kRow>(t, row, hw, beg[j] + i, x[j], p[j], end[j], ch[j], rem[j], sym_out);
+        if (st) return LIC_ECORRUPT;
+    }
+    for (int j = 0; j < G; ++j)
+        for (size_t i = nmin; i < g.count[k0 + j]; ++i) {
+            const int st = dec_step<kRow>(t, row, hw, beg[j] + i, x[j], p[j], end[j], ch[j], rem[j], sym_out);
+            if (st) return (lic_status)st;
+        }
+    for (int j = 0; j < G; ++j)
+        if (x[j] != kRansLow || p[j] != end[j]) return LIC_ECORRUPT;
+    return LIC_OK;
+}
+
+// Range checks hoisted out of the coding loops (vectorisable): every row < n_rows and, for the
+// encoder, every symbol inside the table's support.
+bool validate_planes(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row, size_t n) {
+    uint32_t bad = 0;
+    if (row) {
+        const uint8_t nr = (uint8_t)std::min<uint32_t>(t->n_rows, 255);
+        const uint32_t big = t->n_rows > 255;
+        for (size_t i = 0; i < n; ++i) bad |= (uint32_t)(row[i] >= nr) & (big ^ 1u);
+    }
+    if (sym) {
+        const int smin = t->sym_min, ns = (int)t->nsym;
+        for (size_t i = 0; i < n; ++i) bad |= (uint32_t)((unsigned)((int)sym[i] - smin) >= (unsigned)ns);
+    }
+    return bad == 0;
+}
+
+inline void put_be32(uint8_t* q, uint32_t v) {
+    q[0] = (uint8_t)(v >> 24); q[1] = (uint8_t)(v >> 16); q[2] = (uint8_t)(v >> 8); q[3] = (uint8_t)v;
+}
+inline uint32_t get_be32(const uint8_t* q) {
+    return ((uint32_t)q[0] << 24) | ((uint32_t)q[1] << 16) | ((uint32_t)q[2] << 8) | q[3];
+}
+
+}  // namespace
+
+extern "C" lic_status lic_rans_encode_slabs(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row,
+                                            lic_shape plane, uint32_t K, uint8_t* out, size_t cap, size_t* out_len) {
+    if (!t || !out || !out_len) return LIC_EINVAL;
+    if (K <= 1) return lic_rans_encode_fast(t, sym, row, plane, out, cap, out_len);
+    SlabGeom g;
+    if (!slab_geom(plane, K, g)) return LIC_EINVAL;
+    if (g.hw * plane.c && !sym) return LIC_EINVAL;
+    if (!validate_planes(t, sym, row, g.hw * plane.c)) return LIC_EINVAL;
+    if (!row && plane.c > t->n_rows) return LIC_EINVAL;
+    // per-slab scratch regions: 2 bytes per symbol + 8 (renormalisation emits <= 16 bits per symbol)
+    thread_local std::vector<uint8_t> scratch;
+    size_t need = 0;
+    size_t off[64];
+    for (uint32_t k = 0; k < K; ++k) { off[k] = need; need += 2 * g.count[k] + 8; }
+    if (scratch.size() < need) scratch.resize(need);
+    uint8_t* hi[64]; uint8_t* start[64];
+    for (uint32_t k = 0; k < K; ++k) hi[k] = scratch.data() + off[k] + 2 * g.count[k] + 8;
+    for (uint32_t k0 = 0; k0 < K;) {
+        const uint32_t left = K - k0;
+        const int G = left >= 4 ? 4 : left >= 2 ? 2 : 1;
+        lic_status st;
+        if (row) {
+            st = G == 4 ? enc_group<4, true>(t, sym, row, g, (int)k0, hi + k0, start + k0)
+               : G == 2 ? enc_group<2, true>(t, sym, row, g, (int)k0, hi + k0, start + k0)
+                        : enc_group<1, true>(t, sym, row, g, (int)k0, hi + k0, start + k0);
+        } else {
+            st = G == 4 ? enc_group<4, false>(t, sym, row, g, (int)k0, hi + k0, start + k0)
+               : G == 2 ? enc_group<2, false>(t, sym, row, g, (int)k0, hi + k0, start + k0)
+                        : enc_group<1, false>(t, sym, row, g, (int)k0, hi + k0, start + k0);
+        }
+        if (st) return st;
+        k0 += (uint32_t)G;
+    }
+    size_t total = 4 * (size_t)K;
+    for (uint32_t k = 0; k < K; ++k) total += (size_t)(hi[k] - start[k]);
+    if (total > cap) return LIC_ENOSPACE;
+    uint8_t* w = out + 4 * (size_t)K;
+    for (uint32_t k = 0; k < K; ++k) {
+        const size_t n = (size_t)(hi[k] - start[k]);
+        put_be32(out + 4 * k, (uint32_t)n);
+        std::memcpy(w, start[k], n);
+        w += n;
+    }
+    *out_len = total;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_rans_decode_slabs(const lic_rans_tables* t, const uint8_t* in, size_t len, const uint8_t* row,
+                                            lic_shape plane, uint32_t K, int8_t* sym_out) {
+    if (!t) return LIC_EINVAL;
+    if (K <= 1) return lic_rans_decode_fast(t, in, len, row, plane, sym_out);
+    SlabGeom g;
+    if (!slab_geom(plane, K, g)) return LIC_EINVAL;
+    if (g.hw * plane.c && !sym_out) return LIC_EINVAL;
+    if (!validate_planes(t, nullptr, row, g.hw * plane.c)) return LIC_EINVAL;
+    if (!row && plane.c > t->n_rows) return LIC_EINVAL;
+    if (!in || len < 4 * (size_t)K) return LIC_ECORRUPT;
+    const uint8_t* sp[64];
+    size_t sl[64];
+    size_t pos = 4 * (size_t)K;
+    for (uint32_t k = 0; k < K; ++k) {
+        sl[k] = get_be32(in + 4 * k);
+        if (sl[k] > len - pos) return LIC_ECORRUPT;
+        sp[k] = in + pos;
+        pos += sl[k];
+    }
+    if (pos != len) return LIC_ECORRUPT;
+    for (uint32_t k0 = 0; k0 < K;) {
+        const uint32_t left = K - k0;
+        const int G = left >= 4 ? 4 : left >= 2 ? 2 : 1;
+        lic_status st;
+        if (row) {
+            st = G == 4 ? dec_group<4, true>(t, sp + k0, sl + k0, row, g, (int)k0, sym_out)
+               : G == 2 ? dec_group<2, true>(t, sp + k0, sl + k0, row, g, (int)k0, sym_out)
+                        : dec_group<1, true>(t, sp + k0, sl + k0, row, g, (int)k0, sym_out);
+        } else {
+            st = G == 4 ? dec_group<4, false>(t, sp + k0, sl + k0, row, g, (int)k0, sym_out)
+               : G == 2 ? dec_group<2, false>(t, sp + k0, sl + k0, row, g, (int)k0, sym_out)
+                        : dec_group<1, false>(t, sp + k0, sl + k0, row, g, (int)k0, sym_out);
+        }
+        if (st) return st;
+        k0 += (uint32_t)G;
+    }
+    return LIC_OK;
+}

@@ -73,6 +73,8 @@ struct ConvParams {
     float* out_f32;                   // f32 [batch][Cout][Hout or crop_H][Wout or crop_W]
     uint8_t* out_u8;                  // u8 [batch][crop_H][crop_W][3]
     int abs_out;                      // EP_YQUANT: also write |y| planes
+    int onedn;                        // EP_GDN / EP_IGDN as 1DN: the norm
+                                      // contracts |x| (not x^2) with gamma and y = x / n (x * n inverse)
     int pack4;                        // EP_FINAL of a stride-2 deconv with all 4 sub-pixel
                                       // phases packed into N: column j = phase (j>>2), channel (j&3)
     int crop_top, crop_left, crop_H, crop_W;

@@ -71,6 +71,7 @@ struct lic_pipeline {
     const uint32_t* cdf_y = nullptr; uint32_t rows_y = 0;
     const uint32_t* cdf_z = nullptr; uint32_t rows_z = 0;
     uint32_t row_len = 0;
+    uint32_t ksub = 1;                      // y substreams (channel slabs, lic_rans_encode_slabs)
     int sym_min = 0;
     lic_rans_tables* tab_y = nullptr;       // prepared coder tables (lic_rans_prepare)
     lic_rans_tables* tab_z = nullptr;
@@ -111,8 +112,8 @@ static void coder_task(lic_pipeline* p, const CpuTask& t) {
     uint64_t mism = 0;
     if (t.kind == C_ONE) {
         // encoder CPU workload: E(y) (and E(z)); then decoder CPU1: E^-1(z) (hyper) or E^-1(y)
-        st = lic_rans_encode_fast(p->tab_y, s.y_sym + f * p->ny, p->hyper ? s.y_idx + f * p->ny : nullptr, p->ys,
-                                  s.ystr[f].data(), s.ystr[f].size(), &s.ylen[f]);
+        st = lic_rans_encode_slabs(p->tab_y, s.y_sym + f * p->ny, p->hyper ? s.y_idx + f * p->ny : nullptr, p->ys,
+                                   p->ksub, s.ystr[f].data(), s.ystr[f].size(), &s.ylen[f]);
         if (!st && p->hyper)
             st = lic_rans_encode_fast(p->tab_z, s.z_sym + f * p->nz, nullptr, p->zs, s.zstr[f].data(),
                                       s.zstr[f].size(), &s.zlen[f]);
@@ -120,13 +121,14 @@ static void coder_task(lic_pipeline* p, const CpuTask& t) {
             st = lic_rans_decode_fast(p->tab_z, s.zstr[f].data(), s.zlen[f], nullptr, p->zs, s.z_dec + f * p->nz);
             if (!st && std::memcmp(s.z_dec + f * p->nz, s.z_sym + f * p->nz, p->nz) != 0) mism += 1;
         } else if (!st) {
-            st = lic_rans_decode_fast(p->tab_y, s.ystr[f].data(), s.ylen[f], nullptr, p->ys, s.y_dec + f * p->ny);
+            st = lic_rans_decode_slabs(p->tab_y, s.ystr[f].data(), s.ylen[f], nullptr, p->ys, p->ksub,
+                                       s.y_dec + f * p->ny);
             if (!st && std::memcmp(s.y_dec + f * p->ny, s.y_sym + f * p->ny, p->ny) != 0) mism += 1;
         }
     } else {
         // decoder CPU2: E^-1(y) with the indexes from decoder GPU1
-        st = lic_rans_decode_fast(p->tab_y, s.ystr[f].data(), s.ylen[f], s.idx_dec + f * p->ny, p->ys,
-                                  s.y_dec + f * p->ny);
+        st = lic_rans_decode_slabs(p->tab_y, s.ystr[f].data(), s.ylen[f], s.idx_dec + f * p->ny, p->ys, p->ksub,
+                                   s.y_dec + f * p->ny);
         if (!st && std::memcmp(s.y_dec + f * p->ny, s.y_sym + f * p->ny, p->ny) != 0) mism += 1;
     }
     std::lock_guard<std::mutex> g(p->mu);
@@ -191,6 +193,8 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
     if (p->cfg.serial) p->cfg.inflight = 1;
     lic_status st = lic_shapes(codec, &p->ys, &p->zs, &p->hyper);
     if (st) { delete p; return st; }
+    p->ksub = cfg->substreams ? cfg->substreams : 1;
+    if (p->ksub > 64 || p->ksub > p->ys.c) { delete p; return LIC_EINVAL; }
     p->ny = (size_t)p->ys.c * p->ys.h * p->ys.w;
     p->nz = (size_t)p->zs.c * p->zs.h * p->zs.w;
     uint32_t rl = 0;
@@ -254,7 +258,7 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
             lic_pipeline_close(p);
             return LIC_ENOMEM;
         }
-        s.ystr.assign(B, std::vector<uint8_t>(2 * p->ny + 64));
+        s.ystr.assign(B, std::vector<uint8_t>(2 * p->ny + 64 + 8 * p->ksub));
         s.zstr.assign(B, std::vector<uint8_t>(2 * p->nz + 64));
         s.ylen.assign(B, 0);
         s.zlen.assign(B, 0);

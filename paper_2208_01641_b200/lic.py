@@ -80,7 +80,8 @@ _L.lic_trace_read.argtypes = [_P, _P, _sz]
 
 class PipelineConfig(ctypes.Structure):
     _fields_ = [("coder_threads", ctypes.c_uint32), ("batch", ctypes.c_uint32), ("inflight", ctypes.c_uint32),
-                ("u8", ctypes.c_int), ("serial", ctypes.c_int), ("keep_bitstreams", ctypes.c_int)]
+                ("u8", ctypes.c_int), ("serial", ctypes.c_int), ("keep_bitstreams", ctypes.c_int),
+                ("substreams", ctypes.c_uint32)]
 
 
 class PipelineStats(ctypes.Structure):
@@ -106,6 +107,8 @@ _L.lic_rans_tables_free.argtypes = [_P]
 _L.lic_rans_tables_free.restype = None
 _L.lic_rans_encode_fast.argtypes = [_P, _P, _P, Shape, _P, _sz, ctypes.POINTER(_sz)]
 _L.lic_rans_decode_fast.argtypes = [_P, _P, _sz, _P, Shape, _P]
+_L.lic_rans_encode_slabs.argtypes = [_P, _P, _P, Shape, _u32, _P, _sz, ctypes.POINTER(_sz)]
+_L.lic_rans_decode_slabs.argtypes = [_P, _P, _sz, _P, Shape, _u32, _P]
 
 EXPORTED = [n for n in dir(_L) if n.startswith("lic_")]
 
@@ -206,24 +209,32 @@ class RansTables:
         if st:
             raise LicError(st, "lic_rans_prepare")
 
-    def encode(self, sym, rows=None):
+    def encode(self, sym, rows=None, substreams=1):
+        """lic_rans_encode_fast (substreams = 1) or lic_rans_encode_slabs (K channel slabs)."""
         sym = np.ascontiguousarray(sym, np.int8)
         shp = Shape(*sym.shape) if sym.ndim == 3 else Shape(1, 1, sym.size)
         rows = None if rows is None else np.ascontiguousarray(rows, np.uint8)
-        cap = 2 * sym.size + 64
+        cap = 2 * sym.size + 64 + 8 * substreams
         out = np.empty(cap, np.uint8)
         n = ctypes.c_size_t(0)
-        st = _L.lic_rans_encode_fast(self._h, _ptr(sym), _ptr(rows), shp, _ptr(out), cap, ctypes.byref(n))
+        if substreams == 1:
+            st = _L.lic_rans_encode_fast(self._h, _ptr(sym), _ptr(rows), shp, _ptr(out), cap, ctypes.byref(n))
+        else:
+            st = _L.lic_rans_encode_slabs(self._h, _ptr(sym), _ptr(rows), shp, substreams, _ptr(out), cap,
+                                          ctypes.byref(n))
         if st:
             raise LicError(st, "rans_encode_fast")
         return out[: n.value].tobytes()
 
-    def decode(self, data, shape, rows=None):
+    def decode(self, data, shape, rows=None, substreams=1):
         shp = Shape(*shape) if len(shape) == 3 else Shape(1, 1, int(np.prod(shape)))
         rows = None if rows is None else np.ascontiguousarray(rows, np.uint8)
         out = np.empty(shape, np.int8)
         buf = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)
-        st = _L.lic_rans_decode_fast(self._h, _ptr(buf), len(data), _ptr(rows), shp, _ptr(out))
+        if substreams == 1:
+            st = _L.lic_rans_decode_fast(self._h, _ptr(buf), len(data), _ptr(rows), shp, _ptr(out))
+        else:
+            st = _L.lic_rans_decode_slabs(self._h, _ptr(buf), len(data), _ptr(rows), shp, substreams, _ptr(out))
         if st == LIC_ECORRUPT:
             raise CorruptStream(st, "corrupt stream")
         if st:
@@ -378,9 +389,11 @@ class Pipeline:
     """lic_pipeline: GPU control thread (the caller) + native coder worker pool."""
 
     def __init__(self, codec: Codec, coder_threads: int, batch: int, inflight: int = 2, u8: bool = True,
-                 serial: bool = False, keep_bitstreams: bool = False):
+                 serial: bool = False, keep_bitstreams: bool = False, substreams: int = 1):
         self.codec = codec
-        self.cfg = PipelineConfig(coder_threads, batch, inflight, int(u8), int(serial), int(keep_bitstreams))
+        self.substreams = substreams
+        self.cfg = PipelineConfig(coder_threads, batch, inflight, int(u8), int(serial), int(keep_bitstreams),
+                                  substreams)
         self._h = _P()
         st = _L.lic_pipeline_open(codec.handle, ctypes.byref(self.cfg), ctypes.byref(self._h))
         if st:

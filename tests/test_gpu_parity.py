@@ -202,3 +202,55 @@ def test_factorized_c1(lic):
     if np.array_equal(ys[0], p["y_sym"]):
         assert lic.rans_encode(ys[0], c.cdf(0)) == O.code_planes(p, tabs, False)[0]
     c.close()
+
+
+# ---------------------------------------------------------------- 1DN (NEXT-1)
+@pytest.mark.parametrize("kind", [0, 1])
+def test_onedn_codec(lic, kind):
+    """The paper's implementation C: GDN/IGDN replaced by 1DN
+    (n = beta + gamma |x|, y = x / n; inverse x * n) in the same fused epilogue.  Every
+    normalised layer on the oracle's own input, then encode planes and decode from the
+    oracle's symbols.  kind 0 = the factorized-prior + 1DN codec of the paper's streaming
+    demo (PAPER.md:187)."""
+    from lic_synth.weights import ACT_1DN
+    spec = ModelSpec(kind=kind, N=128, M=192, activation=ACT_1DN)
+    w = generate_weights(spec, seed=0)
+    fr = synth_frames_u8(1, H, W, seed=13)
+    x = u8_to_f32_chw(fr)
+    hyp = kind == 1
+    xp, crop = O.pad_chw(x[0], hyper=hyp)
+    c = lic.Codec(write_licw(spec, w), H, W, max_batch=1)
+    # layer chain of the oracle
+    acts = {"x": xp}
+    h = xp
+    for i in (1, 2, 3):
+        h = O.onedn(O.conv2d(h, w[f"ga{i}.w"], w[f"ga{i}.b"], 2, 2), w[f"ga{i}.beta"], w[f"ga{i}.gamma"])
+        acts[f"ga{i}"] = h
+    y = O.conv2d(h, w["ga4.w"], w["ga4.b"], 2, 2)
+    sym, yhat, _ = O.quantize(y, None if hyp else w["mu_y"], 32)
+    g = yhat
+    for i in (1, 2, 3):
+        g = O.onedn(O.deconv2d(g, w[f"gs{i}.w"], w[f"gs{i}.b"], 2, 2, 1), w[f"gs{i}.beta"], w[f"gs{i}.gamma"],
+                    inverse=True)
+        acts[f"gs{i}"] = g
+    acts["yhat"] = yhat
+    for layer, src in (("ga1", "x"), ("ga2", "ga1"), ("ga3", "ga2"), ("gs1", "yhat"), ("gs2", "gs1"),
+                       ("gs3", "gs2")):
+        got = c.test_layer(layer, acts[src][None])
+        worst = check_float(got[0], acts[layer], what=f"1DN {layer}")
+        print(f"1DN {layer}: max-abs {worst:.2e}")
+    # full encode vs the oracle codec (act = 1)
+    p = O.encode_planes(xp, w, hyp, 32, act=1)
+    np.testing.assert_array_equal(p["y"], y)
+    ys = np.empty((1,) + c.y_shape, np.int8)
+    yi = np.empty((1,) + c.y_shape, np.uint8) if hyp else None
+    zs = np.empty((1,) + c.z_shape, np.int8) if hyp else None
+    c.set_debug(True)
+    c.encode(x, ys, yi, zs)
+    yd, _, _ = c.debug_latents(1)
+    check_float(yd[0], p["y"], what="1DN y")
+    check_symbols(ys[0], p["y_sym"], p["y"] - (0 if hyp else w["mu_y"][:, None, None]), what="1DN y_sym")
+    out = np.empty((1, 3, H, W), np.float32)
+    c.decode(p["y_sym"][None], out)
+    check_float(out[0], O.decode_frame(p["y_sym"], w, hyp, crop, H, W, act=1), what="1DN xhat")
+    c.close()

@@ -23,26 +23,28 @@ def lic():
     return L
 
 
-def run_pipeline(lic, codec, frames, serial, inflight=3, threads=3):
+def run_pipeline(lic, codec, frames, serial, inflight=3, threads=3, substreams=1):
     import torch
     fin = torch.from_numpy(frames).cuda()
     fout = torch.zeros_like(fin)
     p = lic.Pipeline(codec, coder_threads=threads, batch=B, inflight=inflight, u8=True, serial=serial,
-                     keep_bitstreams=True)
+                     keep_bitstreams=True, substreams=substreams)
     st = p.run(fin, fout, NF)
     streams = [p.bitstream(i) for i in range(NF)]
     p.close()
     return st, streams, fout.cpu().numpy()
 
 
-@pytest.mark.parametrize("kind", [1, 0])
-def test_pipeline_matches_serial_and_direct(lic, kind):
+@pytest.mark.parametrize("kind,K", [(1, 1), (0, 1), (1, 8), (0, 5)])
+def test_pipeline_matches_serial_and_direct(lic, kind, K):
+    """K > 1: the y string as K channel-slab substreams (R21), byte-identical to the
+    oracle's framing of the same planes."""
     spec = ModelSpec(kind=kind, N=128, M=192)
     w = generate_weights(spec, seed=0)
     codec = lic.Codec(write_licw(spec, w), H, W, max_batch=B)
     frames = synth_frames_u8(NF, H, W, seed=21)
-    st, streams, out = run_pipeline(lic, codec, frames, serial=False)
-    st_s, streams_s, out_s = run_pipeline(lic, codec, frames, serial=True)
+    st, streams, out = run_pipeline(lic, codec, frames, serial=False, substreams=K)
+    st_s, streams_s, out_s = run_pipeline(lic, codec, frames, serial=True, substreams=K)
     assert st["frames"] == NF and st["symbol_mismatches"] == 0 and st_s["symbol_mismatches"] == 0
     assert streams == streams_s                               # SPEC.md acceptance #3
     assert np.array_equal(out, out_s)
@@ -60,6 +62,13 @@ def test_pipeline_matches_serial_and_direct(lic, kind):
         assert np.array_equal(dec, out[b0:b0 + B])
         for f in range(B):
             yb, zb = streams[b0 + f]
+            if K > 1:
+                assert yb == O.rans_encode_slabs(ys[f], yi[f] if hyper else None, tabs_y, K)
+                assert np.array_equal(O.rans_decode_slabs(yb, ys[f].shape, yi[f] if hyper else None, tabs_y, K),
+                                      ys[f])
+                if hyper:
+                    assert zb == O.rans_encode(zs[f], O.channel_rows(zs[f].shape), tabs_z)
+                continue
             if hyper:
                 assert yb == lic.rans_encode(ys[f].ravel(), tabs_y, rows=yi[f].ravel())
                 assert zb == lic.rans_encode(zs[f], tabs_z)

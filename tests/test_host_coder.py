@@ -126,3 +126,53 @@ def test_fast_coder_general_tables(lic):
     sym = RNG.integers(0, 2, 5000).astype(np.int8)
     b = t.encode(sym, rows=np.zeros(5000, np.uint8))
     assert b == O.rans_encode(sym, np.zeros(5000), c, sym_min=0)
+
+
+# ---------------------------------------------------------------- channel-slab substreams (R21)
+@pytest.mark.parametrize("C,H,W,K", [(192, 48, 80, 4), (192, 12, 20, 8), (128, 3, 5, 3), (10, 7, 9, 4),
+                                     (5, 4, 4, 5), (192, 2, 3, 1), (64, 1, 1, 64)])
+def test_slab_substreams_channel_rows_bit_exact(lic, C, H, W, K):
+    """Product lic_rans_encode_slabs == oracle rans_encode_slabs byte for byte (ragged slabs
+    when K does not divide C), lossless through both decoders."""
+    L = 32
+    cdf = O.cdf_table(RNG.uniform(0.5, 1.5, C), L)
+    sym = np.clip(np.round(RNG.standard_normal((C, H, W)) * 1.3), -L, L).astype(np.int8)
+    t = lic.RansTables(cdf)
+    b = t.encode(sym, substreams=K)
+    assert b == O.rans_encode_slabs(sym, None, cdf, K)
+    assert np.array_equal(t.decode(b, sym.shape, substreams=K), sym)
+    assert np.array_equal(O.rans_decode_slabs(b, sym.shape, None, cdf, K), sym)
+
+
+@pytest.mark.parametrize("K", [1, 2, 4, 6, 8])
+def test_slab_substreams_indexed_rows_bit_exact(lic, K):
+    L = 32
+    cdf = O.cdf_table(scale_table(), L)
+    C, H, W = 192, 24, 40
+    idx = RNG.integers(0, 64, (C, H, W)).astype(np.uint8)
+    sym = np.clip(np.round(RNG.standard_normal((C, H, W)) * scale_table()[idx] * 0.5), -L, L).astype(np.int8)
+    sym[0, 0, :] = 32                     # freq-1 edge symbols in the first and last slab
+    sym[-1, -1, :] = -32
+    t = lic.RansTables(cdf)
+    b = t.encode(sym, rows=idx, substreams=K)
+    assert b == O.rans_encode_slabs(sym, idx, cdf, K)
+    assert np.array_equal(t.decode(b, sym.shape, rows=idx, substreams=K), sym)
+
+
+def test_slab_substreams_corrupt(lic):
+    L = 32
+    C = 16
+    cdf = O.cdf_table(RNG.uniform(0.5, 1.5, C), L)
+    sym = np.clip(np.round(RNG.standard_normal((C, 8, 8)) * 2), -L, L).astype(np.int8)
+    t = lic.RansTables(cdf)
+    b = t.encode(sym, substreams=4)
+    for bad in (b[:-1], b + b"\x00", b[:10]):
+        with pytest.raises(lic.CorruptStream):
+            t.decode(bad, sym.shape, substreams=4)
+    # a length field pointing past the end
+    bb = bytearray(b)
+    bb[0:4] = (len(b)).to_bytes(4, "big")
+    with pytest.raises(lic.CorruptStream):
+        t.decode(bytes(bb), sym.shape, substreams=4)
+    with pytest.raises(lic.LicError):
+        t.encode(sym, substreams=C + 1)   # more slabs than channels

@@ -83,6 +83,35 @@ def test_transforms_vs_torch_float64(hyper_case):
     np.testing.assert_allclose(xs, torch_gs(yhat, w).numpy(), atol=2e-5, rtol=0)
 
 
+def _onedn64(x, beta, gamma, inverse):
+    n = _t(beta)[:, None, None] + torch.einsum("ij,jhw->ihw", _t(gamma), x.abs())
+    return x * n if inverse else x / n
+
+
+def test_onedn_transforms_vs_torch_float64(hyper_case):
+    """1DN variant (the paper's implementation C): oracle g_a / g_s with
+    act = 1 against a torch float64 composition of conv / conv_transpose and the 1DN
+    formula (SPEC.md:76)."""
+    w, x, _ = hyper_case
+    h = _t(x)
+    for i in (1, 2, 3):
+        h = F.conv2d(h[None], _t(w[f"ga{i}.w"]), _t(w[f"ga{i}.b"]), stride=2, padding=2)[0]
+        h = _onedn64(h, w[f"ga{i}.beta"], w[f"ga{i}.gamma"], False)
+    y_ref = F.conv2d(h[None], _t(w["ga4.w"]), _t(w["ga4.b"]), stride=2, padding=2)[0].numpy()
+    y = O.g_a(x, w, act=1)
+    np.testing.assert_allclose(y, y_ref, atol=2e-5, rtol=0)
+    assert np.abs(y - O.g_a(x, w)).max() > 1e-2                     # really a different activation
+    yh = np.round(y).astype(np.float32)
+    g = _t(yh)
+    for i in (1, 2, 3):
+        g = F.conv_transpose2d(g[None], _t(w[f"gs{i}.w"]).transpose(0, 1), _t(w[f"gs{i}.b"]),
+                               stride=2, padding=2, output_padding=1)[0]
+        g = _onedn64(g, w[f"gs{i}.beta"], w[f"gs{i}.gamma"], True)
+    xr = F.conv_transpose2d(g[None], _t(w["gs4.w"]).transpose(0, 1), _t(w["gs4.b"]),
+                            stride=2, padding=2, output_padding=1)[0].numpy()
+    np.testing.assert_allclose(O.g_s(yh, w, act=1), xr, atol=2e-5, rtol=1e-5)
+
+
 def test_latents_are_not_degenerate(hyper_case):
     """SURVEY.md finding 2 / c15: the init must exercise the coder (non-zero
     symbols, several CDF indexes), else parity passes vacuously."""

@@ -335,3 +335,58 @@ def test_rans_corrupt_streams():
         O.rans_decode(b + b"\x00", rows, cdf)
     with pytest.raises(O.CorruptStream):
         O.rans_decode(b"", rows, cdf)
+
+
+def test_rans_slabs_framing_pins():
+    """DESIGN.md R21 (SURVEY.md §8(f) NEXT-2 (i)): K = 1 is the plain string (known answer);
+    K > 1 = big-endian u32 lengths + independent strings of channel slabs
+    [floor(kC/K), floor((k+1)C/K)).  Pinned without the slab code: each substring equals the
+    plain coder run on that slab alone with its own rows (so a dropped row offset or a wrong
+    slab boundary fails), and the framing sizes add up."""
+    rng = np.random.default_rng(11)
+    L = 32
+    C, H, W = 7, 3, 5
+    sig = rng.uniform(0.5, 2.0, C)
+    cdf = O.cdf_table(sig, L)
+    sym = np.clip(np.round(rng.standard_normal((C, H, W)) * 2), -L, L).astype(np.int8)
+    assert O.rans_encode_slabs(sym, None, cdf, 1) == O.rans_encode(sym, O.channel_rows(sym.shape), cdf)
+    b = O.rans_encode_slabs(sym, None, cdf, 3)
+    lens = [int.from_bytes(b[4 * k:4 * k + 4], "big") for k in range(3)]
+    assert 12 + sum(lens) == len(b)
+    bounds = [(0, 2), (2, 4), (4, 7)]            # floor(k*7/3): 0, 2, 4, 7
+    pos = 12
+    for (c0, c1_), n in zip(bounds, lens):
+        # the slab coded alone with a table holding only its own channels' rows
+        sub_cdf = O.cdf_table(sig[c0:c1_], L)
+        plain = O.rans_encode(sym[c0:c1_], O.channel_rows(sym[c0:c1_].shape), sub_cdf)
+        assert b[pos:pos + n] == plain
+        pos += n
+    assert np.array_equal(O.rans_decode_slabs(b, sym.shape, None, cdf, 3), sym)
+    with pytest.raises(O.CorruptStream):
+        O.rans_decode_slabs(b[:-1], sym.shape, None, cdf, 3)
+
+
+def test_onedn_gamma_zero_roundtrip_and_fixed_point():
+    """1DN (SPEC.md:76, PAPER.md:131-137): gamma = 0 -> inverse(forward(x)) = x; in general
+    x = y * (beta + gamma |x|) for y = 1DN(x), and the fixed-point iteration
+    x_{t+1} = y * (beta + gamma |x_t|) recovers x (a transposed gamma, x^2 in place of |x|
+    or a dropped beta breaks one of these)."""
+    C = 12
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((C, 4, 4)).astype(np.float32)
+    beta = (1 + rng.random(C)).astype(np.float32)
+    g0 = np.zeros((C, C), np.float32)
+    np.testing.assert_allclose(O.onedn(O.onedn(x, beta, g0), beta, g0, inverse=True), x, rtol=3e-7)
+    beta, gamma = _gdn_params(C, rng)
+    gamma = gamma + 0.02 * rng.random((C, C)).astype(np.float32)
+    y = O.onedn(x, beta, gamma).astype(np.float64)
+    X, Y = x.reshape(C, -1).astype(np.float64), y.reshape(C, -1)
+    g, b = gamma.astype(np.float64), beta.astype(np.float64)[:, None]
+    np.testing.assert_allclose(Y * (b + g @ np.abs(X)), X, rtol=1e-6, atol=1e-6)
+    xt = Y.copy()
+    for _ in range(300):
+        xt = Y * (b + g @ np.abs(xt))
+    np.testing.assert_allclose(xt, X, rtol=1e-5, atol=1e-5)
+    # the inverse is the multiply form on the same norm
+    inv = O.onedn(x, beta, gamma, inverse=True).astype(np.float64).reshape(C, -1)
+    np.testing.assert_allclose(inv, X * (b + g @ np.abs(X)), rtol=1e-6)
