@@ -154,6 +154,9 @@ lic_status lic_debug_latents(lic_codec* codec, uint32_t batch, float* y, float* 
  * the stream it is launched on; lic_profile_read synchronises and returns the summed
  * device time and launch count per layer since profiling was enabled (then resets). */
 lic_status lic_profile(lic_codec* codec, int on);
+/* The same for a subset of layers: bit i of `mask` = layer id i (0: off).  Events between
+ * kernels serialise them, so a timed run brackets only the layers it reports. */
+lic_status lic_profile_layers(lic_codec* codec, uint32_t mask);
 lic_status lic_profile_read(lic_codec* codec, int layer_id, double* ms, uint64_t* launches);
 /* Test-only timeline: while on, launches of `layer_id` record clock64 events of CTA 0 per
  * tile (8 per tile: MMA start/end, norm issue, epilogue start / x^2 written / norm ready /

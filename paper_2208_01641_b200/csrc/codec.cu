@@ -166,6 +166,7 @@ struct lic_codec {
     int tma_out_enabled = 1;       // LIC_TMA_OUT=0 disables the TMA-store epilogue
     int cg_enabled = 1;            // LIC_CG=1 forces one CTA per tile (no cta_group::2 pairs)
     int gs4_bn = 32;               // packed g_s L4 N tile (env LIC_GS4_BN=16|32)
+    int pdl_enabled = 1;           // programmatic dependent launch of the GEMM engine (env LIC_PDL=0 disables)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
@@ -178,6 +179,7 @@ struct lic_codec {
     // measurement
     uint64_t launches = 0;
     int profiling = 0;
+    uint32_t prof_mask = 0;        // layers whose launches are bracketed by events
     int trace_layer = -1;
     unsigned long long* d_trace = nullptr;   // 256 tiles x 8 events
     std::vector<cudaEvent_t> ev;            // [2 * kProfSlots]
@@ -270,10 +272,10 @@ static bool encode_out_conv_map(CUtensorMap* m, const __half* base, int C, int W
     if (!enc) return false;
     cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
     cuuint64_t str[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-    cuuint32_t box[4] = {16, (cuuint32_t)bw, (cuuint32_t)bh, 1};
+    cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, 1};      // 64-channel blocks, 128-byte rows
     cuuint32_t es[4] = {1, 1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, (void*)base, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // sub-pixel phase view of a stride-2 transposed conv output (NHWC, H = 2 Hin, W = 2 Win):
@@ -283,10 +285,10 @@ static bool encode_out_phase_map(CUtensorMap* m, const __half* base, int C, int 
     if (!enc) return false;
     cuuint64_t dims[5] = {(cuuint64_t)C, 2, (cuuint64_t)(W / 2), 2, (cuuint64_t)B * (H / 2)};
     cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)2 * C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)2 * W * C * 2};
-    cuuint32_t box[5] = {16, 1, (cuuint32_t)bw, 1, (cuuint32_t)bh};
+    cuuint32_t box[5] = {64, 1, (cuuint32_t)bw, 1, (cuuint32_t)bh};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, (void*)base, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -385,9 +387,11 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
     const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64) * 4;
     const uint32_t budget = 227u * 1024u;
-    // TMA-store epilogue: 16 warps x 2 KB staging, when the layer writes an activation and the
+    // TMA-store epilogue: 4 lane quadrants x 8 KB block slots (1 or 2 slots), when the layer writes an activation and the
     // pipeline keeps >= 3 stages with it (env LIC_TMA_OUT=0 disables)
-    const bool has_act = Ly.out_buf != nullptr && Ly.ep != EP_SIGMA && Ly.ep != EP_FINAL;
+    // (64-channel store blocks: N tiles that are not a multiple of 64 -- g_a L4 at M = 320, two
+    // N tiles of 160 -- store directly)
+    const bool has_act = Ly.out_buf != nullptr && Ly.ep != EP_SIGMA && Ly.ep != EP_FINAL && P.BN % 64 == 0;
     bool tma_out = has_act && c->tma_out_enabled;
     const uint32_t ostage_bytes = 16 * 2048;
     {
@@ -547,12 +551,14 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
     P.total_tiles = batch * P.nphase * P.tiles_y * txs * P.n_ntiles;
     const int grid = P.cg * std::min(P.total_tiles, c->num_sms / P.cg);
     const int lid = (int)(&Ly - c->layers);
+    P.pdl = c->pdl_enabled;
     if (c->trace_layer == lid && c->d_trace) {
         P.trace = c->d_trace;
         if (const char* e = std::getenv("LIC_DBG_NOSTORE")) P.dbg_nostore = atoi(e);
         CK(cudaMemsetAsync(c->d_trace, 0, 256 * 16 * 8, st));
     }
-    if (c->profiling) {
+    const bool prof = c->profiling && ((c->prof_mask >> lid) & 1u);
+    if (prof) {
         if (c->ev_used == kProfSlots) prof_flush(c);
         CK(cudaEventRecord(c->ev[2 * c->ev_used], st));
     }
@@ -563,7 +569,7 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
                         lid, grid, P.cg, P.smem_bytes, P.total_tiles, P.stages, P.halo, cudaGetErrorString(e));
     }
     ++c->launches;
-    if (c->profiling) {
+    if (prof) {
         CK(cudaEventRecord(c->ev[2 * c->ev_used + 1], st));
         c->ev_layer[c->ev_used++] = lid;
     }
@@ -686,6 +692,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_TMA_OUT")) c->tma_out_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_CG")) c->cg_enabled = (e[0] != '1');
     if (const char* e = std::getenv("LIC_GS4_BN")) c->gs4_bn = (atoi(e) == 16) ? 16 : 32;
+    if (const char* e = std::getenv("LIC_PDL")) c->pdl_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_NO_WRES")) c->wres_enabled = (e[0] != '1');
     c->max_batch = (int)max_batch;
     c->H = (int)height; c->W = (int)width;
@@ -1140,8 +1147,12 @@ extern "C" lic_status lic_test_sigma_to_index(lic_codec* c, const float* sigma, 
 }
 
 // ------------------------------------------------------------------ measurement
-extern "C" lic_status lic_profile(lic_codec* c, int on) {
+extern "C" lic_status lic_profile(lic_codec* c, int on) { return lic_profile_layers(c, on ? ~0u : 0u); }
+
+extern "C" lic_status lic_profile_layers(lic_codec* c, uint32_t mask) {
     if (!c) return LIC_EINVAL;
+    const int on = mask != 0;
+    c->prof_mask = mask;
     cudaSetDevice(c->device);
     if (on && c->ev.empty()) {
         c->ev.resize(2 * kProfSlots);

@@ -165,10 +165,18 @@ constexpr int kTraceEv = 16;
 constexpr int kTraceTiles = 256;
 enum TraceEv { T_MMA_START = 0, T_MMA_END = 1, T_NORM_ISSUE = 2, T_EPI_START = 3, T_EPI_XSQ = 4,
                T_EPI_NORM = 5, T_EPI_END = 6, T_PROD_START = 7,
-               T_B_PATCH = 8, T_B_C0_READY = 9, T_B_C0_DONE = 10, T_B_C1_READY = 11, T_B_C1_DONE = 12 };
+               T_B_PATCH = 8, T_B_C0_READY = 9, T_B_C0_DONE = 10, T_B_C1_READY = 11, T_B_C1_DONE = 12,
+               T_MMA_K0 = 13, T_MMA_KL = 14, T_PEER_B_DONE = 15 };
 #define LIC_TRACE(it, ev)                                                                         \
     do {                                                                                          \
         if (p.trace && blockIdx.x == 0 && (it) < kTraceTiles)                                     \
+            p.trace[(size_t)(it) * kTraceEv + (ev)] = (unsigned long long)clock64();              \
+    } while (0)
+// the same event recorded by CTA 1 (the pair's peer) -- clock64 is per SM, so only compare
+// durations, not absolute times, with CTA 0's events
+#define LIC_TRACE_PEER(it, ev)                                                                    \
+    do {                                                                                          \
+        if (p.trace && blockIdx.x == 1 && (it) < kTraceTiles)                                     \
             p.trace[(size_t)(it) * kTraceEv + (ev)] = (unsigned long long)clock64();              \
     } while (0)
 
@@ -267,6 +275,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (p.pdl) griddep_launch();          // the next layer may start its prologue on SMs we free
 
     const uint32_t a_bytes = kBM * kBK * 2;          // 16 KB per activation plane
     const int bnc = p.BN / CG;                        // B (and gamma) rows held by this CTA
@@ -323,6 +332,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             }
             cp_async_commit();
         };
+        if (p.pdl) griddep_wait();
         if (fast && cid < p.total_tiles) raw_issue(cid, 0);
         int stage = 0;
         uint32_t phase = 0;
@@ -435,6 +445,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     if constexpr (CG == 2) mbar_arrive_cluster(lbar(&full_bar[stage]));
                     else mbar_arrive(&full_bar[stage]);
                     if (bw == 0) LIC_TRACE(it, c ? T_B_C1_DONE : T_B_C0_DONE);
+                    if (bw == 0 && c) LIC_TRACE_PEER(it, T_PEER_B_DONE);
                 }
                 if (++stage == p.stages) { stage = 0; phase ^= 1; }
             }
@@ -468,6 +479,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             }
             __syncwarp();
         }
+        if (p.pdl) griddep_wait();                // activations below come from the previous kernel
         int stage = 0;
         uint32_t phase = 0;
         int pit = 0;
@@ -513,6 +525,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         // ====================== halo producer (halo mode) ======================
         if (p.fuse_l1) build_l1(2);
         if (p.halo) {
+            if (p.pdl) griddep_wait();
             int hs = 0;
             uint32_t hphase = 0;
             const uint32_t hbytes = (uint32_t)p.halo_w * (p.Ht + 2) * 128 * p.split;
@@ -647,6 +660,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 for (int k = 0; k < nk; ++k) {
                     wait_poll(&full_bar[stage], phase);
                     tc_fence_after();
+                    if (lane == 0 && k == 0) LIC_TRACE(it, T_MMA_K0);
+                    if (lane == 0 && k == nk - 1) LIC_TRACE(it, T_MMA_KL);
                     const uint32_t st = smem_u32(smem + stage * p.stage_bytes);
                     const uint64_t ah = sdesc_sw128(st);
                     const uint64_t al = sdesc_sw128(st + a_bytes);
@@ -680,6 +695,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         if (kGdn && pend && leader) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(); }
     } else if (warp >= 4) {
         // ====================== epilogue ======================
+        if (p.pdl) griddep_wait();                  // global writes only after the previous kernel
         const int q = warp & 3;                     // TMEM lane quadrant
         const int g = (warp - 4) >> 2;              // channel group (quarter)
         const int r = q * 32 + lane;                // tile row (pixel) of this thread
@@ -713,61 +729,73 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const int bw = p.Wt < 32 ? p.Wt : 32, bh = 32 / bw;
             const int ty0 = (q * 32) >> p.wt_log2, tx0 = (q * 32) & (p.Wt - 1);
             const bool tma_ok = p.tma_out && (p.nphase == 1 || tc.gy0 + ty0 + bh <= p.Hg);
-            uint8_t* ostage_base = smem + p.off_ostage + (warp - 4) * 2048 * p.ostage_slots;
-            // 16 channels [cb, cb+16) of this thread's pixel -> fp16 hi/lo NHWC activation.
-            // TMA path: chunks are staged per warp (32 px x 16 ch, hi + lo: 2 KB) into the
-            // warp's ostage_slots slots and flushed together -- one proxy fence and one bulk
-            // group per batch; the first chunk of a batch waits until the previous batch's
-            // stores have read their staging.
-            int npend = 0, pcb0 = 0, pcb1 = 0;
-            auto flush = [&]() {
-                if (npend == 0) return;                       // warp-uniform
+            // TMA-store staging, per TMEM lane quadrant: the quadrant's 4 warps (channel groups)
+            // fill 64-channel blocks of their 32 pixels -- [plane hi | lo][32 px][128 B], 128B-
+            // swizzled (16-byte piece c of row r at ((c ^ (r & 7)) << 4): conflict-free 16-byte
+            // stores) -- in p.ostage_slots 8 KB slots; one elected thread per quadrant then stores
+            // each block with one bulk tensor store per plane (128-byte rows: 4x fewer TMA
+            // requests than 16-channel boxes).
+            const int qslots = p.ostage_slots;
+            const uint32_t qstage = smem_u32(smem + p.off_ostage) + (uint32_t)(q * qslots * 8192);
+            const bool qissuer = (g == 0) && (lane == 0);
+            auto stage16 = [&](const float* v16, int cb, int slot) {
+                uint4 h0, h1, l0, l1;
+                split2(v16[0], v16[1], h0.x, l0.x);   split2(v16[2], v16[3], h0.y, l0.y);
+                split2(v16[4], v16[5], h0.z, l0.z);   split2(v16[6], v16[7], h0.w, l0.w);
+                split2(v16[8], v16[9], h1.x, l1.x);   split2(v16[10], v16[11], h1.y, l1.y);
+                split2(v16[12], v16[13], h1.z, l1.z); split2(v16[14], v16[15], h1.w, l1.w);
+                if (p.dbg_nostore & 16) return;                                   // experiment: no staging writes
+                const uint32_t base = qstage + (uint32_t)slot * 8192u + (uint32_t)lane * 128u;
+                const uint32_t c0 = (uint32_t)((cb & 63) >> 3);                 // 16-byte piece of channel cb
+                const uint32_t o0 = ((c0 ^ (uint32_t)(lane & 7)) << 4), o1 = (((c0 + 1) ^ (uint32_t)(lane & 7)) << 4);
+                stsu4(base + o0, h0);
+                stsu4(base + o1, h1);
+                stsu4(base + 4096u + o0, l0);
+                stsu4(base + 4096u + o1, l1);
+            };
+            // every thread of the quadrant: slots free (the issuer waited for their previous stores
+            // to finish reading smem; `keep` groups may stay in flight)
+            auto q_acquire = [&](int keep) {
+                if (qissuer) { if (keep) bulk_wait_read1(); else bulk_wait_read0(); }
+                named_bar_sync(5 + q, 128);
+            };
+            // blocks [blk0, blk0 + nblk) are in slots 0.. : make them visible and store them
+            auto q_flush = [&](int blk0, int nblk, int slot0) {
                 fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    for (int k = 0; k < npend; ++k) {
-                        uint8_t* os = ostage_base + k * 2048;
-                        const int cb = k ? pcb1 : pcb0;
+                named_bar_sync(5 + q, 128);
+                if (qissuer && !(p.dbg_nostore & 8)) {                               // 8: experiment, no TMA
+                    for (int k = 0; k < nblk; ++k) {
+                        const uint8_t* os = smem + p.off_ostage + (size_t)(q * qslots + slot0 + k) * 8192u;
+                        const int cb = co0 + 64 * (blk0 + k);
                         if (p.nphase == 1) {
                             tma_store_4d(&mapOH, os, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b);
-                            if (p.split == 2) tma_store_4d(&mapOL, os + 1024, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b);
+                            if (p.split == 2) tma_store_4d(&mapOL, os + 4096, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b);
                         } else {
                             const int qyb = tc.b * p.Hg + tc.gy0 + ty0;
                             tma_store_5d(&mapOH, os, cb, px, tc.gx0 + tx0, py, qyb);
-                            if (p.split == 2) tma_store_5d(&mapOL, os + 1024, cb, px, tc.gx0 + tx0, py, qyb);
+                            if (p.split == 2) tma_store_5d(&mapOL, os + 4096, cb, px, tc.gx0 + tx0, py, qyb);
                         }
                     }
                     bulk_commit();
                 }
-                __syncwarp();
-                npend = 0;
             };
-            auto emit16 = [&](const float* v16, int cb) {
+            auto direct16 = [&](const float* v16, int cb) {
                 __half* out = reinterpret_cast<__half*>(p.out_act);
-                if (tma_ok) {
-                    if (npend == 0) {
-                        if (lane == 0) bulk_wait_read0();
-                        __syncwarp();
-                    }
-                    uint8_t* ostage = ostage_base + npend * 2048;
-                    uint4 h0, h1, l0, l1;
-                    split2(v16[0], v16[1], h0.x, l0.x);   split2(v16[2], v16[3], h0.y, l0.y);
-                    split2(v16[4], v16[5], h0.z, l0.z);   split2(v16[6], v16[7], h0.w, l0.w);
-                    split2(v16[8], v16[9], h1.x, l1.x);   split2(v16[10], v16[11], h1.y, l1.y);
-                    split2(v16[12], v16[13], h1.z, l1.z); split2(v16[14], v16[15], h1.w, l1.w);
-                    reinterpret_cast<uint4*>(ostage)[2 * lane] = h0;
-                    reinterpret_cast<uint4*>(ostage)[2 * lane + 1] = h1;
-                    reinterpret_cast<uint4*>(ostage + 1024)[2 * lane] = l0;
-                    reinterpret_cast<uint4*>(ostage + 1024)[2 * lane + 1] = l1;
-                    if (npend == 0) pcb0 = cb; else pcb1 = cb;
-                    if (++npend == p.ostage_slots) flush();
-                } else if (valid) {
-                    split_store8(out + pix * p.Cout + cb, p.split == 2 ? out + p.act_plane + pix * p.Cout + cb : nullptr, v16);
-                    split_store8(out + pix * p.Cout + cb + 8, p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + 8 : nullptr,
-                                 v16 + 8);
-                }
+                if (!valid) return;
+                split_store8(out + pix * p.Cout + cb, p.split == 2 ? out + p.act_plane + pix * p.Cout + cb : nullptr, v16);
+                split_store8(out + pix * p.Cout + cb + 8, p.split == 2 ? out + p.act_plane + pix * p.Cout + cb + 8 : nullptr,
+                             v16 + 8);
             };
-
+            // generic epilogues: round k of the channel loop holds block k (warp g: channels
+            // 64k + 16g ..) -- one block per round through alternating slots
+            auto emit16 = [&](const float* v16, int cb) {
+                if (!tma_ok) { direct16(v16, cb); return; }
+                const int blk = (cb - co0) >> 6, slot = blk % qslots;
+                q_acquire(qslots - 1);
+                stage16(v16, cb - co0, slot);
+                q_flush(blk, 1, slot);
+            };
+            bool released = false;
             if constexpr (kGdn) {
                 constexpr int G = 16 * GC;                   // channels of this group
                 float x[GC][16];
@@ -857,7 +885,31 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                         for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(cb + i) * HWo] = x[j][i];
                     }
-                    if (out && !(p.dbg_nostore & 1)) emit16(x[j], cb);
+                }
+                // the accumulator is in registers: release TMEM before storing
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2) mbar_arrive_cluster(lbar(&tempty_bar[buf]));
+                    else mbar_arrive(&tempty_bar[buf]);
+                }
+                released = true;
+                if (out && !(p.dbg_nostore & 1)) {
+                    if (tma_ok) {
+                        const int nblk = p.BN >> 6;
+                        for (int b0 = 0; b0 < nblk; b0 += qslots) {
+                            q_acquire(0);
+#pragma unroll
+                            for (int j = 0; j < GC; ++j) {
+                                const int cb = g * G + j * 16, blk = cb >> 6;
+                                if (blk >= b0 && blk < b0 + qslots) stage16(x[j], cb, blk - b0);
+                            }
+                            q_flush(b0, min(qslots, nblk - b0), 0);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < GC; ++j) direct16(x[j], g * G + j * 16);
+                    }
                 }
             } else if (p.pack4) {
                 // packed g_s L4: channel group g takes sub-pixel phase g (columns 4g .. 4g+2), so
@@ -984,16 +1036,17 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     }
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if constexpr (CG == 2) mbar_arrive_cluster(lbar(&tempty_bar[buf]));
-                else mbar_arrive(&tempty_bar[buf]);
+            if (!released) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2) mbar_arrive_cluster(lbar(&tempty_bar[buf]));
+                    else mbar_arrive(&tempty_bar[buf]);
+                }
             }
-            flush();                                     // after releasing the accumulator
             if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_END);
         }
-        if (p.tma_out && lane == 0) bulk_wait0();
+        if (p.tma_out && lane == 0 && g == 0) bulk_wait0();
         if (p.sat_count) {
             for (int o = 16; o > 0; o >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, o);
             if (lane == 0 && sat) atomicAdd(p.sat_count, (unsigned long long)sat);
@@ -1021,24 +1074,28 @@ static cudaError_t launch_t(const CUtensorMap& mapA, const CUtensorMap& mapB, co
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    if constexpr (CG == 1) {
-        conv_umma_kernel<GC, 1><<<grid, kThreads, p.smem_bytes, stream>>>(mapA, mapB, mapG, mapOH, mapOL, p);
-        return cudaGetLastError();
-    } else {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)grid);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = p.smem_bytes;
-        cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, conv_umma_kernel<GC, 2>, mapA, mapB, mapG, mapOH, mapOL, p);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if constexpr (CG == 2) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 2;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
     }
+    if (p.pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, conv_umma_kernel<GC, CG>, mapA, mapB, mapG, mapOH, mapOL, p);
 }
 
 cudaError_t launch_conv_umma(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,

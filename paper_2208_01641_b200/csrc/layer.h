@@ -81,6 +81,9 @@ struct ConvParams {
     unsigned long long* sat_count;    // saturation counter (nullable)
     unsigned long long* trace;        // test-only: per-tile clock64 events of CTA 0 (nullable)
     int dbg_nostore;                  // test-only experiment switch: skip activation stores
+    int pdl;                          // launched with programmatic stream serialization: constants and
+                                      // the prologue overlap the previous kernel; griddepcontrol.wait
+                                      // before any global read of its outputs or any global write
     // fused g_a L1 (im2col GEMM, K = 75 padded to 128): warps 0, 2 and 3 build the A tiles
     // (hi, lo) in shared memory straight from the frame -- u8 HWC (x = u8 / 255) or f32 CHW --
     // through a per-tile input patch; no ingest kernel and no im2col tensor in HBM.  Tile fixed

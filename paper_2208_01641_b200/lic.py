@@ -70,6 +70,7 @@ _L.lic_rans_encode.argtypes = [_P, _P, Shape, _P, _u32, _u32, _i, _P, _sz, ctype
 _L.lic_rans_decode.argtypes = [_P, _sz, _P, Shape, _P, _u32, _u32, _i, _P]
 _L.lic_version.restype = ctypes.c_char_p
 _L.lic_profile.argtypes = [_P, _i]
+_L.lic_profile_layers.argtypes = [_P, _u32]
 _L.lic_profile_read.argtypes = [_P, _i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
 _L.lic_launch_count.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64)]
 _L.lic_set_zero_copy.argtypes = [_P, _i]
@@ -326,8 +327,15 @@ class Codec:
         self._chk(_L.lic_set_zero_copy(self._h, int(on)), "lic_set_zero_copy")
 
     # -- measurement
-    def profile(self, on=True):
-        self._chk(_L.lic_profile(self._h, int(on)), "lic_profile")
+    def profile(self, on=True, layers=None):
+        """Bracket GEMM-engine launches with CUDA events: all layers, or only `layers` (names)."""
+        if layers is None:
+            self._chk(_L.lic_profile(self._h, int(on)), "lic_profile")
+        else:
+            mask = 0
+            for n in layers:
+                mask |= 1 << LAYERS.index(n)
+            self._chk(_L.lic_profile_layers(self._h, mask if on else 0), "lic_profile_layers")
 
     def profile_read(self):
         """{layer: (ms, launches)} accumulated since profile(True); resets."""
