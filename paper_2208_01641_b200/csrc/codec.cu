@@ -167,6 +167,7 @@ struct lic_codec {
     int cg_enabled = 1;            // LIC_CG=1 forces one CTA per tile (no cta_group::2 pairs)
     int gs4_bn = 32;               // packed g_s L4 N tile (env LIC_GS4_BN=16|32)
     int pdl_enabled = 1;           // programmatic dependent launch of the GEMM engine (env LIC_PDL=0 disables)
+    int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
@@ -305,6 +306,7 @@ static void choose_tile(int Hg, int Wg, int* Wt, int* Ht) {
 // mbarrier area: full/empty[<= 8] + tfull/tempty[2] + norm + gamma + hfull/hempty[4] + xsq +
 // wres (34 x 8 B) + the TMEM base slot
 static constexpr uint32_t kBarBytes = 512;
+static constexpr int kGatherN = 144;     // g_s L4 gather mode: 9 input offsets x 16 packed outputs
 static_assert(kBarBytes >= (2 * 8 + 2 * 2 + 2 + 2 * 4 + 2) * 8 + 4, "barrier area too small");
 
 // q = (umulhi(n, m) + n) >> s == n / d for 0 <= n < 2^31 (round-up magic, d >= 1)
@@ -333,7 +335,10 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.Cin = Ly.Cin_eff;
     P.kchunks = Ly.Cin_eff / 64;
     P.Cout = Ly.Cout;
-    if (Ly.ep == EP_FINAL && Ly.deconv) { P.BN = c->gs4_bn; P.n_ntiles = 1; }
+    const bool gs4g = Ly.ep == EP_FINAL && Ly.deconv && c->gs4_gather;
+    P.tsx = 0; P.tsy = 0;
+    if (gs4g) { P.BN = kGatherN; P.n_ntiles = 1; }
+    else if (Ly.ep == EP_FINAL && Ly.deconv) { P.BN = c->gs4_bn; P.n_ntiles = 1; }
     else if (Ly.Cout <= 256) { P.BN = (Ly.Cout + 15) / 16 * 16; P.n_ntiles = 1; }
     else { P.n_ntiles = (Ly.Cout + 255) / 256; P.BN = ((Ly.Cout + P.n_ntiles - 1) / P.n_ntiles + 15) / 16 * 16; }
     const bool gdn = (Ly.ep == EP_GDN || Ly.ep == EP_IGDN);
@@ -353,6 +358,12 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
                 P.tap_dy[ntap] = ky - Ly.p; P.tap_dx[ntap] = kx - Ly.p; P.tap_w[ntap] = ky * Ly.k + kx; ++ntap;
             }
         P.ntaps[0] = ntap;
+    } else if (gs4g) {
+        // g_s L4 gather mode: one "tap" -- the 16 x 8 input tile itself, starting one pixel
+        // up-left of the 14 x 6 output interior; B rows t*16 + phase*4 + co (9 offsets t)
+        P.Hg = Ly.Hin; P.Wg = Ly.Win; P.stride = 1; P.out_s = 2; P.nphase = 1; P.gather = 1;
+        P.tap0[0] = 0; P.ntaps[0] = 1; P.tap_dy[0] = -1; P.tap_dx[0] = -1; P.tap_w[0] = 0;
+        ntap = 1;
     } else if (Ly.ep == EP_FINAL) {
         // g_s L4 (Cout = 3): all 4 sub-pixel phases packed into one N = 16 GEMM over the 9
         // input offsets (dy, dx) in {-1,0,1}^2 shared by the phases; B row (phase*4 + co)
@@ -381,7 +392,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     }
     // CTA pair (cta_group::2, M = 256) unless disabled (env LIC_CG=1); B / gamma split by rows
     // (N tiles >= 64 only: the packed N = 16 g_s L4 stays on one CTA per tile)
-    P.cg = (c->cg_enabled && P.BN % 16 == 0 && P.BN >= 32) ? 2 : 1;
+    P.cg = (c->cg_enabled && P.BN % 16 == 0 && P.BN >= 32 && !gs4g) ? 2 : 1;
     // shared memory plan: stage ring | halo ring (halo mode) | gamma (GDN) | mbarriers | constants
     const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)(P.BN / P.cg) * 64 * 2;
     const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
@@ -423,6 +434,18 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.off_halo = 0;
         P.off_raw = (P.off_lut + 257 * 4 + 15) / 16 * 16;
         P.off_gamma = (P.off_raw + 2 * 19 * 112 + 1023) / 1024 * 1024;
+    } else if (gs4g) {
+        P.halo = 0;
+        P.halo_slots = 0;
+        P.Wt = 16; P.Ht = 8;
+        P.tsx = 14; P.tsy = 6;
+        P.stage_bytes = a_bytes * P.split;
+        P.stages = 3;
+        P.wres = 1;
+        P.off_wres = P.stages * P.stage_bytes;
+        P.off_gp = P.off_wres + P.kchunks * b_bytes;
+        P.off_halo = 0;
+        P.off_gamma = (P.off_gp + 9u * 128u * 48u + 1023) / 1024 * 1024;
     } else if (stride1 && fixed + 2 * P.split * hpb + 2 * b_bytes <= budget && c->halo_enabled) {
         P.halo = 1;
         P.Wt = 8; P.Ht = 16;
@@ -461,8 +484,9 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.off_halo = 0;
         P.off_gamma = stages * P.stage_bytes;
     }
-    P.tiles_x = (P.Wg + P.Wt - 1) / P.Wt;
-    P.tiles_y = (P.Hg + P.Ht - 1) / P.Ht;
+    if (!P.tsx) { P.tsx = P.Wt; P.tsy = P.Ht; }
+    P.tiles_x = (P.Wg + P.tsx - 1) / P.tsx;
+    P.tiles_y = (P.Hg + P.tsy - 1) / P.tsy;
     P.txs = (P.tiles_x + P.cg - 1) / P.cg;
     fast_div(P.n_ntiles, &P.fd_nt_m, &P.fd_nt_s);
     fast_div(P.txs, &P.fd_txs_m, &P.fd_txs_s);
@@ -504,7 +528,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.tmem_cols = pow2_cols(P.n_accbuf * per);
     P.L = c->L;
     // tensor maps
-    const int ntaps_w = gemm_l1 ? 1 : (P.pack4 ? 9 : Ly.k * Ly.k);
+    const int ntaps_w = (gemm_l1 || P.gather) ? 1 : (P.pack4 ? 9 : Ly.k * Ly.k);
     const int cout_pad = P.BN * P.n_ntiles;
     if (!P.fuse_l1 && !encode_act_map(&Ly.mapA, Ly.in_buf, P.Cin, Ly.deconv ? Ly.Win : (gemm_l1 ? Ly.Wout : Ly.Win),
                         Ly.deconv ? Ly.Hin : (gemm_l1 ? Ly.Hout : Ly.Hin), c->max_batch, P.split, Ly.in_plane,
@@ -693,6 +717,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_CG")) c->cg_enabled = (e[0] != '1');
     if (const char* e = std::getenv("LIC_GS4_BN")) c->gs4_bn = (atoi(e) == 16) ? 16 : 32;
     if (const char* e = std::getenv("LIC_PDL")) c->pdl_enabled = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_GS4_GATHER")) c->gs4_gather = (e[0] != '0');
     if (const char* e = std::getenv("LIC_NO_WRES")) c->wres_enabled = (e[0] != '1');
     c->max_batch = (int)max_batch;
     c->H = (int)height; c->W = (int)width;
@@ -775,10 +800,26 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
         const std::vector<float>& w = blk[wn + ".w"];
         int bn = d.cout <= 256 ? (d.cout + 15) / 16 * 16 : 0;
         if (!bn) { int nt = (d.cout + 255) / 256; bn = ((d.cout + nt - 1) / nt + 15) / 16 * 16 * nt; }
-        const bool pack4 = d.id == GS4;
-        const int cout_pad = pack4 ? c->gs4_bn : bn;
-        const int taps = d.id == GA1 ? 1 : (pack4 ? 9 : d.k * d.k);
+        const bool gather = d.id == GS4 && c->gs4_gather;
+        const bool pack4 = d.id == GS4 && !gather;
+        const int cout_pad = gather ? kGatherN : pack4 ? c->gs4_bn : bn;
+        const int taps = (d.id == GA1 || gather) ? 1 : (pack4 ? 9 : d.k * d.k);
         std::vector<__half> wp((size_t)taps * cout_pad * Ly.Cin_eff, __float2half(0.0f));
+        if (gather) {
+            // row t*16 + phase*4 + co, t = (dy+1)*3 + (dx+1): the tap of sub-pixel phase (py, px)
+            // that reads input offset (dy, dx) (ky = py + 2 - 2dy, kx = px + 2 - 2dx)
+            for (int t = 0; t < 9; ++t) {
+                const int dy = t / 3 - 1, dx = t % 3 - 1;
+                for (int ph = 0; ph < 4; ++ph) {
+                    const int ky = (ph >> 1) + 2 - 2 * dy, kx = (ph & 1) + 2 - 2 * dx;
+                    if (ky < 0 || ky > 4 || kx < 0 || kx > 4) continue;
+                    for (int co = 0; co < 3; ++co)
+                        for (int ci = 0; ci < d.cin; ++ci)
+                            wp[((size_t)t * 16 + ph * 4 + co) * Ly.Cin_eff + ci] =
+                                __float2half_rn(w[(((size_t)co * d.cin + ci) * 5 + ky) * 5 + kx]);
+                }
+            }
+        }
         if (pack4) {
             for (int t = 0; t < 9; ++t) {
                 const int dy = t / 3 - 1, dx = t % 3 - 1;
@@ -792,7 +833,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
                 }
             }
         }
-        for (int co = 0; co < d.cout && !pack4; ++co)
+        for (int co = 0; co < d.cout && !pack4 && !gather; ++co)
             for (int ci = 0; ci < d.cin; ++ci)
                 for (int ky = 0; ky < d.k; ++ky)
                     for (int kx = 0; kx < d.k; ++kx) {

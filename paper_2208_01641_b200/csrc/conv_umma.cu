@@ -59,8 +59,8 @@ __device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t, int
     q = fdiv(t, p.fd_ty_m, p.fd_ty_s);
     const int ty = t - q * p.tiles_y;
     c.b = q;
-    c.gx0 = tx * p.Wt;
-    c.gy0 = ty * p.Ht;
+    c.gx0 = tx * p.tsx;
+    c.gy0 = ty * p.tsy;
     return c;
 }
 
@@ -483,7 +483,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         int stage = 0;
         uint32_t phase = 0;
         int pit = 0;
-        for (int t = cid; t < p.total_tiles && !p.wres; t += ncl, ++pit) {
+        // (resident weights: only the gather mode still streams A tiles from here)
+        for (int t = cid; t < p.total_tiles && (!p.wres || p.gather); t += ncl, ++pit) {
             TileCoord tc = decode_tile(p, t, rank);
             const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
             if (lane == 0) LIC_TRACE(pit, T_PROD_START);
@@ -510,10 +511,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* st = smem + stage * p.stage_bytes;
                     if (elect_one()) {
-                        expect(&full_bar[stage], a_bytes * p.split + b_bytes);
+                        expect(&full_bar[stage], a_bytes * p.split + (p.wres ? 0u : b_bytes));
                         ld5(st, &mapA, &full_bar[stage], c * kBK, x0, y0, tc.b, 0);
                         if (p.split == 2) ld5(st + a_bytes, &mapA, &full_bar[stage], c * kBK, x0, y0, tc.b, 1);
-                        ld3(st + a_bytes * p.split, &mapB, &full_bar[stage], c * kBK, tc.nt * p.BN + rank * bnc, wt);
+                        if (!p.wres)
+                            ld3(st + a_bytes * p.split, &mapB, &full_bar[stage], c * kBK, tc.nt * p.BN + rank * bnc, wt);
                     }
                     __syncwarp();
                     if (++stage == p.stages) { stage = 0; phase ^= 1; }
@@ -911,6 +913,60 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         for (int j = 0; j < GC; ++j) direct16(x[j], g * G + j * 16);
                     }
                 }
+            } else if (p.gather) {
+                // ---- gather mode (g_s L4): P[p][t][0..11] -> smem, then each output sums its 9
+                // neighbours' slices.  Column chunk t (16 wide) of the accumulator = offset t.
+                const uint32_t gp = smem_u32(smem + p.off_gp);
+                for (int t9 = g; t9 < 9; t9 += kEpiGroups) {
+                    float v[16];
+                    __syncwarp();
+                    tmem_ld16(taddr + t9 * 16, v);
+                    const uint32_t row = gp + (uint32_t)((t9 * 128 + r) * 48);
+                    // compact the 12 real columns (phase*4 + co, co < 3) to phase*3 + co
+                    stsu4(row, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
+                                          __float_as_uint(v[4])));
+                    stsu4(row + 16, make_uint4(__float_as_uint(v[5]), __float_as_uint(v[6]), __float_as_uint(v[8]),
+                                               __float_as_uint(v[9])));
+                    stsu4(row + 32, make_uint4(__float_as_uint(v[10]), __float_as_uint(v[12]), __float_as_uint(v[13]),
+                                               __float_as_uint(v[14])));
+                }
+                // accumulator consumed: release it, then gather once every warp has staged P
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2) mbar_arrive_cluster(lbar(&tempty_bar[buf]));
+                    else mbar_arrive(&tempty_bar[buf]);
+                }
+                released = true;
+                named_bar_sync(3, 32 * kEpiWarps);
+                // work item: output row (oy, py) = w / 28, column x = 2 ox + px = w % 28
+                for (int w = threadIdx.x - 128; w < 6 * 2 * 28; w += 32 * kEpiWarps) {
+                    const int rowi = w / 28, xi = w - rowi * 28;
+                    const int oy = rowi >> 1, pyy = rowi & 1, ox = xi >> 1, pxx = xi & 1;
+                    const int ggy = tc.gy0 + oy, ggx = tc.gx0 + ox;
+                    if (ox >= p.tsx || ggy >= p.Hg || ggx >= p.Wg) continue;
+                    const int j0 = (pyy * 2 + pxx) * 3;
+                    float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll
+                    for (int t9 = 0; t9 < 9; ++t9) {
+                        const int dy = t9 / 3 - 1, dx = t9 % 3 - 1;
+                        const int ar = (oy + 1 + dy) * 16 + (ox + 1 + dx);        // A-tile pixel
+                        const uint32_t a = gp + (uint32_t)((t9 * 128 + ar) * 48 + j0 * 4);
+                        a0 += ldsf(a); a1 += ldsf(a + 4); a2 += ldsf(a + 8);
+                    }
+                    const int ry = 2 * ggy + pyy - p.crop_top, rx = 2 * ggx + pxx - p.crop_left;
+                    if (ry < 0 || ry >= p.crop_H || rx < 0 || rx >= p.crop_W) continue;
+                    const float c3[3] = {a0, a1, a2};
+                    const size_t o = ((size_t)tc.b * p.crop_H + ry) * p.crop_W + rx;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const float xv = fminf(fmaxf(c3[ch] + s_bias[ch], 0.0f), 1.0f);
+                        if (p.out_f32) p.out_f32[((size_t)tc.b * 3 + ch) * p.crop_H * p.crop_W + (size_t)ry * p.crop_W + rx] = xv;
+                        if (p.out_u8) p.out_u8[o * 3 + ch] = (uint8_t)roundf(xv * 255.0f);
+                    }
+                }
+                // P is reused by the next tile: everyone done reading
+                named_bar_sync(3, 32 * kEpiWarps);
             } else if (p.pack4) {
                 // packed g_s L4: channel group g takes sub-pixel phase g (columns 4g .. 4g+2), so
                 // all 16 epilogue warps share the 12 outputs of each grid pixel

@@ -100,6 +100,13 @@ struct ConvParams {
     // (C, px, W/2, py, B*H/2) of the NHWC output, one map per plane
     int tma_out, ostage_slots;        // staging buffers per warp (1 or 2, 2 KB each)
     uint32_t off_ostage;
+    // gather mode (g_s L4, stride-2 transposed conv N -> 3): the 9 input offsets go into N instead
+    // of K -- P[p][t][j] = A[p] . W_t[j] over a 16 x 8 input tile (one A read per pixel, N = 9 x 16),
+    // then out[g][j] = sum_t P[g + off_t][t][j] gathered through shared memory for the 14 x 6
+    // interior; tiles step by (tsx, tsy) = (14, 6) and start one pixel up-left (TMA zero fill)
+    int gather;
+    int tsx, tsy;                     // tile step (= Wt, Ht except in gather mode)
+    uint32_t off_gp;                  // P staging: [9][128 px][12] f32
 };
 
 }  // namespace lic
