@@ -625,6 +625,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 for (int c = 0; c < p.kchunks; ++c) {
                     wait_poll(&hfull_bar[hs], hphase);
                     tc_fence_after();
+                    if (lane == 0 && c == 0) LIC_TRACE(it, T_MMA_K0);
                     const uint32_t hb = smem_u32(smem + p.off_halo + hs * (2 * p.halo_plane_bytes));
                     for (int ti = 0; ti < nt; ++ti) {
                         uint32_t bsm;
@@ -686,6 +687,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (elect_one()) commit(&tfull_bar[buf]);
             __syncwarp();
             if (lane == 0) LIC_TRACE(it, T_MMA_END);
+
             if (kGdn) {
                 // the previous tile's norm must be issued before this one becomes pending
                 if (pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(); }

@@ -50,3 +50,4 @@ for i in range(min(n, 40)):
 per_tile = (t[n - 1, 6] - t[0, 0]) / max(n, 1)
 print(f"mean cycles per tile (first MMA start -> last epilogue end): {per_tile:.0f}")
 print(f"mean MMA-busy per tile: {np.mean(t[:n,1]-t[:n,0]):.0f}, mean epilogue per tile: {np.mean(t[:n,6]-t[:n,3]):.0f}")
+
