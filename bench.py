@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--serial", action="store_true", help="serial reference pipeline (no overlap)")
     ap.add_argument("--zero-copy", action="store_true", help="kernels touch pinned host planes in place")
+    ap.add_argument("--precision", default="split", choices=["split", "f16"],
+                    help="split: fp16 hi + lo activations (graded); f16: one fp16 plane (NEXT-4, ungraded)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "timing rules: >= 3 warm-up steps"
 
@@ -199,7 +201,8 @@ def main():
     B = args.batch
     spec = ModelSpec(kind=1, N=N_CH, M=M_CH)
     blob = write_licw(spec, generate_weights(spec, seed=0))
-    codec = lic.Codec(blob, H, W, max_batch=B, device=local)
+    codec = lic.Codec(blob, H, W, max_batch=B, device=local,
+                      precision=lic.PREC_F16 if args.precision == "f16" else lic.PREC_SPLIT)
     codec.set_zero_copy(args.zero_copy)
     pipe = lic.Pipeline(codec, coder_threads=threads, batch=B, inflight=args.inflight, u8=True,
                         serial=args.serial, substreams=args.substreams)
@@ -304,7 +307,7 @@ def main():
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f16x2(split hi/lo)->f32",
+        "dtype": "f16x2(split hi/lo)->f32" if args.precision == "split" else "f16->f32 (single plane, ungraded)",
         "data": "synthetic",
         "config": {"workload": WORKLOAD, "batch_per_gpu": B, "frames_per_gpu": nfr,
                    "coder_threads_per_gpu": threads, "inflight": args.inflight,
@@ -321,7 +324,8 @@ def main():
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_source": f"{pk_src} bf16_tflops_sustained (fp16 dense rate = bf16)",
                      "algorithmic_flops_per_launch": flops[dom] * B, "avg_launch_ms": round(per_launch_ms, 4),
-                     "note": "split-FP16 issues 2 MMAs per algorithmic FLOP: ceiling frac 0.5"},
+                     "note": ("split-FP16 issues 2 MMAs per algorithmic FLOP: ceiling frac 0.5"
+                              if args.precision == "split" else "single fp16 plane: 1 MMA per algorithmic FLOP")},
         "kernel_time_share": kernel_share,
         "kernel_time_share_note": f"untimed pass of {nprof} frames with every layer bracketed by events",
         "gpu_launches": int(launches),

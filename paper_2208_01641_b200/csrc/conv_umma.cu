@@ -535,7 +535,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 TileCoord tc = decode_tile(p, t, rank);
                 for (int c = 0; c < p.kchunks; ++c) {
                     mbar_wait(&hempty_bar[hs], hphase ^ 1);
-                    uint8_t* hb = smem + p.off_halo + hs * (2 * p.halo_plane_bytes);
+                    uint8_t* hb = smem + p.off_halo + hs * (p.split * p.halo_plane_bytes);
                     if (elect_one()) {
                         expect(&hfull_bar[hs], hbytes);
                         ld5(hb, &mapA, &hfull_bar[hs], c * kBK, tc.gx0 - 1, tc.gy0 - 1, tc.b, 0);
@@ -626,7 +626,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     wait_poll(&hfull_bar[hs], hphase);
                     tc_fence_after();
                     if (lane == 0 && c == 0) LIC_TRACE(it, T_MMA_K0);
-                    const uint32_t hb = smem_u32(smem + p.off_halo + hs * (2 * p.halo_plane_bytes));
+                    const uint32_t hb = smem_u32(smem + p.off_halo + hs * (p.split * p.halo_plane_bytes));
                     for (int ti = 0; ti < nt; ++ti) {
                         uint32_t bsm;
                         if (p.wres) {
