@@ -167,6 +167,7 @@ struct lic_codec {
     int cg_enabled = 1;            // LIC_CG=1 forces one CTA per tile (no cta_group::2 pairs)
     int gs4_bn = 32;               // packed g_s L4 N tile (env LIC_GS4_BN=16|32)
     int pdl_enabled = 1;           // programmatic dependent launch of the GEMM engine (env LIC_PDL=0 disables)
+    int small_bn = 0;              // N tile of the h_a / h_s layers (env LIC_SMALL_BN=64|128; 0 = whole Cout: measured no gain)
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
@@ -341,6 +342,18 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     else if (Ly.ep == EP_FINAL && Ly.deconv) { P.BN = c->gs4_bn; P.n_ntiles = 1; }
     else if (Ly.Cout <= 256) { P.BN = (Ly.Cout + 15) / 16 * 16; P.n_ntiles = 1; }
     else { P.n_ntiles = (Ly.Cout + 255) / 256; P.BN = ((Ly.Cout + P.n_ntiles - 1) / P.n_ntiles + 15) / 16 * 16; }
+    // h_a / h_s run on a few dozen pixel tiles (one per CTA pair, a serial load -> MMA ->
+    // epilogue chain each): split their output channels into 64-wide N tiles so more CTAs work
+    // and each CTA pipelines several tiles (env LIC_SMALL_BN=0 keeps one N tile)
+    {
+        const int lid = (int)(&Ly - c->layers);
+        const bool hyper_layer = lid >= HA1 && lid <= HS3;
+        if (hyper_layer && c->small_bn && Ly.Cout % c->small_bn == 0 && Ly.Cout > c->small_bn &&
+            Ly.ep != EP_GDN && Ly.ep != EP_IGDN) {
+            P.BN = c->small_bn;
+            P.n_ntiles = Ly.Cout / c->small_bn;
+        }
+    }
     const bool gdn = (Ly.ep == EP_GDN || Ly.ep == EP_IGDN);
     if (gdn && (P.n_ntiles != 1 || P.BN != Ly.Cout || Ly.Cout % 64))
         return fail(c, LIC_EINVAL, "GDN layer needs Cout %% 64 == 0 and Cout <= 256");
@@ -718,6 +731,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_GS4_BN")) c->gs4_bn = (atoi(e) == 16) ? 16 : 32;
     if (const char* e = std::getenv("LIC_PDL")) c->pdl_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_GS4_GATHER")) c->gs4_gather = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_SMALL_BN")) c->small_bn = atoi(e) == 64 || atoi(e) == 128 ? atoi(e) : 0;
     if (const char* e = std::getenv("LIC_NO_WRES")) c->wres_enabled = (e[0] != '1');
     c->max_batch = (int)max_batch;
     c->H = (int)height; c->W = (int)width;

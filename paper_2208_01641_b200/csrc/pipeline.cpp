@@ -24,6 +24,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -384,10 +385,11 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
     }
     const double t_run0 = now_s();
     // GPU control loop.  GPU tasks are issued asynchronously on p->stream (at most
-    // kMaxPending in flight) so the device never idles while ready work exists; the
+    // kMaxPending in flight, env LIC_MAX_PENDING) so the device never idles while ready work exists; the
     // oldest issued task is retired by waiting on its event, which then releases its
     // coder tasks (ENC, IDX) or its slot (DEC).
-    constexpr size_t kMaxPending = 3;
+    size_t kMaxPending = 5;
+    if (const char* e = std::getenv("LIC_MAX_PENDING")) kMaxPending = (size_t)std::max(1, std::min(16, atoi(e)));
     size_t ev_next = 0;
     for (;;) {
         GpuTask t{};
