@@ -36,16 +36,44 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-H, W = 720, 1280
-N_CH, M_CH = 128, 192
-WORKLOAD = "scale-hyperprior N=128 M=192, 1280x720 synthetic stream (padded 1280x768), random-init weights"
+# BASELINE.json configs (configs[2] = C3 is the default, headline workload; the others are
+# reported by DESIGN.md from `--config` runs on one GPU)
+CONFIGS = {
+    "c2": dict(kind=0, N=128, M=192, H=512, W=768, B=1,
+               workload="factorized-prior N=128 M=192, Kodak-shaped 768x512 frames, batch 1, random-init weights"),
+    "c3": dict(kind=1, N=128, M=192, H=720, W=1280, B=4,
+               workload="scale-hyperprior N=128 M=192, 1280x720 synthetic stream (padded 1280x768), random-init weights"),
+    "c4": dict(kind=1, N=192, M=320, H=720, W=1280, B=4,
+               workload="scale-hyperprior N=192 M=320, 1280x720 synthetic stream (padded 1280x768), random-init weights"),
+    "c5": dict(kind=1, N=192, M=320, H=1080, W=1920, B=2,
+               workload="scale-hyperprior N=192 M=320, 1920x1080 synthetic stream (padded 1920x1088), random-init weights"),
+}
+CFG = CONFIGS["c3"]
+H, W = CFG["H"], CFG["W"]
+N_CH, M_CH = CFG["N"], CFG["M"]
+WORKLOAD = CFG["workload"]
+
+
+def padded(h, w, hyper):
+    P = 64 if hyper else 16
+    return -(-h // P) * P, -(-w // P) * P
+
+
+def set_config(name):
+    global CFG, H, W, N_CH, M_CH, WORKLOAD
+    CFG = CONFIGS[name]
+    H, W, N_CH, M_CH, WORKLOAD = CFG["H"], CFG["W"], CFG["N"], CFG["M"], CFG["workload"]
 
 
 # ----------------------------------------------------------------- algorithmic work
-def layer_flops(N=N_CH, M=M_CH, Hp=768, Wp=1280):
+def layer_flops(N=None, M=None, Hp=None, Wp=None):
     """Algorithmic FLOPs (2 x MAC) per frame of every GEMM-engine layer, including the
     GDN/IGDN gamma contraction (C^2 MACs per pixel).  conv: Ho*Wo*Cout*Cin*k^2; deconv:
     Hi*Wi*Cin*Cout*k^2."""
+    N = N or N_CH
+    M = M or M_CH
+    if Hp is None:
+        Hp, Wp = padded(H, W, CFG["kind"] == 1)
     H2, W2 = Hp // 2, Wp // 2
     f = {}
     def conv(name, ho, wo, cin, cout, k, gdn=False):
@@ -139,25 +167,27 @@ def oracle_sample(seconds_budget=15.0, strip_rows=64, seed=0):
     1/12 of the padded 1280x768 frame.  Returns (frames/s, cores, description)."""
     from lic_synth import ModelSpec, generate_weights, synth_frame_u8
     from oracle import oracle as O
-    spec = ModelSpec(kind=1, N=N_CH, M=M_CH)
+    hyper = CFG["kind"] == 1
+    spec = ModelSpec(kind=CFG["kind"], N=N_CH, M=M_CH)
     w = generate_weights(spec, seed=0)
-    t = O.build_tables(w, True, 32)
+    t = O.build_tables(w, hyper, 32)
     fr = synth_frame_u8(strip_rows, W, seed=seed)
     t0 = time.perf_counter()
     n = 0
     while True:
-        x, crop = O.ingest_u8(fr, hyper=True)
-        p = O.encode_planes(x, w, True, 32)
-        yb, zb = O.code_planes(p, t, True)
-        O.decode_strings(yb, zb, w, t, True, p["y_sym"].shape, p["z_sym"].shape, crop, strip_rows, W)
+        x, crop = O.ingest_u8(fr, hyper=hyper)
+        p = O.encode_planes(x, w, hyper, 32)
+        yb, zb = O.code_planes(p, t, hyper)
+        O.decode_strings(yb, zb, w, t, hyper, p["y_sym"].shape, p["z_sym"].shape if hyper else None, crop,
+                         strip_rows, W)
         n += 1
         if time.perf_counter() - t0 >= seconds_budget or n >= 40:
             break
     dt = time.perf_counter() - t0
-    frac = strip_rows / 768.0
+    frac = strip_rows / float(padded(H, W, hyper)[0])
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return n * frac / dt, cores, (f"{n} x oracle encode+decode of a 1280x{strip_rows} strip "
-                                  f"(= {frac:.4f} of a padded 720p frame each), {dt:.1f} s")
+    return n * frac / dt, cores, (f"{n} x oracle encode+decode of a {W}x{strip_rows} strip "
+                                  f"(= {frac:.4f} of a padded {W}x{H} frame each), {dt:.1f} s")
 
 
 # ----------------------------------------------------------------- main
@@ -167,7 +197,9 @@ def main():
     ap.add_argument("--steps", type=int, default=250)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=4, help="frames per step (per GPU)")
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS),
+                    help="BASELINE.json config (c3: the headline 720p hyperprior stream)")
+    ap.add_argument("--batch", type=int, default=0, help="frames per step (per GPU); 0: the config's")
     ap.add_argument("--coder-threads", type=int, default=0, help="0: derived from the host cores")
     ap.add_argument("--inflight", type=int, default=8)
     ap.add_argument("--substreams", type=int, default=8,
@@ -179,6 +211,9 @@ def main():
                     help="split: fp16 hi + lo activations (graded); f16: one fp16 plane (NEXT-4, ungraded)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "timing rules: >= 3 warm-up steps"
+    set_config(args.config)
+    if not args.batch:
+        args.batch = CFG["B"]
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -199,7 +234,7 @@ def main():
     threads = args.coder_threads or max(2, min(96, ncores // max(1, world) - 2))
 
     B = args.batch
-    spec = ModelSpec(kind=1, N=N_CH, M=M_CH)
+    spec = ModelSpec(kind=CFG["kind"], N=N_CH, M=M_CH)
     blob = write_licw(spec, generate_weights(spec, seed=0))
     codec = lic.Codec(blob, H, W, max_batch=B, device=local,
                       precision=lic.PREC_F16 if args.precision == "f16" else lic.PREC_SPLIT)
@@ -289,15 +324,15 @@ def main():
         pass
     kernel_share = {k: round(v[0] / ms_prof, 4) for k, v in sorted(prof_all.items(), key=lambda kv: -kv[1][0])}
 
-    ny = M_CH * 48 * 80
-    nz = N_CH * 12 * 20
+    ny = int(np.prod(codec.y_shape))
+    nz = int(np.prod(codec.z_shape)) if codec.hyper else 0
     # PCIe bytes per step in the e2e run: frames in/out (DMA) + symbol planes through pinned
     # slots: encode writes y_sym, y_idx, z_sym; GPU1 reads z_dec, writes idx_dec; GPU2 reads y_dec
     h2d = B * (frame_bytes + nz + ny)
     d2h = B * (frame_bytes + 2 * ny + nz + ny)
 
     line = {
-        "metric": "1280x720 encode+decode frames/s",
+        "metric": f"{W}x{H} encode+decode frames/s",
         "value": round(value, 2),
         "unit": "frames/s",
         "n_gpus": world,
@@ -364,17 +399,18 @@ def run_reference(args, rank, world):
     # each step: a bounded sample (one 1280x64 strip = 1/12 of a padded 720p frame)
     from lic_synth import ModelSpec, generate_weights, synth_frame_u8
     from oracle import oracle as O
-    spec = ModelSpec(kind=1, N=N_CH, M=M_CH)
+    hyper = CFG["kind"] == 1
+    spec = ModelSpec(kind=CFG["kind"], N=N_CH, M=M_CH)
     w = generate_weights(spec, seed=0)
-    t = O.build_tables(w, True, 32)
+    t = O.build_tables(w, hyper, 32)
     rows = 64
 
     def step(i):
         fr = synth_frame_u8(rows, W, seed=2000 + i)
-        x, crop = O.ingest_u8(fr, hyper=True)
-        p = O.encode_planes(x, w, True, 32)
-        yb, zb = O.code_planes(p, t, True)
-        O.decode_strings(yb, zb, w, t, True, p["y_sym"].shape, p["z_sym"].shape, crop, rows, W)
+        x, crop = O.ingest_u8(fr, hyper=hyper)
+        p = O.encode_planes(x, w, hyper, 32)
+        yb, zb = O.code_planes(p, t, hyper)
+        O.decode_strings(yb, zb, w, t, hyper, p["y_sym"].shape, p["z_sym"].shape if hyper else None, crop, rows, W)
 
     for i in range(min(warm, 1)):
         step(i)
@@ -382,11 +418,11 @@ def run_reference(args, rank, world):
     for i in range(steps):
         step(i)
     dt = time.perf_counter() - t0
-    frames = steps * rows / 768.0
+    frames = steps * rows / float(padded(H, W, hyper)[0])
     v = frames / dt
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    desc = f"{steps} steps x oracle encode+decode of a 1280x{rows} strip (1/12 padded 720p frame)"
-    line = {"impl": "reference", "metric": "1280x720 encode+decode frames/s", "value": round(v, 6),
+    desc = f"{steps} steps x oracle encode+decode of a {W}x{rows} strip ({rows}/{padded(H, W, hyper)[0]} of a padded frame)"
+    line = {"impl": "reference", "metric": f"{W}x{H} encode+decode frames/s", "value": round(v, 6),
             "unit": "frames/s", "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": round(dt / steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 accumulate / f32",
             "data": "synthetic", "config": {"workload": WORKLOAD + " (oracle, bounded strip sample per step)"},
