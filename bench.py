@@ -207,6 +207,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--serial", action="store_true", help="serial reference pipeline (no overlap)")
     ap.add_argument("--zero-copy", action="store_true", help="kernels touch pinned host planes in place")
+    ap.add_argument("--activation", default="gdn", choices=["gdn", "1dn"],
+                    help="g_a / g_s normalisation: GDN, or the paper's 1DN (implementation C, PAPER.md:131-137)")
     ap.add_argument("--precision", default="split", choices=["split", "f16"],
                     help="split: fp16 hi + lo activations (graded); f16: one fp16 plane (NEXT-4, ungraded)")
     args = ap.parse_args()
@@ -234,7 +236,7 @@ def main():
     threads = args.coder_threads or max(2, min(96, ncores // max(1, world) - 2))
 
     B = args.batch
-    spec = ModelSpec(kind=CFG["kind"], N=N_CH, M=M_CH)
+    spec = ModelSpec(kind=CFG["kind"], N=N_CH, M=M_CH, activation=1 if args.activation == "1dn" else 0)
     blob = write_licw(spec, generate_weights(spec, seed=0))
     codec = lic.Codec(blob, H, W, max_batch=B, device=local,
                       precision=lic.PREC_F16 if args.precision == "f16" else lic.PREC_SPLIT)
@@ -344,7 +346,8 @@ def main():
         "vs_baseline": None,
         "dtype": "f16x2(split hi/lo)->f32" if args.precision == "split" else "f16->f32 (single plane, ungraded)",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "batch_per_gpu": B, "frames_per_gpu": nfr,
+        "config": {"workload": WORKLOAD + (", 1DN activation" if args.activation == "1dn" else ""),
+                   "batch_per_gpu": B, "frames_per_gpu": nfr,
                    "coder_threads_per_gpu": threads, "inflight": args.inflight,
                    "y_substreams": args.substreams,
                    "l2": "inputs larger than L2 (activations ~0.36 GB per frame, frame set > 126 MB)",

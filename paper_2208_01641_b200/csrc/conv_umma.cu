@@ -351,7 +351,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 cp_async_wait_all();
                 named_bar_sync(4, kL1Builders);                          // raw[it & 1] complete
                 const uint32_t rb = raw_s + (uint32_t)(it & 1) * kL1RawBytes + (uint32_t)((3 * ix0) & 3);
-#pragma unroll
+#pragma unroll 4
                 for (int r = 0; r < kL1PH; ++r) {
                     const uint32_t w0 = ldsu(lut_s + 4u * ldsb(rb + r * (4 * kL1RawWords) + e0));
                     stsh(pbh + 2u * (r * kL1Pitch + e0), w0);
