@@ -285,10 +285,9 @@ def main():
 
     # ---- device-resident run (value), events around the dominant kernel's launches only
     codec.profile(True, layers=[dom])
-    l0 = codec.launch_count()
     with ClockSampler(local) as clocks:
         ms, st = timed(dev_in, dev_out, nfr)
-    launches = codec.launch_count() - l0
+    launches = st["gpu_launches"]
     prof = codec.profile_read()
     codec.profile(False)
     if st["symbol_mismatches"]:

@@ -220,6 +220,7 @@ typedef struct {
     uint64_t y_bytes, z_bytes;/* total bitstream bytes */
     uint64_t symbol_mismatches; /* decoded != encoded symbols (must be 0: lossless) */
     double gpu_busy_s, coder_busy_s; /* summed busy time of the GPU thread / coder threads */
+    uint64_t gpu_launches;    /* kernels launched by the run (all of the pipeline's codecs) */
 } lic_pipeline_stats;
 lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_config* cfg, lic_pipeline** out);
 void lic_pipeline_close(lic_pipeline* p);

@@ -162,6 +162,8 @@ struct lic_codec {
     float *dbg_y = nullptr, *dbg_z = nullptr, *dbg_s = nullptr;
     int debug = 0;
     int zero_copy = 0;
+    std::vector<uint8_t> licw;     // the weights container, for lic_internal_clone
+    int precision = 0;
     int halo_enabled = 1;          // LIC_NO_HALO=1 in the environment disables halo mode
     int tma_out_enabled = 1;       // LIC_TMA_OUT=0 disables the TMA-store epilogue
     int cg_enabled = 1;            // LIC_CG=1 forces one CTA per tile (no cta_group::2 pairs)
@@ -675,6 +677,8 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (len < 13 || std::memcmp(licw, "LICW", 4) != 0 || licw[4] != 1) return LIC_EDIGEST;
     lic_codec* c = new lic_codec();
     auto bail = [&](lic_status st) { lic_close(c); return st; };
+    c->licw.assign(licw, licw + len);
+    c->precision = precision;
     c->kind = licw[5];
     c->act = licw[6];
     c->N = rd<uint16_t>(licw + 7);
@@ -1237,6 +1241,18 @@ extern "C" lic_status lic_launch_count(const lic_codec* c, uint64_t* n) {
 }
 
 size_t lic_internal_frame_pixels(const lic_codec* c) { return c ? (size_t)c->H * c->W : 0; }
+
+// A second codec with the same weights and geometry (own activation buffers, tensor maps and
+// stream): lets a pipeline run decoder GPU1 on its own stream concurrently with the others.
+lic_status lic_internal_clone(const lic_codec* c, lic_codec** out) {
+    if (!c || !out) return LIC_EINVAL;
+    const lic_status st = lic_open(c->licw.data(), c->licw.size(), c->device, (uint32_t)c->H, (uint32_t)c->W,
+                                   (uint32_t)c->max_batch, c->precision, out);
+    if (st == LIC_OK) (*out)->zero_copy = c->zero_copy;
+    return st;
+}
+
+uint64_t lic_internal_launches(const lic_codec* c) { return c ? c->launches : 0; }
 
 extern "C" lic_status lic_set_zero_copy(lic_codec* c, int on) {
     if (!c) return LIC_EINVAL;

@@ -65,6 +65,8 @@ struct CpuTask { CpuKind kind; int slot; int frame; };
 
 struct lic_pipeline {
     lic_codec* codec = nullptr;
+    lic_codec* codec2 = nullptr;            // decoder GPU1 (h_s on decoded z) on its own stream
+    cudaStream_t stream2 = nullptr;
     lic_pipeline_config cfg{};
     int hyper = 0;
     lic_shape ys{}, zs{};
@@ -173,7 +175,10 @@ extern "C" void lic_pipeline_close(lic_pipeline* p) {
     if (p->stream) cudaStreamSynchronize(p->stream);
     if (p->cstream) cudaStreamSynchronize(p->cstream);
     if (p->dstream) cudaStreamSynchronize(p->dstream);
+    if (p->stream2) cudaStreamSynchronize(p->stream2);
     for (cudaEvent_t e : p->events) cudaEventDestroy(e);
+    if (p->stream2) cudaStreamDestroy(p->stream2);
+    if (p->codec2) lic_close(p->codec2);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->cstream) cudaStreamDestroy(p->cstream);
     if (p->dstream) cudaStreamDestroy(p->dstream);
@@ -271,6 +276,19 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
         lic_pipeline_close(p);
         return LIC_ECUDA;
     }
+    // decoder GPU1 (three small h_s launches per batch) on a second codec and stream, so its
+    // kernels can fill the SMs other batches' kernels leave idle (env LIC_IDX_STREAM=0: off)
+    {
+        const char* e = std::getenv("LIC_IDX_STREAM");
+        if (p->hyper && !p->cfg.serial && !(e && e[0] == '0')) {
+            if ((st = lic_internal_clone(codec, &p->codec2)) != LIC_OK ||
+                cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking) != cudaSuccess) {
+                cudaGetLastError();
+                lic_pipeline_close(p);
+                return st ? st : LIC_ECUDA;
+            }
+        }
+    }
     p->events.resize(32);
     for (auto& e : p->events)
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
@@ -322,13 +340,16 @@ static lic_status gpu_call(lic_pipeline* p, const GpuTask& t, cudaEvent_t done, 
         }
         break;
     }
-    case G_IDX:
+    case G_IDX: {
+        lic_codec* cc = p->codec2 ? p->codec2 : p->codec;
+        cudaStream_t ks = p->codec2 ? p->stream2 : p->stream;
         cp(s.d_zdec, s.z_dec, B * p->nz, cudaMemcpyHostToDevice);
-        to_k();
-        if (!st) st = lic_hyper_indexes(p->codec, s.d_zdec, B, s.d_idxdec, p->stream);
-        to_c();
+        if (!st && !join(p, p->cstream, ks, ev_next)) st = LIC_ECUDA;
+        if (!st) st = lic_hyper_indexes(cc, s.d_zdec, B, s.d_idxdec, ks);
+        if (!st && !join(p, ks, p->dstream, ev_next)) st = LIC_ECUDA;
         cp(s.idx_dec, s.d_idxdec, B * p->ny, cudaMemcpyDeviceToHost);
         break;
+    }
     case G_DEC: {
         cp(s.d_ydec, s.y_dec, B * p->ny, cudaMemcpyHostToDevice);
         to_k();
@@ -383,6 +404,7 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
             p->keep_z.assign(nframes, {});
         }
     }
+    const uint64_t launches0 = lic_internal_launches(p->codec) + lic_internal_launches(p->codec2);
     const double t_run0 = now_s();
     // GPU control loop.  GPU tasks are issued asynchronously on p->stream (at most
     // kMaxPending in flight, env LIC_MAX_PENDING) so the device never idles while ready work exists; the
@@ -470,6 +492,7 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
     }
     // leave nothing running on the streams
     cudaStreamSynchronize(p->stream);
+    if (p->stream2) cudaStreamSynchronize(p->stream2);
     cudaStreamSynchronize(p->cstream);
     cudaStreamSynchronize(p->dstream);
     const double t_run1 = now_s();
@@ -493,6 +516,7 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         stats->symbol_mismatches = p->mismatches;
         stats->gpu_busy_s = p->gpu_busy;
         stats->coder_busy_s = p->coder_busy;
+        stats->gpu_launches = lic_internal_launches(p->codec) + lic_internal_launches(p->codec2) - launches0;
     }
     return p->err;
 }

@@ -89,7 +89,8 @@ class PipelineStats(ctypes.Structure):
     _fields_ = [("frames", ctypes.c_uint64), ("seconds", ctypes.c_double), ("latency_p50_ms", ctypes.c_double),
                 ("latency_p95_ms", ctypes.c_double), ("latency_max_ms", ctypes.c_double),
                 ("y_bytes", ctypes.c_uint64), ("z_bytes", ctypes.c_uint64), ("symbol_mismatches", ctypes.c_uint64),
-                ("gpu_busy_s", ctypes.c_double), ("coder_busy_s", ctypes.c_double)]
+                ("gpu_busy_s", ctypes.c_double), ("coder_busy_s", ctypes.c_double),
+                ("gpu_launches", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
