@@ -202,7 +202,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="frames per step (per GPU); 0: the config's")
     ap.add_argument("--coder-threads", type=int, default=0, help="0: derived from the host cores")
     ap.add_argument("--inflight", type=int, default=8)
-    ap.add_argument("--substreams", type=int, default=8,
+    ap.add_argument("--substreams", type=int, default=32,
                     help="y string as K channel-slab rANS substreams (DESIGN.md R21); 1 = one string")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--serial", action="store_true", help="serial reference pipeline (no overlap)")

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -174,7 +175,7 @@ extern "C" lic_status lic_rans_prepare(const uint32_t* cdf, uint32_t n_rows, uin
     t->n_rows = n_rows; t->row_len = row_len; t->nsym = row_len - 1; t->sym_min = sym_min;
     t->cdf.assign(cdf, cdf + (size_t)n_rows * row_len);
     t->enc.resize((size_t)n_rows * t->nsym);
-    t->bucket.resize((size_t)n_rows * 4096);
+    t->bucket.resize((size_t)n_rows * 4096 + 4);     // +4: 4-byte gathers of the last entry (AVX-512 path)
     for (uint32_t r = 0; r < n_rows; ++r) {
         const uint32_t* c = &t->cdf[(size_t)r * row_len];
         if (c[0] != 0 || c[t->nsym] != kProbScale) { delete t; return LIC_EINVAL; }
@@ -480,6 +481,248 @@ bool validate_planes(const lic_rans_tables* t, const int8_t* sym, const uint8_t*
     return bad == 0;
 }
 
+// ------------------------------------------------------------------ AVX-512: 16 strings per thread
+// The 16 channel-slab strings of a group are coded in the 16 lanes of a vector (state x, input /
+// output offsets, table lookups by gather).  Same bitstream as the scalar coder: each lane runs the
+// exact scalar recurrence.  Used when the slabs of a group are equal (C % K == 0) and the CPU has
+// AVX-512 (env LIC_NO_AVX512=1 disables); the first (encoder) / last (decoder) few symbols of
+// every string, where 4-byte gathers could read past an array, run through the scalar steps.
+#if defined(__x86_64__) && defined(__GNUC__)
+#include <immintrin.h>
+#define LIC_AVX512 __attribute__((target("avx512f,avx512bw,avx512vl,avx512dq")))
+
+bool use_avx512() {
+    static const bool ok = [] {
+        const char* e = std::getenv("LIC_NO_AVX512");
+        if (e && e[0] == '1') return false;
+        __builtin_cpu_init();
+        return __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
+               __builtin_cpu_supports("avx512vl") && __builtin_cpu_supports("avx512dq");
+    }();
+    return ok;
+}
+
+bool simd_group_ok(const SlabGeom& g, uint32_t k0, int nl) {
+    const size_t n = g.count[k0];
+    if (n < 16 || n % 4 || n * (size_t)nl >= (1ull << 31)) return false;
+    for (int j = 1; j < nl; ++j)
+        if (g.count[k0 + j] != n || g.begin[k0 + j] != g.begin[k0] + (size_t)j * n) return false;
+    return true;
+}
+
+// V vectors of 16 lanes (16V strings): V independent dependency chains per step hide the
+// gather latencies of one chain (slot -> bucket -> cdf -> state -> renormalisation).
+template <int V>
+LIC_AVX512 lic_status dec_avx512(const lic_rans_tables* tab, const uint8_t* base, const uint8_t* const* in,
+                                 const size_t* len, const uint8_t* row, const SlabGeom& g, int k0, int8_t* sym_out) {
+    constexpr int NL = 16 * V;
+    const size_t n = g.count[k0], hw = g.hw ? g.hw : 1;
+    alignas(64) uint32_t xs[NL], off[NL], endo[NL], chs[NL];
+    for (int j = 0; j < NL; ++j) {
+        if (len[j] < 4) return LIC_ECORRUPT;
+        const uint8_t* q = in[j];
+        xs[j] = ((uint32_t)q[0] << 24) | ((uint32_t)q[1] << 16) | ((uint32_t)q[2] << 8) | q[3];
+        off[j] = (uint32_t)(q + 4 - base);
+        endo[j] = (uint32_t)(q + len[j] - base);
+        chs[j] = g.ch0[k0 + j];
+    }
+    const int* cdf = reinterpret_cast<const int*>(tab->cdf.data());
+    const void* bucket = tab->bucket.data();
+    __m512i x[V], vo[V], ve[V], ch0[V], slab[V];
+    const __m512i lanes = _mm512_setr_epi32(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15);
+    for (int v = 0; v < V; ++v) {
+        x[v] = _mm512_load_si512(xs + 16 * v);
+        vo[v] = _mm512_load_si512(off + 16 * v);
+        ve[v] = _mm512_load_si512(endo + 16 * v);
+        ch0[v] = _mm512_load_si512(chs + 16 * v);
+        slab[v] = _mm512_mullo_epi32(_mm512_add_epi32(lanes, _mm512_set1_epi32(16 * v)), _mm512_set1_epi32((int)n));
+    }
+    const __m512i L = _mm512_set1_epi32((int)kRansLow), m16 = _mm512_set1_epi32(0xFFFF), ff = _mm512_set1_epi32(0xFF);
+    const __m512i one = _mm512_set1_epi32(1), rl = _mm512_set1_epi32((int)tab->row_len);
+    const __m512i smin = _mm512_set1_epi32(tab->sym_min), twelve = _mm512_set1_epi32(12);
+    const uint8_t* rowg = row ? row + g.begin[k0] : nullptr;
+    int8_t* outg = sym_out + g.begin[k0];
+    size_t i = 0;
+    // de-interleave two vectors of 8 (lo, hi) dword pairs into 16 lo / 16 hi dwords
+    const __m512i even = _mm512_setr_epi32(0, 2, 4, 6, 8, 10, 12, 14, 16, 18, 20, 22, 24, 26, 28, 30);
+    const __m512i odd = _mm512_setr_epi32(1, 3, 5, 7, 9, 11, 13, 15, 17, 19, 21, 23, 25, 27, 29, 31);
+    for (; i + 8 <= n; i += 4) {
+        // <= 8 input bytes per lane in 4 steps, 4-byte gather windows: stop 12 bytes before an end
+        __mmask16 low = 0;
+        for (int v = 0; v < V; ++v) low |= _mm512_cmplt_epu32_mask(_mm512_sub_epi32(ve[v], vo[v]), twelve);
+        if (low) break;
+        __m512i w[V], rows4[V];
+        for (int v = 0; v < V; ++v) {
+            w[v] = _mm512_setzero_si512();
+            if (rowg) rows4[v] = _mm512_i32gather_epi32(slab[v], rowg + i, 1);     // rows of steps i .. i+3
+        }
+        for (int u = 0; u < 4; ++u) {
+            const size_t ii = i + u;
+            const __m512i chv = _mm512_set1_epi32((int)(ii / hw));
+#pragma GCC unroll 4
+            for (int v = 0; v < V; ++v) {
+                const __m512i r = rowg ? _mm512_and_si512(_mm512_srli_epi32(rows4[v], 8 * u), ff)
+                                       : _mm512_add_epi32(ch0[v], chv);
+                const __m512i slot = _mm512_and_si512(x[v], m16);
+                const __m512i bidx = _mm512_add_epi32(_mm512_slli_epi32(r, 12), _mm512_srli_epi32(slot, 4));
+                __m512i s = _mm512_and_si512(_mm512_i32gather_epi32(bidx, bucket, 1), ff);
+                const __m512i cb = _mm512_mullo_epi32(r, rl);
+                __m512i st, nxt;
+                for (;;) {                   // (c[s], c[s + 1]) pairs by 64-bit gathers; c[s + 1] <= slot: next
+                    const __m512i ci = _mm512_add_epi32(cb, s);
+                    const __m512i p0 = _mm512_i32gather_epi64(_mm512_castsi512_si256(ci), cdf, 4);
+                    const __m512i p1 = _mm512_i32gather_epi64(_mm512_extracti64x4_epi64(ci, 1), cdf, 4);
+                    st = _mm512_permutex2var_epi32(p0, even, p1);
+                    nxt = _mm512_permutex2var_epi32(p0, odd, p1);
+                    const __mmask16 m = _mm512_cmple_epu32_mask(nxt, slot);
+                    if (!m) break;
+                    s = _mm512_mask_add_epi32(s, m, s, one);
+                }
+                __m512i xv = _mm512_add_epi32(_mm512_mullo_epi32(_mm512_sub_epi32(nxt, st), _mm512_srli_epi32(x[v], 16)),
+                                              _mm512_sub_epi32(slot, st));
+                // at most two renormalisation bytes, both from one 4-byte gather
+                const __mmask16 m1 = _mm512_cmplt_epu32_mask(xv, L);
+                const __m512i b4 = _mm512_mask_i32gather_epi32(_mm512_setzero_si512(), m1, vo[v], base, 1);
+                xv = _mm512_mask_or_epi32(xv, m1, _mm512_slli_epi32(xv, 8), _mm512_and_si512(b4, ff));
+                const __mmask16 m2 = _mm512_cmplt_epu32_mask(xv, L);              // subset of m1
+                xv = _mm512_mask_or_epi32(xv, m2, _mm512_slli_epi32(xv, 8), _mm512_and_si512(_mm512_srli_epi32(b4, 8), ff));
+                vo[v] = _mm512_mask_add_epi32(vo[v], m1, vo[v], one);
+                vo[v] = _mm512_mask_add_epi32(vo[v], m2, vo[v], one);
+                x[v] = xv;
+                w[v] = _mm512_or_si512(w[v], _mm512_slli_epi32(_mm512_and_si512(_mm512_add_epi32(s, smin), ff), 8 * u));
+            }
+        }
+        for (int v = 0; v < V; ++v) _mm512_i32scatter_epi32(outg + i, slab[v], w[v], 1);
+    }
+    // scalar continuation of every lane
+    for (int v = 0; v < V; ++v) {
+        _mm512_store_si512(xs + 16 * v, x[v]);
+        _mm512_store_si512(off + 16 * v, vo[v]);
+    }
+    const DecCtx t{tab->cdf.data(), tab->bucket.data(), tab->row_len, tab->n_rows, tab->sym_min};
+    for (int j = 0; j < NL; ++j) {
+        uint32_t xv = xs[j], ch = g.ch0[k0 + j] + (uint32_t)(i / hw);
+        size_t rem = hw - i % hw;
+        const uint8_t* pj = base + off[j];
+        const uint8_t* end = base + endo[j];
+        const size_t b0 = g.begin[k0 + j];
+        for (size_t ii = i; ii < n; ++ii) {
+            const int st = row ? dec_step<true>(t, row, hw, b0 + ii, xv, pj, end, ch, rem, sym_out)
+                               : dec_step<false>(t, row, hw, b0 + ii, xv, pj, end, ch, rem, sym_out);
+            if (st) return (lic_status)st;
+        }
+        if (xv != kRansLow || pj != end) return LIC_ECORRUPT;
+    }
+    return LIC_OK;
+}
+
+template <int V>
+LIC_AVX512 lic_status enc_avx512(const lic_rans_tables* tab, const int8_t* sym, const uint8_t* row,
+                                 const SlabGeom& g, int k0, uint8_t* base, uint8_t* const* hi, uint8_t** ptr_out) {
+    constexpr int NL = 16 * V;
+    const size_t n = g.count[k0], hw = g.hw ? g.hw : 1;
+    const EncCtx t{tab->enc.data(), tab->nsym, tab->n_rows, tab->sym_min};
+    alignas(64) uint32_t xs[NL], off[NL], chs[NL];
+    // scalar head: the last 4 symbols of every string (4-byte gathers stay inside the planes below)
+    const size_t head = 4;
+    for (int j = 0; j < NL; ++j) {
+        uint32_t xv = kRansLow, ch = g.ch0[k0 + j] + (uint32_t)((n - 1) / hw);
+        size_t rem = (n - 1) % hw + 1;
+        uint8_t* pj = hi[j];
+        for (size_t ii = n; ii-- > n - head;)
+            row ? enc_step<true>(t, sym, row, hw, g.begin[k0 + j] + ii, xv, pj, ch, rem)
+                : enc_step<false>(t, sym, row, hw, g.begin[k0 + j] + ii, xv, pj, ch, rem);
+        xs[j] = xv;
+        off[j] = (uint32_t)(pj - base);
+        chs[j] = g.ch0[k0 + j];
+    }
+    const int* enc = reinterpret_cast<const int*>(tab->enc.data());
+    __m512i x[V], vp[V], ch0[V], slab[V];
+    const __m512i lanes = _mm512_setr_epi32(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15);
+    for (int v = 0; v < V; ++v) {
+        x[v] = _mm512_load_si512(xs + 16 * v);
+        vp[v] = _mm512_load_si512(off + 16 * v);
+        ch0[v] = _mm512_load_si512(chs + 16 * v);
+        slab[v] = _mm512_mullo_epi32(_mm512_add_epi32(lanes, _mm512_set1_epi32(16 * v)), _mm512_set1_epi32((int)n));
+    }
+    const __m512i ff = _mm512_set1_epi32(0xFF), one = _mm512_set1_epi32(1), two = _mm512_set1_epi32(2);
+    const __m512i three = _mm512_set1_epi32(3);
+    const __m512i nsym = _mm512_set1_epi32((int)tab->nsym), smin = _mm512_set1_epi32(tab->sym_min);
+    const __m512i m16 = _mm512_set1_epi32(0xFFFF);
+    const uint8_t* rowg = row ? row + g.begin[k0] : nullptr;
+    const int8_t* symg = sym + g.begin[k0];
+    const __m512i even = _mm512_setr_epi32(0, 2, 4, 6, 8, 10, 12, 14, 16, 18, 20, 22, 24, 26, 28, 30);
+    const __m512i odd = _mm512_setr_epi32(1, 3, 5, 7, 9, 11, 13, 15, 17, 19, 21, 23, 25, 27, 29, 31);
+    // groups of 4 symbols (n - head is a multiple of 4): rows and symbols of steps i0 .. i0+3 from one
+    // 4-byte gather each, coded i0+3 first
+    for (size_t i0 = n - head; i0 >= 4;) {
+        i0 -= 4;
+        __m512i rows4[V], syms4[V];
+        for (int v = 0; v < V; ++v) {
+            if (rowg) rows4[v] = _mm512_i32gather_epi32(slab[v], rowg + i0, 1);
+            syms4[v] = _mm512_i32gather_epi32(slab[v], symg + i0, 1);
+        }
+        for (int u = 3; u >= 0; --u) {
+            const size_t i = i0 + (size_t)u;
+            const __m512i chv = _mm512_set1_epi32((int)(i / hw));
+#pragma GCC unroll 4
+            for (int v = 0; v < V; ++v) {
+                const __m512i r = rowg ? _mm512_and_si512(_mm512_srli_epi32(rows4[v], 8 * u), ff)
+                                       : _mm512_add_epi32(ch0[v], chv);
+                const __m512i sv = _mm512_srai_epi32(_mm512_slli_epi32(syms4[v], 24 - 8 * u), 24);
+                const __m512i e4 = _mm512_slli_epi32(_mm512_add_epi32(_mm512_mullo_epi32(r, nsym), _mm512_sub_epi32(sv, smin)), 2);
+                // EncSym = {xmax, rcp} {bias, cmpl | shift << 16}: two 64-bit gathers per half
+                const __m512i e2 = _mm512_add_epi32(e4, two);
+                const __m512i a0 = _mm512_i32gather_epi64(_mm512_castsi512_si256(e4), enc, 4);
+                const __m512i a1 = _mm512_i32gather_epi64(_mm512_extracti64x4_epi64(e4, 1), enc, 4);
+                const __m512i b0 = _mm512_i32gather_epi64(_mm512_castsi512_si256(e2), enc, 4);
+                const __m512i b1 = _mm512_i32gather_epi64(_mm512_extracti64x4_epi64(e2, 1), enc, 4);
+                const __m512i xmax = _mm512_permutex2var_epi32(a0, even, a1);
+                const __m512i rcp = _mm512_permutex2var_epi32(a0, odd, a1);
+                const __m512i bias = _mm512_permutex2var_epi32(b0, even, b1);
+                const __m512i cs = _mm512_permutex2var_epi32(b0, odd, b1);
+                __m512i xv = x[v];
+                for (int rn = 0; rn < 2; ++rn) {             // at most two renormalisation bytes, emitted downwards
+                    const __mmask16 m = _mm512_cmpge_epu32_mask(xv, xmax);
+                    vp[v] = _mm512_mask_sub_epi32(vp[v], m, vp[v], one);
+                    // a 4-byte store whose top byte lands at the new pointer (the 3 bytes below belong
+                    // to this lane's region and are rewritten later or lie outside the string)
+                    _mm512_mask_i32scatter_epi32(base, m, _mm512_sub_epi32(vp[v], three), _mm512_slli_epi32(xv, 24), 1);
+                    xv = _mm512_mask_srli_epi32(xv, m, xv, 8);
+                }
+                const __m512i pe = _mm512_srli_epi64(_mm512_mul_epu32(xv, rcp), 32);
+                const __m512i po = _mm512_mul_epu32(_mm512_srli_epi64(xv, 32), _mm512_srli_epi64(rcp, 32));
+                const __m512i q = _mm512_srlv_epi32(_mm512_mask_blend_epi32(0xAAAA, pe, po), _mm512_srli_epi32(cs, 16));
+                x[v] = _mm512_add_epi32(_mm512_add_epi32(xv, bias), _mm512_mullo_epi32(q, _mm512_and_si512(cs, m16)));
+            }
+        }
+    }
+    for (int v = 0; v < V; ++v) {
+        _mm512_store_si512(xs + 16 * v, x[v]);
+        _mm512_store_si512(off + 16 * v, vp[v]);
+    }
+    for (int j = 0; j < NL; ++j) {
+        uint8_t* pj = base + off[j];
+        *--pj = (uint8_t)xs[j];
+        *--pj = (uint8_t)(xs[j] >> 8);
+        *--pj = (uint8_t)(xs[j] >> 16);
+        *--pj = (uint8_t)(xs[j] >> 24);
+        ptr_out[j] = pj;
+    }
+    return LIC_OK;
+}
+
+// largest vector group (V = 4, 2, 1 x 16 strings) that fits the remaining slabs
+int simd_lanes(const SlabGeom& g, uint32_t k0, uint32_t left) {
+    if (!use_avx512()) return 0;
+    for (int nl = 64; nl >= 16; nl >>= 1)
+        if ((int)left >= nl && simd_group_ok(g, k0, nl)) return nl;
+    return 0;
+}
+#else
+int simd_lanes(const SlabGeom&, uint32_t, uint32_t) { return 0; }
+#endif
+
 inline void put_be32(uint8_t* q, uint32_t v) {
     q[0] = (uint8_t)(v >> 24); q[1] = (uint8_t)(v >> 16); q[2] = (uint8_t)(v >> 8); q[3] = (uint8_t)v;
 }
@@ -508,6 +751,16 @@ extern "C" lic_status lic_rans_encode_slabs(const lic_rans_tables* t, const int8
     for (uint32_t k = 0; k < K; ++k) hi[k] = scratch.data() + off[k] + 2 * g.count[k] + 8;
     for (uint32_t k0 = 0; k0 < K;) {
         const uint32_t left = K - k0;
+#if defined(__x86_64__) && defined(__GNUC__)
+        if (const int nl = simd_lanes(g, k0, left)) {
+            const lic_status st = nl == 64 ? enc_avx512<4>(t, sym, row, g, (int)k0, scratch.data(), hi + k0, start + k0)
+                                : nl == 32 ? enc_avx512<2>(t, sym, row, g, (int)k0, scratch.data(), hi + k0, start + k0)
+                                           : enc_avx512<1>(t, sym, row, g, (int)k0, scratch.data(), hi + k0, start + k0);
+            if (st) return st;
+            k0 += (uint32_t)nl;
+            continue;
+        }
+#endif
         const int G = left >= 4 ? 4 : left >= 2 ? 2 : 1;
         lic_status st;
         if (row) {
@@ -558,6 +811,16 @@ extern "C" lic_status lic_rans_decode_slabs(const lic_rans_tables* t, const uint
     if (pos != len) return LIC_ECORRUPT;
     for (uint32_t k0 = 0; k0 < K;) {
         const uint32_t left = K - k0;
+#if defined(__x86_64__) && defined(__GNUC__)
+        if (const int nl = simd_lanes(g, k0, left)) {
+            const lic_status st = nl == 64 ? dec_avx512<4>(t, in, sp + k0, sl + k0, row, g, (int)k0, sym_out)
+                                : nl == 32 ? dec_avx512<2>(t, in, sp + k0, sl + k0, row, g, (int)k0, sym_out)
+                                           : dec_avx512<1>(t, in, sp + k0, sl + k0, row, g, (int)k0, sym_out);
+            if (st) return st;
+            k0 += (uint32_t)nl;
+            continue;
+        }
+#endif
         const int G = left >= 4 ? 4 : left >= 2 ? 2 : 1;
         lic_status st;
         if (row) {

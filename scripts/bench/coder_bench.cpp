@@ -29,7 +29,7 @@ int main(int argc, char** argv) {
     }
     std::vector<uint8_t> out(2 * n + 1024);
     lic_shape sh{C, H, W};
-    for (uint32_t K : {1u, 2u, 4u, 8u, 16u}) {
+    for (uint32_t K : {1u, 4u, 8u, 16u, 32u, 64u}) {
         size_t len = 0;
         double be = 1e9, bd = 1e9;
         for (int rep = 0; rep < 15; ++rep) {

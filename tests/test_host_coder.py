@@ -130,7 +130,9 @@ def test_fast_coder_general_tables(lic):
 
 # ---------------------------------------------------------------- channel-slab substreams (R21)
 @pytest.mark.parametrize("C,H,W,K", [(192, 48, 80, 4), (192, 12, 20, 8), (128, 3, 5, 3), (10, 7, 9, 4),
-                                     (5, 4, 4, 5), (192, 2, 3, 1), (64, 1, 1, 64)])
+                                     (5, 4, 4, 5), (192, 2, 3, 1), (64, 1, 1, 64),
+                                     (192, 48, 80, 16), (320, 12, 20, 32), (192, 3, 7, 16), (48, 8, 8, 16),
+                                     (192, 48, 80, 64), (192, 12, 20, 32), (320, 6, 10, 64), (128, 5, 4, 48)])
 def test_slab_substreams_channel_rows_bit_exact(lic, C, H, W, K):
     """Product lic_rans_encode_slabs == oracle rans_encode_slabs byte for byte (ragged slabs
     when K does not divide C), lossless through both decoders."""
@@ -144,8 +146,9 @@ def test_slab_substreams_channel_rows_bit_exact(lic, C, H, W, K):
     assert np.array_equal(O.rans_decode_slabs(b, sym.shape, None, cdf, K), sym)
 
 
-@pytest.mark.parametrize("K", [1, 2, 4, 6, 8])
+@pytest.mark.parametrize("K", [1, 2, 4, 6, 8, 16, 32, 64])
 def test_slab_substreams_indexed_rows_bit_exact(lic, K):
+    """K a multiple of 16 with equal slabs runs the AVX-512 coder where the CPU has it (same bytes)."""
     L = 32
     cdf = O.cdf_table(scale_table(), L)
     C, H, W = 192, 24, 40
@@ -176,3 +179,30 @@ def test_slab_substreams_corrupt(lic):
         t.decode(bytes(bb), sym.shape, substreams=4)
     with pytest.raises(lic.LicError):
         t.encode(sym, substreams=C + 1)   # more slabs than channels
+
+
+@pytest.mark.parametrize("K", [16, 32, 64])
+def test_slab_substreams_simd_corrupt_fuzz(lic, K):
+    """Damaged K = 16..64 strings (the vectorised decoder's lanes) fail cleanly: truncation and
+    trailing bytes are corrupt; flipped bytes either fail or decode to some symbols, never read
+    outside the string."""
+    L = 32
+    rng = np.random.default_rng(99)
+    cdf = O.cdf_table(scale_table(), L)
+    C, H, W = 192, 6, 10
+    idx = rng.integers(0, 64, (C, H, W)).astype(np.uint8)
+    sym = np.clip(np.round(rng.standard_normal((C, H, W)) * scale_table()[idx] * 0.5), -L, L).astype(np.int8)
+    t = lic.RansTables(cdf)
+    b = t.encode(sym, rows=idx, substreams=K)
+    assert np.array_equal(t.decode(b, sym.shape, rows=idx, substreams=K), sym)
+    for bad in (b[:-1], b + b"\x00", b[:4 * K + 6]):
+        with pytest.raises(lic.CorruptStream):
+            t.decode(bad, sym.shape, rows=idx, substreams=K)
+    for _ in range(200):
+        bb = bytearray(b)
+        for pos in rng.integers(4 * K, len(bb), 3):
+            bb[pos] ^= int(rng.integers(1, 256))
+        try:
+            t.decode(bytes(bb), sym.shape, rows=idx, substreams=K)
+        except lic.CorruptStream:
+            pass
