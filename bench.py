@@ -190,6 +190,22 @@ def oracle_sample(seconds_budget=15.0, strip_rows=64, seed=0):
                                   f"(= {frac:.4f} of a padded {W}x{H} frame each), {dt:.1f} s")
 
 
+# ----------------------------------------------------------------- per-rank cores
+def bind_rank_cores(local, world):
+    """One process per GPU shares the host: give local rank r its own contiguous slice of the
+    cores it may run on, so each rank's coder pool and GPU control thread stay off the others'
+    cores (env LIC_BIND_CORES=0: no binding).  Returns the slice (or None)."""
+    if world <= 1 or os.environ.get("LIC_BIND_CORES", "1") == "0" or not hasattr(os, "sched_setaffinity"):
+        return None
+    cores = sorted(os.sched_getaffinity(0))
+    per = len(cores) // world
+    if per < 2:
+        return None
+    mine = cores[local * per:(local + 1) * per]
+    os.sched_setaffinity(0, mine)
+    return mine
+
+
 # ----------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -234,6 +250,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 8)
     threads = args.coder_threads or max(2, min(96, ncores // max(1, world) - 2))
+    bound = bind_rank_cores(local, world)
 
     B = args.batch
     spec = ModelSpec(kind=CFG["kind"], N=N_CH, M=M_CH, activation=1 if args.activation == "1dn" else 0)
@@ -348,6 +365,7 @@ def main():
         "config": {"workload": WORKLOAD + (", 1DN activation" if args.activation == "1dn" else ""),
                    "batch_per_gpu": B, "frames_per_gpu": nfr,
                    "coder_threads_per_gpu": threads, "inflight": args.inflight,
+                   "cores_per_rank": len(bound) if bound else ncores,
                    "y_substreams": args.substreams,
                    "l2": "inputs larger than L2 (activations ~0.36 GB per frame, frame set > 126 MB)",
                    "pipeline": "serial" if args.serial else "overlapped"},
