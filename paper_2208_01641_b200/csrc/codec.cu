@@ -334,6 +334,7 @@ static int pow2_cols(int n) {
 static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     ConvParams& P = Ly.prm;
     std::memset(&P, 0, sizeof P);
+    P.tps = 1;
     const bool gemm_l1 = (&Ly == &c->layers[GA1]);
     P.Cin = Ly.Cin_eff;
     P.kchunks = Ly.Cin_eff / 64;
@@ -466,7 +467,10 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.Wt = 8; P.Ht = 16;
         P.halo_plane_bytes = hpb;
         P.halo_w = halo_w;
-        P.stage_bytes = b_bytes;
+        // several taps per weight stage (one wait per 8 * tps MMAs; env LIC_TPS=1..4)
+        P.tps = 2;
+        if (const char* e = std::getenv("LIC_TPS")) P.tps = std::max(1, std::min(kMaxTps, atoi(e)));
+        P.stage_bytes = b_bytes * (uint32_t)P.tps;
         // halo ring depth: env LIC_HALO_SLOTS (2..4, default 2: a halo chunk is reused by all
         // its taps, while every tap needs a fresh weight tile, so smem goes to the weight ring)
         int slots = 2;

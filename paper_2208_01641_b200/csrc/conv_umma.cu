@@ -489,14 +489,17 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
             if (lane == 0) LIC_TRACE(pit, T_PROD_START);
             if (p.halo) {
-                // chunk-outer, tap-inner weight tiles (halos come from warp 3)
+                // chunk-outer, tap-inner weight tiles (halos come from warp 3); p.tps consecutive
+                // taps share a stage (one barrier wait per 8 * tps MMAs)
                 for (int c = 0; c < p.kchunks; ++c)
-                    for (int ti = 0; ti < nt; ++ti) {
+                    for (int ti = 0; ti < nt; ti += p.tps) {
+                        const int ntp = min(p.tps, nt - ti);
                         mbar_wait(&empty_bar[stage], phase ^ 1);
                         if (elect_one()) {
-                            expect(&full_bar[stage], b_bytes);
-                            ld3(smem + stage * p.stage_bytes, &mapB, &full_bar[stage], c * kBK,
-                                tc.nt * p.BN + rank * bnc, p.tap_w[t0 + ti]);
+                            expect(&full_bar[stage], b_bytes * (uint32_t)ntp);
+                            for (int u = 0; u < ntp; ++u)
+                                ld3(smem + stage * p.stage_bytes + u * b_bytes, &mapB, &full_bar[stage], c * kBK,
+                                    tc.nt * p.BN + rank * bnc, p.tap_w[t0 + ti + u]);
                         }
                         __syncwarp();
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
@@ -627,7 +630,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     tc_fence_after();
                     if (lane == 0 && c == 0) LIC_TRACE(it, T_MMA_K0);
                     const uint32_t hb = smem_u32(smem + p.off_halo + hs * (p.split * p.halo_plane_bytes));
-                    for (int ti = 0; ti < nt; ++ti) {
+                    // p.tps taps per weight stage: one barrier wait / fence / commit per 8 * tps MMAs
+                    // (the issue loop, not the tensor pipe, is what waits between groups)
+                    const int tps = p.wres ? 1 : p.tps;
+                    for (int ti = 0; ti < nt; ti += tps) {
+                        const int ntp = min(tps, nt - ti);
                         uint32_t bsm;
                         if (p.wres) {
                             bsm = smem_u32(smem + p.off_wres + ((t0 + ti) * p.kchunks + c) * b_bytes);
@@ -636,16 +643,21 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             tc_fence_after();
                             bsm = smem_u32(smem + stage * p.stage_bytes);
                         }
-                        // window of this tap: halo row (dy+1)*(Wt+2) + (dx+1), 8-row groups every Wt+2 rows
-                        const uint32_t row0 = (uint32_t)((p.tap_dy[t0 + ti] + 1) * p.halo_w + p.tap_dx[t0 + ti] + 1);
-                        const uint64_t ah = sdesc_sw128_sbo(hb + row0 * 128, sbo);
-                        const uint64_t al = sdesc_sw128_sbo(hb + p.halo_plane_bytes + row0 * 128, sbo);
-                        const uint64_t bd = sdesc_sw128(bsm);
+                        // window of tap ti + u: halo row (dy+1)*(Wt+2) + (dx+1), 8-row groups every Wt+2 rows
                         if (elect_one()) {
 #pragma unroll
-                            for (int kk = 0; kk < kBK / 16; ++kk) {
-                                mma_ss(d, ah + 2 * kk, bd + 2 * kk, (c | ti | kk) != 0);
-                                if (p.split == 2) mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
+                            for (int u = 0; u < kMaxTps; ++u) {
+                                if (u < ntp) {
+                                    const uint32_t r0 = (uint32_t)((p.tap_dy[t0 + ti + u] + 1) * p.halo_w + p.tap_dx[t0 + ti + u] + 1);
+                                    const uint64_t ah = sdesc_sw128_sbo(hb + r0 * 128, sbo);
+                                    const uint64_t al = sdesc_sw128_sbo(hb + p.halo_plane_bytes + r0 * 128, sbo);
+                                    const uint64_t bd = sdesc_sw128(bsm + (uint32_t)u * b_bytes);
+#pragma unroll
+                                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                                        mma_ss(d, ah + 2 * kk, bd + 2 * kk, (c | ti | u | kk) != 0);
+                                        if (p.split == 2) mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
+                                    }
+                                }
                             }
                             if (!p.wres) commit(&empty_bar[stage]);
                         }

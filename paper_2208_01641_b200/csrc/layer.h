@@ -24,6 +24,7 @@ enum EpKind : int {
 };
 
 constexpr int kMaxTaps = 32;
+constexpr int kMaxTps = 4;      // halo mode: at most 4 taps per weight stage
 constexpr int kBM = 128;        // pixels per tile (UMMA M)
 constexpr int kBK = 64;         // channels per K chunk (one 128-byte swizzle row of fp16)
 
@@ -55,6 +56,7 @@ struct ConvParams {
     // 2-slot ring and every tap reads its A operand as a shifted window of it; the stage
     // ring then carries only weight tiles.  Tile fixed at Wt = 8, Ht = 16.
     int halo, halo_slots, halo_w;      // halo_w: halo row pitch in pixels (>= Wt + 2)
+    int tps;                          // halo mode: taps per weight stage (1 .. kMaxTps)
     uint32_t off_halo, halo_plane_bytes;
     int wres;                         // all weight tiles resident in smem (loaded once per CTA)
     uint32_t off_wres;
