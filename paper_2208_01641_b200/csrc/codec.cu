@@ -170,6 +170,7 @@ struct lic_codec {
     int gs4_bn = 32;               // packed g_s L4 N tile (env LIC_GS4_BN=16|32)
     int pdl_enabled = 1;           // programmatic dependent launch of the GEMM engine (env LIC_PDL=0 disables)
     int small_bn = 0;              // N tile of the h_a / h_s layers (env LIC_SMALL_BN=64|128; 0 = whole Cout: measured no gain)
+    int s2halo_enabled = 1;        // 5x5/s2 convs in parity-sub-grid halo mode (env LIC_S2HALO=0: per-tap tiles)
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
@@ -366,6 +367,24 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.Hg = Ly.Hout; P.Wg = Ly.Wout; P.stride = 1; P.out_s = 1; P.nphase = 1;
         P.tap0[0] = 0; P.ntaps[0] = 1; P.tap_dy[0] = 0; P.tap_dx[0] = 0; P.tap_w[0] = 0;
         ntap = 1;
+    } else if (!Ly.deconv && Ly.k == 5 && Ly.s == 2 && c->s2halo_enabled && c->halo_enabled) {
+        // 5x5 / stride 2 / pad 2 conv as four stride-1 convolutions over the input's parity
+        // sub-grids (py, px): tap (ky, kx) reads sub-grid (ky % 2, kx % 2) at offset
+        // ((ky - py) / 2 - 1, (kx - px) / 2 - 1) in [-1, 1]^2 of the output pixel, so each
+        // sub-grid contributes through a (Wt + 2) x (Ht + 2) halo (loaded with TMA element
+        // stride 2) and its taps are shifted windows of it -- 4 halo loads per 64-channel chunk
+        // instead of 25 tap tiles.  Groups g = py * 2 + px with 9 / 6 / 6 / 4 taps.
+        P.Hg = Ly.Hout; P.Wg = Ly.Wout; P.stride = 2; P.out_s = 1; P.nphase = 1; P.sub4 = 1;
+        for (int g = 0; g < 4; ++g) {
+            const int py = g >> 1, px = g & 1;
+            P.tap0[g] = ntap;
+            for (int ky = py; ky < 5; ky += 2)
+                for (int kx = px; kx < 5; kx += 2) {
+                    P.tap_dy[ntap] = (ky - py) / 2 - 1; P.tap_dx[ntap] = (kx - px) / 2 - 1;
+                    P.tap_w[ntap] = ky * 5 + kx; ++ntap;
+                }
+            P.ntaps[g] = ntap - P.tap0[g];
+        }
     } else if (!Ly.deconv) {
         P.Hg = Ly.Hout; P.Wg = Ly.Wout; P.stride = Ly.s; P.out_s = 1; P.nphase = 1;
         P.tap0[0] = 0;
@@ -424,12 +443,12 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     {
         const uint32_t fx = gamma_bytes + kBarBytes + par_bytes + 1024 + ostage_bytes;
         const uint32_t st_b = a_bytes * P.split + b_bytes;     // per-tap stage (non-halo)
-        const bool stride1_ = !gemm_l1 && (Ly.deconv || (Ly.k == 3 && Ly.s == 1));
+        const bool stride1_ = !gemm_l1 && (Ly.deconv || (Ly.k == 3 && Ly.s == 1) || P.sub4);
         if (!stride1_ && fx + 3 * st_b > budget) tma_out = false;
     }
     const uint32_t fixed = gamma_bytes + kBarBytes + par_bytes + 1024 + (tma_out ? ostage_bytes : 0);
     // halo mode: every stride-1 layer whose taps stay inside a 3x3 neighbourhood
-    const bool stride1 = !gemm_l1 && (Ly.deconv || (Ly.k == 3 && Ly.s == 1));
+    const bool stride1 = !gemm_l1 && (Ly.deconv || (Ly.k == 3 && Ly.s == 1) || P.sub4);
     int halo_w = 10;                                                   // Wt + 2
     if (const char* e = std::getenv("LIC_HALO_W")) halo_w = std::max(10, std::min(32, atoi(e)));
     const uint32_t hpb = ((uint32_t)(halo_w * 18 * 128) + 1023) / 1024 * 1024;   // halo_w x (Ht+2) rows
@@ -503,6 +522,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.off_halo = 0;
         P.off_gamma = stages * P.stage_bytes;
     }
+    if (P.sub4 && !P.halo) return fail(c, LIC_EINVAL, "parity-halo conv does not fit shared memory");
     if (!P.tsx) { P.tsx = P.Wt; P.tsy = P.Ht; }
     P.tiles_x = (P.Wg + P.tsx - 1) / P.tsx;
     P.tiles_y = (P.Hg + P.tsy - 1) / P.tsy;
@@ -739,6 +759,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_GS4_BN")) c->gs4_bn = (atoi(e) == 16) ? 16 : 32;
     if (const char* e = std::getenv("LIC_PDL")) c->pdl_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_GS4_GATHER")) c->gs4_gather = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_SMALL_BN")) c->small_bn = atoi(e) == 64 || atoi(e) == 128 ? atoi(e) : 0;
     if (const char* e = std::getenv("LIC_NO_WRES")) c->wres_enabled = (e[0] != '1');
     c->max_batch = (int)max_batch;

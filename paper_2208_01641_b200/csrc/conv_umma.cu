@@ -491,18 +491,22 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (p.halo) {
                 // chunk-outer, tap-inner weight tiles (halos come from warp 3); p.tps consecutive
                 // taps share a stage (one barrier wait per 8 * tps MMAs)
+                // (sub4: the 4 parity groups of each chunk in turn)
                 for (int c = 0; c < p.kchunks; ++c)
-                    for (int ti = 0; ti < nt; ti += p.tps) {
-                        const int ntp = min(p.tps, nt - ti);
-                        mbar_wait(&empty_bar[stage], phase ^ 1);
-                        if (elect_one()) {
-                            expect(&full_bar[stage], b_bytes * (uint32_t)ntp);
-                            for (int u = 0; u < ntp; ++u)
-                                ld3(smem + stage * p.stage_bytes + u * b_bytes, &mapB, &full_bar[stage], c * kBK,
-                                    tc.nt * p.BN + rank * bnc, p.tap_w[t0 + ti + u]);
+                    for (int gi = 0; gi < (p.sub4 ? 4 : 1); ++gi) {
+                        const int gnt = p.sub4 ? p.ntaps[gi] : nt, gt0 = p.sub4 ? p.tap0[gi] : t0;
+                        for (int ti = 0; ti < gnt; ti += p.tps) {
+                            const int ntp = min(p.tps, gnt - ti);
+                            mbar_wait(&empty_bar[stage], phase ^ 1);
+                            if (elect_one()) {
+                                expect(&full_bar[stage], b_bytes * (uint32_t)ntp);
+                                for (int u = 0; u < ntp; ++u)
+                                    ld3(smem + stage * p.stage_bytes + u * b_bytes, &mapB, &full_bar[stage], c * kBK,
+                                        tc.nt * p.BN + rank * bnc, p.tap_w[gt0 + ti + u]);
+                            }
+                            __syncwarp();
+                            if (++stage == p.stages) { stage = 0; phase ^= 1; }
                         }
-                        __syncwarp();
-                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     }
                 continue;
             }
@@ -536,19 +540,22 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const uint32_t hbytes = (uint32_t)p.halo_w * (p.Ht + 2) * 128 * p.split;
             for (int t = cid; t < p.total_tiles; t += ncl) {
                 TileCoord tc = decode_tile(p, t, rank);
-                for (int c = 0; c < p.kchunks; ++c) {
+                for (int c = 0; c < p.kchunks; ++c)
+                  for (int gi = 0; gi < (p.sub4 ? 4 : 1); ++gi) {
+                    // sub4: parity sub-grid (py, px) = (gi >> 1, gi & 1), rows / columns gy0 - 1 ..
+                    // of the sub-grid = input 2 * (gy0 - 1) + py .. in steps of 2 (the map's stride)
+                    const int hx = p.sub4 ? 2 * (tc.gx0 - 1) + (gi & 1) : tc.gx0 - 1;
+                    const int hy = p.sub4 ? 2 * (tc.gy0 - 1) + (gi >> 1) : tc.gy0 - 1;
                     mbar_wait(&hempty_bar[hs], hphase ^ 1);
                     uint8_t* hb = smem + p.off_halo + hs * (p.split * p.halo_plane_bytes);
                     if (elect_one()) {
                         expect(&hfull_bar[hs], hbytes);
-                        ld5(hb, &mapA, &hfull_bar[hs], c * kBK, tc.gx0 - 1, tc.gy0 - 1, tc.b, 0);
-                        if (p.split == 2)
-                            ld5(hb + p.halo_plane_bytes, &mapA, &hfull_bar[hs], c * kBK, tc.gx0 - 1,
-                                        tc.gy0 - 1, tc.b, 1);
+                        ld5(hb, &mapA, &hfull_bar[hs], c * kBK, hx, hy, tc.b, 0);
+                        if (p.split == 2) ld5(hb + p.halo_plane_bytes, &mapA, &hfull_bar[hs], c * kBK, hx, hy, tc.b, 1);
                     }
                     __syncwarp();
                     if (++hs == p.halo_slots) { hs = 0; hphase ^= 1; }
-                }
+                  }
             }
         }
     } else if (warp == 1) {
@@ -625,10 +632,12 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (p.halo) {
                 const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
                 const uint32_t sbo = (uint32_t)p.halo_w * 128;
-                for (int c = 0; c < p.kchunks; ++c) {
+                for (int c = 0; c < p.kchunks; ++c)
+                  for (int gi = 0; gi < (p.sub4 ? 4 : 1); ++gi) {
+                    const int nt = p.sub4 ? p.ntaps[gi] : p.ntaps[tc.ph], t0 = p.sub4 ? p.tap0[gi] : p.tap0[tc.ph];
                     wait_poll(&hfull_bar[hs], hphase);
                     tc_fence_after();
-                    if (lane == 0 && c == 0) LIC_TRACE(it, T_MMA_K0);
+                    if (lane == 0 && c == 0 && gi == 0) LIC_TRACE(it, T_MMA_K0);
                     const uint32_t hb = smem_u32(smem + p.off_halo + hs * (p.split * p.halo_plane_bytes));
                     // p.tps taps per weight stage: one barrier wait / fence / commit per 8 * tps MMAs
                     // (the issue loop, not the tensor pipe, is what waits between groups)
@@ -654,7 +663,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                                     const uint64_t bd = sdesc_sw128(bsm + (uint32_t)u * b_bytes);
 #pragma unroll
                                     for (int kk = 0; kk < kBK / 16; ++kk) {
-                                        mma_ss(d, ah + 2 * kk, bd + 2 * kk, (c | ti | u | kk) != 0);
+                                        mma_ss(d, ah + 2 * kk, bd + 2 * kk, (c | gi | ti | u | kk) != 0);
                                         if (p.split == 2) mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
                                     }
                                 }

@@ -57,6 +57,8 @@ struct ConvParams {
     // ring then carries only weight tiles.  Tile fixed at Wt = 8, Ht = 16.
     int halo, halo_slots, halo_w;      // halo_w: halo row pitch in pixels (>= Wt + 2)
     int tps;                          // halo mode: taps per weight stage (1 .. kMaxTps)
+    int sub4;                         // halo mode for a 5x5/s2 conv: 4 parity sub-grid halos per chunk,
+                                      // tap groups tap0[g] / ntaps[g] (g = py * 2 + px)
     uint32_t off_halo, halo_plane_bytes;
     int wres;                         // all weight tiles resident in smem (loaded once per CTA)
     uint32_t off_wres;
