@@ -171,6 +171,7 @@ struct lic_codec {
     int pdl_enabled = 1;           // programmatic dependent launch of the GEMM engine (env LIC_PDL=0 disables)
     int small_bn = 0;              // N tile of the h_a / h_s layers (env LIC_SMALL_BN=64|128; 0 = whole Cout: measured no gain)
     int s2halo_enabled = 1;        // 5x5/s2 convs in parity-sub-grid halo mode (env LIC_S2HALO=0: per-tap tiles)
+    int l1_int_enabled = 1;        // u8 frames: integer samples into g_a L1, one MMA pass (env LIC_L1_INT=0: off)
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
@@ -759,6 +760,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_GS4_BN")) c->gs4_bn = (atoi(e) == 16) ? 16 : 32;
     if (const char* e = std::getenv("LIC_PDL")) c->pdl_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_GS4_GATHER")) c->gs4_gather = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_L1_INT")) c->l1_int_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_SMALL_BN")) c->small_bn = atoi(e) == 64 || atoi(e) == 128 ? atoi(e) : 0;
     if (const char* e = std::getenv("LIC_NO_WRES")) c->wres_enabled = (e[0] != '1');
@@ -1041,6 +1043,7 @@ static lic_status encode_impl(lic_codec* c, const void* frames, int hwc, uint32_
     {
         ConvParams p = c->layers[GA1].prm;             // fused im2col: reads the frames directly
         p.frame = fdev; p.fr_u8 = hwc; p.fr_H = c->H; p.fr_W = c->W; p.fr_top = c->top; p.fr_left = c->left;
+        p.l1_int = hwc && c->l1_int_enabled;
         if ((r = run_layer(c, c->layers[GA1], p, B, st))) return r;
     }
     for (int id : {GA2, GA3})

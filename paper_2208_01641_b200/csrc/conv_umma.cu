@@ -266,7 +266,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         uint32_t* lut = reinterpret_cast<uint32_t*>(smem + p.off_lut);
         for (int u = threadIdx.x; u < 257; u += kThreads) {
             uint32_t h = 0, l = 0;
-            if (u < 256) { const float v = __fdiv_rn((float)u, 255.0f); split2(v, 0.0f, h, l); }
+            if (u < 256) {
+                if (p.l1_int) h = (uint32_t)__half_as_ushort(__float2half_rn((float)u));   // exact
+                else { const float v = __fdiv_rn((float)u, 255.0f); split2(v, 0.0f, h, l); }
+            }
             lut[u] = (h & 0xffffu) | (l << 16);
         }
         fence_proxy_async_smem();
@@ -317,6 +320,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         // (4-byte words, zero-filled outside the frame -- the frame edges are word boundaries),
         // one tile ahead of the build; otherwise per-sample loads.
         const bool fast = p.fr_u8 && (p.fr_W & 3) == 0;
+        const bool lo_on = p.split == 2 && !p.l1_int;     // the lo planes of patch and A tiles
         auto raw_issue = [&](int tt, int buf) {
             const TileCoord tn = decode_tile(p, tt, rank);
             const uint8_t* fr = reinterpret_cast<const uint8_t*>(p.frame);
@@ -355,11 +359,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 for (int r = 0; r < kL1PH; ++r) {
                     const uint32_t w0 = ldsu(lut_s + 4u * ldsb(rb + r * (4 * kL1RawWords) + e0));
                     stsh(pbh + 2u * (r * kL1Pitch + e0), w0);
-                    stsh(pbl + 2u * (r * kL1Pitch + e0), w0 >> 16);
+                    if (lo_on) stsh(pbl + 2u * (r * kL1Pitch + e0), w0 >> 16);
                     if (has1) {
                         const uint32_t w1 = ldsu(lut_s + 4u * ldsb(rb + r * (4 * kL1RawWords) + e1));
                         stsh(pbh + 2u * (r * kL1Pitch + e1), w1);
-                        stsh(pbl + 2u * (r * kL1Pitch + e1), w1 >> 16);
+                        if (lo_on) stsh(pbl + 2u * (r * kL1Pitch + e1), w1 >> 16);
                     }
                 }
             } else if (p.fr_u8) {
@@ -380,11 +384,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 for (int r = 0; r < kL1PH; ++r) {
                     const uint32_t w0 = ldsu(lut_s + 4u * u0[r]);                 // hi | lo << 16
                     stsh(pbh + 2u * (r * kL1Pitch + e0), w0);
-                    stsh(pbl + 2u * (r * kL1Pitch + e0), w0 >> 16);
+                    if (lo_on) stsh(pbl + 2u * (r * kL1Pitch + e0), w0 >> 16);
                     if (has1) {
                         const uint32_t w1 = ldsu(lut_s + 4u * u1[r]);
                         stsh(pbh + 2u * (r * kL1Pitch + e1), w1);
-                        stsh(pbl + 2u * (r * kL1Pitch + e1), w1 >> 16);
+                        if (lo_on) stsh(pbl + 2u * (r * kL1Pitch + e1), w1 >> 16);
                     }
                 }
             } else {
@@ -431,12 +435,15 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     for (int r = bt / nj; r < kBM; r += rstep) {
                         const int ty = r >> 4, tx = r & 15;
                         const uint32_t so = (uint32_t)((2 * ty + ky) * (2 * kL1Pitch) + 12 * tx + h8);
-                        uint4 hv, lv;
+                        uint4 hv;
                         hv.x = ldsu(pbh + so); hv.y = ldsu(pbh + so + 4); hv.z = ldsu(pbh + so + 8); hv.w = ldsu(pbh + so + 12);
-                        lv.x = ldsu(pbl + so); lv.y = ldsu(pbl + so + 4); lv.z = ldsu(pbl + so + 8); lv.w = ldsu(pbl + so + 12);
                         const uint32_t o = (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4));
                         stsu4(ah + o, hv);
-                        if (p.split == 2) stsu4(al + o, lv);
+                        if (lo_on) {
+                            uint4 lv;
+                            lv.x = ldsu(pbl + so); lv.y = ldsu(pbl + so + 4); lv.z = ldsu(pbl + so + 8); lv.w = ldsu(pbl + so + 12);
+                            stsu4(al + o, lv);
+                        }
                     }
                 }
                 fence_proxy_async_smem();                             // generic writes -> tensor core
@@ -696,7 +703,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         for (int kk = 0; kk < kBK / 16; ++kk) {
                             // +32 bytes per 16-element K step inside the 128-byte swizzle row
                             mma_ss(d, ah + 2 * kk, bd + 2 * kk, (k | kk) != 0);
-                            if (p.split == 2) mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
+                            if (p.split == 2 && !p.l1_int) mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
                         }
                         commit(&empty_bar[stage]);
                     }
@@ -834,6 +841,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                 for (int j = 0; j < GC; ++j) {
                     uint32_t hi[8], lo[8];
+                    if (p.l1_int) {
+                        // fused g_a L1 on u8 samples: acc = sum W * u exactly; x = acc / 255 + b
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) x[j][i] *= (1.0f / 255.0f);
+                    }
 #pragma unroll
                     for (int i4 = 0; i4 < 4; ++i4) {
                         const float4 bb = lds4(s_bias + g * G + j * 16 + 4 * i4);
