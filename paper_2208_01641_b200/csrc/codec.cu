@@ -171,6 +171,7 @@ struct lic_codec {
     int pdl_enabled = 1;           // programmatic dependent launch of the GEMM engine (env LIC_PDL=0 disables)
     int small_bn = 0;              // N tile of the h_a / h_s layers (env LIC_SMALL_BN=64|128; 0 = whole Cout: measured no gain)
     int s2halo_enabled = 1;        // 5x5/s2 convs in parity-sub-grid halo mode (env LIC_S2HALO=0: per-tap tiles)
+    int a_hi_only_enabled = 1;     // g_s L1 skips the zero lo plane of the integer y-hat (env LIC_YHAT_HI=0: off)
     int l1_int_enabled = 1;        // u8 frames: integer samples into g_a L1, one MMA pass (env LIC_L1_INT=0: off)
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
@@ -761,6 +762,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_PDL")) c->pdl_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_GS4_GATHER")) c->gs4_gather = (e[0] != '0');
     if (const char* e = std::getenv("LIC_L1_INT")) c->l1_int_enabled = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_SMALL_BN")) c->small_bn = atoi(e) == 64 || atoi(e) == 128 ? atoi(e) : 0;
     if (const char* e = std::getenv("LIC_NO_WRES")) c->wres_enabled = (e[0] != '1');
@@ -1122,7 +1124,13 @@ static lic_status decode_impl(lic_codec* c, const int8_t* y_sym, uint32_t batch,
     OutBuf of = route_frames_out(frames, c->d_frames, fbytes);
     CK(launch_sym_ingest(yd, c->kind == 0 ? c->mu_y : nullptr, B, c->M, Hy, Wy, c->bufY, c->planeY, c->split, st));
     ++c->launches;
-    for (int id : {GS1, GS2, GS3})
+    {
+        // hyperprior y-hat = the integer symbols: exact in fp16, its lo plane is zero
+        ConvParams p1 = c->layers[GS1].prm;
+        p1.a_hi_only = c->kind == 1 && c->a_hi_only_enabled;
+        if ((r = run_layer(c, c->layers[GS1], p1, B, st))) return r;
+    }
+    for (int id : {GS2, GS3})
         if ((r = run_layer(c, c->layers[id], c->layers[id].prm, B, st))) return r;
     ConvParams p = c->layers[GS4].prm;
     p.out_f32 = u8 ? nullptr : (float*)of.dev;

@@ -544,7 +544,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (p.pdl) griddep_wait();
             int hs = 0;
             uint32_t hphase = 0;
-            const uint32_t hbytes = (uint32_t)p.halo_w * (p.Ht + 2) * 128 * p.split;
+            const bool hlo = p.split == 2 && !p.a_hi_only;      // load the lo plane
+            const uint32_t hbytes = (uint32_t)p.halo_w * (p.Ht + 2) * 128 * (hlo ? 2 : 1);
             for (int t = cid; t < p.total_tiles; t += ncl) {
                 TileCoord tc = decode_tile(p, t, rank);
                 for (int c = 0; c < p.kchunks; ++c)
@@ -558,7 +559,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     if (elect_one()) {
                         expect(&hfull_bar[hs], hbytes);
                         ld5(hb, &mapA, &hfull_bar[hs], c * kBK, hx, hy, tc.b, 0);
-                        if (p.split == 2) ld5(hb + p.halo_plane_bytes, &mapA, &hfull_bar[hs], c * kBK, hx, hy, tc.b, 1);
+                        if (hlo) ld5(hb + p.halo_plane_bytes, &mapA, &hfull_bar[hs], c * kBK, hx, hy, tc.b, 1);
                     }
                     __syncwarp();
                     if (++hs == p.halo_slots) { hs = 0; hphase ^= 1; }
@@ -671,7 +672,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                                     for (int kk = 0; kk < kBK / 16; ++kk) {
                                         mma_ss(d, ah + 2 * kk, bd + 2 * kk, (c | gi | ti | u | kk) != 0);
-                                        if (p.split == 2) mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
+                                        if (p.split == 2 && !p.a_hi_only) mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
                                     }
                                 }
                             }

@@ -96,6 +96,8 @@ struct ConvParams {
     int fuse_l1;
     const void* frame;                // u8 [B][H][W][3] or f32 [B][3][H][W] (device)
     int fr_u8, fr_H, fr_W, fr_top, fr_left;   // frame size and its offset in the padded grid
+    int a_hi_only;                    // the input activation is exact in fp16 (lo plane zero: the hyperprior's
+                                      // integer y-hat into g_s L1): no lo loads, no lo MMAs
     int l1_int;                       // u8 frames: A holds the integer sample (exact in fp16) -- one MMA pass,
                                       // no lo plane -- and the epilogue scales the sum by 1/255
     uint32_t off_patch;               // split patch [2][hi, lo][19][112] fp16
