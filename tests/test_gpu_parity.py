@@ -294,3 +294,30 @@ def test_f16_mode_close_to_oracle(lic, hyper):
         assert ey <= 1e-2 and ex <= 1e-2
         assert flips[0] <= 1 and flips[1] <= 1e-3
     c.close()
+
+
+def test_odd_width_u8_frames(lic):
+    """Frame width not a multiple of 4 (the fused L1 builder's per-sample u8 path, not the
+    cp.async one) and not of 64 (centred padding): encode + decode against the oracle."""
+    Hh, Ww = 130, 198
+    spec = ModelSpec(kind=1, N=128, M=192)
+    w = generate_weights(spec, seed=0)
+    fr = synth_frames_u8(1, Hh, Ww, seed=17)
+    x = u8_to_f32_chw(fr)
+    c = lic.Codec(write_licw(spec, w), Hh, Ww, max_batch=1)
+    ys = np.empty((1,) + c.y_shape, np.int8)
+    yi = np.empty((1,) + c.y_shape, np.uint8)
+    zs = np.empty((1,) + c.z_shape, np.int8)
+    c.set_debug(True)
+    c.encode(np.ascontiguousarray(fr), ys, yi, zs, u8=True)
+    y, _, _ = c.debug_latents(1)
+    xp, crop = O.pad_chw(x[0], hyper=True)
+    p = O.encode_planes(xp, w, True, 32)
+    check_float(y[0], p["y"], what="odd-width y")
+    check_symbols(ys[0], p["y_sym"], p["y"], what="odd-width y_sym")
+    out = np.empty((1, Hh, Ww, 3), np.uint8)
+    c.decode(p["y_sym"][None], out, u8=True)
+    ref = O.decode_frame(p["y_sym"], w, True, crop, Hh, Ww)
+    ref8 = np.floor(np.moveaxis(ref, 0, -1).astype(np.float64) * 255 + 0.5)
+    assert np.max(np.abs(out[0].astype(np.int32) - ref8)) <= 1
+    c.close()
