@@ -489,7 +489,11 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.halo_plane_bytes = hpb;
         P.halo_w = halo_w;
         // several taps per weight stage (one wait per 8 * tps MMAs; env LIC_TPS=1..4)
-        P.tps = 2;
+        // (measured per layer: 3 for the many-tile parity-halo convs of g_a, 2 elsewhere)
+        {
+            const int lid = (int)(&Ly - c->layers);
+            P.tps = (P.sub4 && lid >= GA2 && lid <= GA4) ? 3 : 2;
+        }
         if (const char* e = std::getenv("LIC_TPS")) P.tps = std::max(1, std::min(kMaxTps, atoi(e)));
         P.stage_bytes = b_bytes * (uint32_t)P.tps;
         // halo ring depth: env LIC_HALO_SLOTS (2..4, default 2: a halo chunk is reused by all
