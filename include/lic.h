@@ -159,8 +159,8 @@ lic_status lic_profile(lic_codec* codec, int on);
 lic_status lic_profile_layers(lic_codec* codec, uint32_t mask);
 lic_status lic_profile_read(lic_codec* codec, int layer_id, double* ms, uint64_t* launches);
 /* Test-only timeline: while on, launches of `layer_id` record clock64 events of CTA 0 per
- * tile (8 per tile: MMA start/end, norm issue, epilogue start / x^2 written / norm ready /
- * end, producer start); lic_trace_read copies up to n values (256 tiles x 16 slots). */
+ * tile (MMA start/end, norm issue, epilogue start / x^2 written / norm ready / end, producer
+ * start, builder / MMA-issue points); lic_trace_read copies up to n values (256 tiles x 24 slots). */
 lic_status lic_trace(lic_codec* codec, int layer_id, int on);
 lic_status lic_trace_read(lic_codec* codec, uint64_t* out, size_t n);
 /* Total kernels this codec has launched (GEMM engine + ingest kernels). */

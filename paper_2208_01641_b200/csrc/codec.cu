@@ -173,6 +173,7 @@ struct lic_codec {
     int s2halo_enabled = 1;        // 5x5/s2 convs in parity-sub-grid halo mode (env LIC_S2HALO=0: per-tap tiles)
     int a_hi_only_enabled = 1;     // g_s L1 skips the zero lo plane of the integer y-hat (env LIC_YHAT_HI=0: off)
     int l1_int_enabled = 1;        // u8 frames: integer samples into g_a L1, one MMA pass (env LIC_L1_INT=0: off)
+    int l1_conv_enabled = 1;       // ... converted arithmetically, 8 per item, no LUT (env LIC_L1_CONV=0: LUT)
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
@@ -636,7 +637,7 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
     if (c->trace_layer == lid && c->d_trace) {
         P.trace = c->d_trace;
         if (const char* e = std::getenv("LIC_DBG_NOSTORE")) P.dbg_nostore = atoi(e);
-        CK(cudaMemsetAsync(c->d_trace, 0, 256 * 16 * 8, st));
+        CK(cudaMemsetAsync(c->d_trace, 0, 256 * kTraceEvents * 8, st));
     }
     const bool prof = c->profiling && ((c->prof_mask >> lid) & 1u);
     if (prof) {
@@ -778,6 +779,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_PDL")) c->pdl_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_GS4_GATHER")) c->gs4_gather = (e[0] != '0');
     if (const char* e = std::getenv("LIC_L1_INT")) c->l1_int_enabled = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_SMALL_BN")) c->small_bn = atoi(e) == 64 || atoi(e) == 128 ? atoi(e) : 0;
@@ -1061,7 +1063,7 @@ static lic_status encode_impl(lic_codec* c, const void* frames, int hwc, uint32_
     {
         ConvParams p = c->layers[GA1].prm;             // fused im2col: reads the frames directly
         p.frame = fdev; p.fr_u8 = hwc; p.fr_H = c->H; p.fr_W = c->W; p.fr_top = c->top; p.fr_left = c->left;
-        p.l1_int = hwc && c->l1_int_enabled;
+        p.l1_int = (hwc && c->l1_int_enabled) ? (c->l1_conv_enabled ? 2 : 1) : 0;
         if ((r = run_layer(c, c->layers[GA1], p, B, st))) return r;
     }
     for (int id : {GA2, GA3})
@@ -1315,7 +1317,7 @@ extern "C" lic_status lic_set_zero_copy(lic_codec* c, int on) {
 extern "C" lic_status lic_trace(lic_codec* c, int layer_id, int on) {
     if (!c || layer_id < 0 || layer_id >= NLAYER) return LIC_EINVAL;
     if (on && !c->d_trace) {
-        lic_status r = dalloc(c, &c->d_trace, 256 * 16 * 8);
+        lic_status r = dalloc(c, &c->d_trace, 256 * kTraceEvents * 8);
         if (r) return r;
     }
     c->trace_layer = on ? layer_id : -1;
@@ -1326,6 +1328,6 @@ extern "C" lic_status lic_trace_read(lic_codec* c, uint64_t* out, size_t n) {
     if (!c || !out || !c->d_trace) return LIC_EINVAL;
     cudaSetDevice(c->device);
     CK(cudaStreamSynchronize(c->stream));
-    CK(cudaMemcpy(out, c->d_trace, std::min<size_t>(n, 256 * 16) * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, c->d_trace, std::min<size_t>(n, 256 * kTraceEvents) * 8, cudaMemcpyDeviceToHost));
     return LIC_OK;
 }

@@ -91,6 +91,24 @@ __device__ __forceinline__ uint32_t ldsu(uint32_t addr) {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ uint2 ldsu2(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void stsu(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void stsu2(uint32_t addr, uint32_t a, uint32_t b) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" :: "r"(addr), "r"(a), "r"(b) : "memory");
+}
+// bytes 2i, 2i+1 of w (i = sel: 0x4140 low pair, 0x4342 high pair) -> f16x2 of the integers
+// (0x6400 | u is 1024 + u exactly; subtracting 1024 is exact)
+__device__ __forceinline__ uint32_t u8pair_to_h2(uint32_t w, uint32_t sel) {
+    uint32_t h = __byte_perm(w, 0x64646464u, sel), r;
+    asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(h), "r"(0x64006400u));
+    return r;
+}
 __device__ __forceinline__ uint32_t ldsb(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -161,12 +179,13 @@ __device__ __forceinline__ int round_clamp(float v, int L, int& sat) {
 }
 
 // test-only timeline: event e of the it-th tile of CTA 0 (kTraceEv slots per tile)
-constexpr int kTraceEv = 16;
+constexpr int kTraceEv = kTraceEvents;
 constexpr int kTraceTiles = 256;
 enum TraceEv { T_MMA_START = 0, T_MMA_END = 1, T_NORM_ISSUE = 2, T_EPI_START = 3, T_EPI_XSQ = 4,
                T_EPI_NORM = 5, T_EPI_END = 6, T_PROD_START = 7,
                T_B_PATCH = 8, T_B_C0_READY = 9, T_B_C0_DONE = 10, T_B_C1_READY = 11, T_B_C1_DONE = 12,
-               T_MMA_K0 = 13, T_MMA_KL = 14, T_PEER_B_DONE = 15 };
+               T_MMA_K0 = 13, T_MMA_KL = 14, T_PEER_B_DONE = 15, T_B_RAW = 16,
+               T_EPI_P2 = 17, T_EPI_ACQ = 18, T_EPI_STAGED = 19 };
 #define LIC_TRACE(it, ev)                                                                         \
     do {                                                                                          \
         if (p.trace && blockIdx.x == 0 && (it) < kTraceTiles)                                     \
@@ -321,6 +340,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         // one tile ahead of the build; otherwise per-sample loads.
         const bool fast = p.fr_u8 && (p.fr_W & 3) == 0;
         const bool lo_on = p.split == 2 && !p.l1_int;     // the lo planes of patch and A tiles
+        const bool int_fast = fast && p.l1_int == 2;            // integer samples, no LUT, shifted copy
         auto raw_issue = [&](int tt, int buf) {
             const TileCoord tn = decode_tile(p, tt, rank);
             const uint8_t* fr = reinterpret_cast<const uint8_t*>(p.frame);
@@ -351,9 +371,33 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             // a thread owns patch columns e0 = bt and e1 = bt + 96 (< 105 for bt < 9).
             const int e0 = bt, e1 = bt + kL1Builders;
             const bool has1 = e1 < kL1PW;
-            if (fast) {
+            if (int_fast) {
+                // integer samples (l1_int): u8 -> f16 arithmetically, 8 values per item (3 raw
+                // words -> one 16-byte store); the lo plane holds a copy shifted by 4 bytes so
+                // that every K-row segment below is two 8-byte-aligned loads
                 cp_async_wait_all();
                 named_bar_sync(4, kL1Builders);                          // raw[it & 1] complete
+                if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_RAW);
+                const uint32_t rw = raw_s + (uint32_t)(it & 1) * kL1RawBytes;
+                const uint32_t sel = 0x3210u + (uint32_t)((3 * ix0) & 3) * 0x1111u;
+                for (int q = bt; q < kL1PH * 14; q += kL1Builders) {
+                    const int r = q / 14, m = q - 14 * r;
+                    const uint32_t src = rw + (uint32_t)(r * (4 * kL1RawWords) + 8 * m);
+                    const uint2 w01 = ldsu2(src);
+                    const uint32_t w2 = ldsu(src + 8);
+                    const uint32_t b0 = __byte_perm(w01.x, w01.y, sel), b1 = __byte_perm(w01.y, w2, sel);
+                    const uint32_t h0 = u8pair_to_h2(b0, 0x4140u), h1 = u8pair_to_h2(b0, 0x4342u);
+                    const uint32_t h2 = u8pair_to_h2(b1, 0x4140u), h3 = u8pair_to_h2(b1, 0x4342u);
+                    const uint32_t d = (uint32_t)(r * (2 * kL1Pitch) + 16 * m);
+                    stsu4(pbh + d, make_uint4(h0, h1, h2, h3));
+                    stsu(pbl + d + 4, h0);
+                    stsu2(pbl + d + 8, h1, h2);
+                    if (m < 13) stsu(pbl + d + 16, h3);                    // (values 110, 111: unused)
+                }
+            } else if (fast) {
+                cp_async_wait_all();
+                named_bar_sync(4, kL1Builders);                          // raw[it & 1] complete
+                if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_RAW);
                 const uint32_t rb = raw_s + (uint32_t)(it & 1) * kL1RawBytes + (uint32_t)((3 * ix0) & 3);
 #pragma unroll 4
                 for (int r = 0; r < kL1PH; ++r) {
@@ -435,9 +479,16 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     for (int r = bt / nj; r < kBM; r += rstep) {
                         const int ty = r >> 4, tx = r & 15;
                         const uint32_t so = (uint32_t)((2 * ty + ky) * (2 * kL1Pitch) + 12 * tx + h8);
+                        const uint32_t o = (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4));
+                        if (int_fast) {
+                            // odd tx: the segment is 4 mod 8 -- read it from the shifted copy
+                            const uint32_t sa = (tx & 1) ? pbl + so + 4 : pbh + so;
+                            const uint2 v0 = ldsu2(sa), v1 = ldsu2(sa + 8);
+                            stsu4(ah + o, make_uint4(v0.x, v0.y, v1.x, v1.y));
+                            continue;
+                        }
                         uint4 hv;
                         hv.x = ldsu(pbh + so); hv.y = ldsu(pbh + so + 4); hv.z = ldsu(pbh + so + 8); hv.w = ldsu(pbh + so + 12);
-                        const uint32_t o = (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4));
                         stsu4(ah + o, hv);
                         if (lo_on) {
                             uint4 lv;
@@ -832,11 +883,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if constexpr (kGdn) {
                 constexpr int G = 16 * GC;                   // channels of this group
                 float x[GC][16];
+                __syncwarp();
 #pragma unroll
-                for (int j = 0; j < GC; ++j) {
-                    __syncwarp();
-                    tmem_ld16(taddr + g * G + j * 16, x[j]);
-                }
+                for (int j = 0; j + 1 < GC; j += 2) tmem_ld32(taddr + g * G + j * 16, x[j]);
+                if constexpr (GC & 1) tmem_ld16(taddr + g * G + (GC - 1) * 16, x[GC - 1]);
                 // x^2 (hi, lo) packed into this group's own accumulator columns:
                 // hi of channel g*G + k at column g*G + k/2, lo at g*G + G/2 + k/2
 #pragma unroll

@@ -25,6 +25,7 @@ enum EpKind : int {
 
 constexpr int kMaxTaps = 32;
 constexpr int kMaxTps = 4;      // halo mode: at most 4 taps per weight stage
+constexpr int kTraceEvents = 24; // test-only per-tile timeline slots (lic_trace_read: 256 tiles x 24)
 constexpr int kBM = 128;        // pixels per tile (UMMA M)
 constexpr int kBK = 64;         // channels per K chunk (one 128-byte swizzle row of fp16)
 
@@ -99,7 +100,8 @@ struct ConvParams {
     int a_hi_only;                    // the input activation is exact in fp16 (lo plane zero: the hyperprior's
                                       // integer y-hat into g_s L1): no lo loads, no lo MMAs
     int l1_int;                       // u8 frames: A holds the integer sample (exact in fp16) -- one MMA pass,
-                                      // no lo plane -- and the epilogue scales the sum by 1/255
+                                      // no lo plane -- and the epilogue scales the sum by 1/255; 2: the
+                                      // builders convert u8 -> f16 arithmetically (no LUT)
     uint32_t off_patch;               // split patch [2][hi, lo][19][112] fp16
     uint32_t off_lut;                 // u8 LUT [257] (hi | lo << 16; entry 256 = 0)
     uint32_t off_raw;                 // raw u8 patch [2][19][112] (cp.async, u8 frames)

@@ -352,9 +352,9 @@ class Codec:
         self._chk(_L.lic_trace(self._h, lid, int(on)), "lic_trace")
 
     def trace_read(self):
-        out = np.zeros(256 * 16, np.uint64)
+        out = np.zeros(256 * 24, np.uint64)
         self._chk(_L.lic_trace_read(self._h, _ptr(out), out.size), "lic_trace_read")
-        return out.reshape(256, 16)
+        return out.reshape(256, 24)
 
     def launch_count(self):
         n = ctypes.c_uint64()
