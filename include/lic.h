@@ -260,6 +260,37 @@ lic_status lic_rans_encode_slabs(const lic_rans_tables* t, const int8_t* sym, co
 lic_status lic_rans_decode_slabs(const lic_rans_tables* t, const uint8_t* in, size_t len, const uint8_t* row,
                                  lic_shape plane, uint32_t K, int8_t* sym_out);
 
+/* ---------------------------------------------------------------- rans64 + bypass escape
+ * the coder the paper's implementations link ("simply integrate
+ * the CompressAI entropy coder [8]") -- 64-bit rANS (L = 2^31, 32-bit words,
+ * precision 16) with escape coding of values outside a table's support, R23.
+ * Host only, reentrant.  Tables: n_cdfs rows of `stride` uint32 (row r valid on
+ * [0, sizes[r]), c[0] = 0, c[sizes[r]-1] = 65536, strictly increasing, 3 <= sizes[r] <=
+ * stride); symbol value s of row r codes v = s - offsets[r]; v outside [0, sizes[r]-2) is
+ * sent as the escape (entry sizes[r]-2) plus its 4-bit "bypass" chunks, so every int32 is
+ * codable.  Stream: little-endian u32 words, final state (low, high) first. */
+
+/* Quantised CDF of pmf[0..n) (the last entry is the escape's tail mass): n + 1 entries into
+ * cdf; each frequency >= 1, total 65536.  LIC_EINVAL: negative / non-finite / all-zero pmf. */
+lic_status lic_cdf_quantize(const float* pmf, uint32_t n, uint32_t* cdf);
+/* Gaussian tables for scales[0..n) with total tail mass `tail_mass` (CompressAI's
+ * GaussianConditional construction, fp64): row r covers |k| <= center_r = ceil(scale_r *
+ * m), Phi(-m) = tail_mass / 2, offsets[r] = -center_r, sizes[r] = 2 center_r + 3.
+ * LIC_ENOSPACE if a row needs more than `stride` entries. */
+lic_status lic_cdf64_gaussian(const float* scales, uint32_t n, double tail_mass, uint32_t* cdfs,
+                              uint32_t stride, int32_t* sizes, int32_t* offsets);
+/* Encode sym[0..n) with rows idx[0..n) into out (capacity cap; written length in *out_len,
+ * a multiple of 4).  LIC_EINVAL: bad table / row index; LIC_ENOSPACE: cap too small
+ * (8 + 8n bytes always suffice). */
+lic_status lic_rans64_encode(const int32_t* sym, const int32_t* idx, size_t n, const uint32_t* cdfs,
+                             uint32_t n_cdfs, uint32_t stride, const int32_t* sizes, const int32_t* offsets,
+                             uint8_t* out, size_t cap, size_t* out_len);
+/* Inverse of lic_rans64_encode.  LIC_ECORRUPT if the words run out, an escape is longer than
+ * 9 chunks or its value leaves int32, or the final state is not 2^31 with every word read. */
+lic_status lic_rans64_decode(const uint8_t* in, size_t len, const int32_t* idx, size_t n, const uint32_t* cdfs,
+                             uint32_t n_cdfs, uint32_t stride, const int32_t* sizes, const int32_t* offsets,
+                             int32_t* sym_out);
+
 /* Library version string. */
 const char* lic_version(void);
 

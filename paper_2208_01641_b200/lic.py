@@ -111,6 +111,10 @@ _L.lic_rans_encode_fast.argtypes = [_P, _P, _P, Shape, _P, _sz, ctypes.POINTER(_
 _L.lic_rans_decode_fast.argtypes = [_P, _P, _sz, _P, Shape, _P]
 _L.lic_rans_encode_slabs.argtypes = [_P, _P, _P, Shape, _u32, _P, _sz, ctypes.POINTER(_sz)]
 _L.lic_rans_decode_slabs.argtypes = [_P, _P, _sz, _P, Shape, _u32, _P]
+_L.lic_cdf_quantize.argtypes = [_P, _u32, _P]
+_L.lic_cdf64_gaussian.argtypes = [_P, _u32, ctypes.c_double, _P, _u32, _P, _P]
+_L.lic_rans64_encode.argtypes = [_P, _P, _sz, _P, _u32, _u32, _P, _P, _P, _sz, ctypes.POINTER(_sz)]
+_L.lic_rans64_decode.argtypes = [_P, _sz, _P, _sz, _P, _u32, _u32, _P, _P, _P]
 
 EXPORTED = [n for n in dir(_L) if n.startswith("lic_")]
 
@@ -196,6 +200,69 @@ def rans_decode(data, shape, cdf, rows=None, sym_min=None, out=None):
     if st:
         raise LicError(st, "rans_decode")
     return out
+
+
+def cdf_quantize(pmf):
+    """lic_cdf_quantize: quantised CDF (len(pmf) + 1 entries) of a pmf whose last entry is
+    the escape's tail mass."""
+    p = np.ascontiguousarray(pmf, np.float32)
+    out = np.empty(p.size + 1, np.uint32)
+    st = _L.lic_cdf_quantize(_ptr(p), p.size, _ptr(out))
+    if st:
+        raise LicError(st, "cdf_quantize")
+    return out
+
+
+class Rans64Tables:
+    """Tables of the rans64 + bypass coder (lic_rans64_*, R23): cdfs [n, stride]
+    uint32, sizes [n] int32, offsets [n] int32."""
+
+    def __init__(self, cdfs, sizes, offsets):
+        self.cdfs = np.ascontiguousarray(cdfs, np.uint32)
+        self.sizes = np.ascontiguousarray(sizes, np.int32)
+        self.offsets = np.ascontiguousarray(offsets, np.int32)
+        assert self.cdfs.ndim == 2 and self.sizes.shape == self.offsets.shape == (self.cdfs.shape[0],)
+
+    @classmethod
+    def gaussian(cls, scales, tail_mass=1e-9, stride=None):
+        """lic_cdf64_gaussian: one row per scale (CompressAI's GaussianConditional tables)."""
+        s = np.ascontiguousarray(scales, np.float32)
+        if stride is None:
+            stride = 2 * int(np.ceil(float(s.max()) * 6.2)) + 8
+        cdfs = np.zeros((s.size, stride), np.uint32)
+        sizes = np.zeros(s.size, np.int32)
+        offs = np.zeros(s.size, np.int32)
+        st = _L.lic_cdf64_gaussian(_ptr(s), s.size, float(tail_mass), _ptr(cdfs), stride, _ptr(sizes), _ptr(offs))
+        if st:
+            raise LicError(st, "cdf64_gaussian")
+        return cls(cdfs, sizes, offs)
+
+    def encode(self, sym, idx):
+        sym = np.ascontiguousarray(sym, np.int32).ravel()
+        idx = np.ascontiguousarray(idx, np.int32).ravel()
+        if sym.size != idx.size:
+            raise ValueError("sym / idx sizes differ")
+        cap = 8 + 8 * sym.size
+        out = np.empty(cap, np.uint8)
+        n = _sz(0)
+        st = _L.lic_rans64_encode(_ptr(sym), _ptr(idx), sym.size, _ptr(self.cdfs), self.cdfs.shape[0],
+                                  self.cdfs.shape[1], _ptr(self.sizes), _ptr(self.offsets), _ptr(out), cap,
+                                  ctypes.byref(n))
+        if st:
+            raise LicError(st, "rans64_encode")
+        return out[: n.value].tobytes()
+
+    def decode(self, data, idx):
+        idx = np.ascontiguousarray(idx, np.int32).ravel()
+        buf = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)
+        out = np.empty(idx.size, np.int32)
+        st = _L.lic_rans64_decode(_ptr(buf), len(data), _ptr(idx), idx.size, _ptr(self.cdfs), self.cdfs.shape[0],
+                                  self.cdfs.shape[1], _ptr(self.sizes), _ptr(self.offsets), _ptr(out))
+        if st == LIC_ECORRUPT:
+            raise CorruptStream(st, "rans64_decode")
+        if st:
+            raise LicError(st, "rans64_decode")
+        return out
 
 
 class RansTables:
