@@ -116,7 +116,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// bar.sync is .aligned: every lane of a warp must execute it together, so reconverge the
+// warp first (callers arrive from lane-divergent code: single-lane waits, ragged loops)
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    __syncwarp();
     asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
 }
 
