@@ -434,7 +434,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     // shared memory plan: stage ring | halo ring (halo mode) | gamma (GDN) | mbarriers | constants
     const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)(P.BN / P.cg) * 64 * 2;
     const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
-    const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64) * 4;
+    const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64 + kMaxTaps) * 4;   // + halo tap offsets
     const uint32_t budget = 227u * 1024u;
     // TMA-store epilogue: 4 lane quadrants x 8 KB block slots (1 or 2 slots), when the layer writes an activation and the
     // pipeline keeps >= 3 stages with it (env LIC_TMA_OUT=0 disables)

@@ -231,6 +231,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     float* s_beta = s_bias + p.BN * p.n_ntiles;                     // [cout_pad]
     float* s_mu = s_beta + p.BN * p.n_ntiles;                       // [cout_pad]
     float* s_tab = s_mu + p.BN * p.n_ntiles;                        // [64]
+    uint32_t* s_tapoff = reinterpret_cast<uint32_t*>(s_tab + 64);   // [kMaxTaps] halo window offsets
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -273,6 +274,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             s_mu[i] = (in && p.mu) ? p.mu[i] : 0.0f;
         }
         for (int i = threadIdx.x - 128; i < 64; i += 32 * kEpiWarps) s_tab[i] = p.table ? p.table[i] : 0.0f;
+        // halo mode: tap t's window starts at halo row (dy+1)*(Wt+2) + dx+1, i.e. this many
+        // 16-byte descriptor units past the halo slot
+        for (int i = threadIdx.x - 128; i < kMaxTaps; i += 32 * kEpiWarps)
+            s_tapoff[i] = (uint32_t)(((p.tap_dy[i] + 1) * p.halo_w + p.tap_dx[i] + 1) * 8);
     }
     if (p.fuse_l1) {
         // zero the A stages (K columns >= 80 are never rewritten) and both patch buffers (the
@@ -689,8 +694,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (lane == 0) LIC_TRACE(it, T_MMA_START);
             const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
             if (p.halo) {
-                const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
                 const uint32_t sbo = (uint32_t)p.halo_w * 128;
+                const bool lo_mma = p.split == 2 && !p.a_hi_only;
                 for (int c = 0; c < p.kchunks; ++c)
                   for (int gi = 0; gi < (p.sub4 ? 4 : 1); ++gi) {
                     const int nt = p.sub4 ? p.ntaps[gi] : p.ntaps[tc.ph], t0 = p.sub4 ? p.tap0[gi] : p.tap0[tc.ph];
@@ -698,6 +703,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     tc_fence_after();
                     if (lane == 0 && c == 0 && gi == 0) LIC_TRACE(it, T_MMA_K0);
                     const uint32_t hb = smem_u32(smem + p.off_halo + hs * (p.split * p.halo_plane_bytes));
+                    // descriptors of the halo slot (hi, lo planes); a tap's window adds its row
+                    // offset (s_tapoff: 16-byte units, no carry out of the 14-bit address field)
+                    const uint64_t ahb = sdesc_sw128_sbo(hb, sbo);
+                    const uint64_t alb = ahb + (p.halo_plane_bytes >> 4);
                     // p.tps taps per weight stage: one barrier wait / fence / commit per 8 * tps MMAs
                     // (the issue loop, not the tensor pipe, is what waits between groups)
                     const int tps = p.wres ? 1 : p.tps;
@@ -711,19 +720,36 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             tc_fence_after();
                             bsm = smem_u32(smem + stage * p.stage_bytes);
                         }
-                        // window of tap ti + u: halo row (dy+1)*(Wt+2) + (dx+1), 8-row groups every Wt+2 rows
+                        const uint64_t bdb = sdesc_sw128(bsm);
+                        uint32_t toff[kMaxTps];
+#pragma unroll
+                        for (int u = 0; u < kMaxTps; ++u) toff[u] = u < ntp ? s_tapoff[t0 + ti + u] : 0u;
                         if (elect_one()) {
+                            const uint32_t acc0 = (c | gi | ti) != 0;
+                            // two copies of the issue loop (hi + lo planes / hi only): no predicated
+                            // MMAs, so the descriptors stay in uniform registers
+                            if (lo_mma) {
 #pragma unroll
-                            for (int u = 0; u < kMaxTps; ++u) {
-                                if (u < ntp) {
-                                    const uint32_t r0 = (uint32_t)((p.tap_dy[t0 + ti + u] + 1) * p.halo_w + p.tap_dx[t0 + ti + u] + 1);
-                                    const uint64_t ah = sdesc_sw128_sbo(hb + r0 * 128, sbo);
-                                    const uint64_t al = sdesc_sw128_sbo(hb + p.halo_plane_bytes + r0 * 128, sbo);
-                                    const uint64_t bd = sdesc_sw128(bsm + (uint32_t)u * b_bytes);
+                                for (int u = 0; u < kMaxTps; ++u) {
+                                    if (u < ntp) {
+                                        const uint64_t ah = ahb + toff[u], al = alb + toff[u];
+                                        const uint64_t bd = bdb + (uint64_t)(u * (b_bytes >> 4));
 #pragma unroll
-                                    for (int kk = 0; kk < kBK / 16; ++kk) {
-                                        mma_ss(d, ah + 2 * kk, bd + 2 * kk, (c | gi | ti | u | kk) != 0);
-                                        if (p.split == 2 && !p.a_hi_only) mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
+                                        for (int kk = 0; kk < kBK / 16; ++kk) {
+                                            mma_ss(d, ah + 2 * kk, bd + 2 * kk, (u | kk) ? 1u : acc0);
+                                            mma_ss(d, al + 2 * kk, bd + 2 * kk, 1u);
+                                        }
+                                    }
+                                }
+                            } else {
+#pragma unroll
+                                for (int u = 0; u < kMaxTps; ++u) {
+                                    if (u < ntp) {
+                                        const uint64_t ah = ahb + toff[u];
+                                        const uint64_t bd = bdb + (uint64_t)(u * (b_bytes >> 4));
+#pragma unroll
+                                        for (int kk = 0; kk < kBK / 16; ++kk)
+                                            mma_ss(d, ah + 2 * kk, bd + 2 * kk, (u | kk) ? 1u : acc0);
                                     }
                                 }
                             }
