@@ -185,7 +185,8 @@ enum TraceEv { T_MMA_START = 0, T_MMA_END = 1, T_NORM_ISSUE = 2, T_EPI_START = 3
                T_EPI_NORM = 5, T_EPI_END = 6, T_PROD_START = 7,
                T_B_PATCH = 8, T_B_C0_READY = 9, T_B_C0_DONE = 10, T_B_C1_READY = 11, T_B_C1_DONE = 12,
                T_MMA_K0 = 13, T_MMA_KL = 14, T_PEER_B_DONE = 15, T_B_RAW = 16,
-               T_EPI_P2 = 17, T_EPI_ACQ = 18, T_EPI_STAGED = 19 };
+               T_EPI_P2 = 17, T_EPI_ACQ = 18, T_EPI_STAGED = 19,
+               T_W_HALO = 20, T_W_B = 21 };
 #define LIC_TRACE(it, ev)                                                                         \
     do {                                                                                          \
         if (p.trace && blockIdx.x == 0 && (it) < kTraceTiles)                                     \
@@ -693,13 +694,16 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             tc_fence_after();
             if (lane == 0) LIC_TRACE(it, T_MMA_START);
             const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
+            long long w_halo = 0, w_b = 0;          // trace only: cycles waiting for operands
             if (p.halo) {
                 const uint32_t sbo = (uint32_t)p.halo_w * 128;
                 const bool lo_mma = p.split == 2 && !p.a_hi_only;
                 for (int c = 0; c < p.kchunks; ++c)
                   for (int gi = 0; gi < (p.sub4 ? 4 : 1); ++gi) {
                     const int nt = p.sub4 ? p.ntaps[gi] : p.ntaps[tc.ph], t0 = p.sub4 ? p.tap0[gi] : p.tap0[tc.ph];
+                    long long tw0 = p.trace ? clock64() : 0;
                     wait_poll(&hfull_bar[hs], hphase);
+                    if (p.trace) w_halo += clock64() - tw0;
                     tc_fence_after();
                     if (lane == 0 && c == 0 && gi == 0) LIC_TRACE(it, T_MMA_K0);
                     const uint32_t hb = smem_u32(smem + p.off_halo + hs * (p.split * p.halo_plane_bytes));
@@ -716,7 +720,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         if (p.wres) {
                             bsm = smem_u32(smem + p.off_wres + ((t0 + ti) * p.kchunks + c) * b_bytes);
                         } else {
+                            long long tw1 = p.trace ? clock64() : 0;
                             wait_poll(&full_bar[stage], phase);
+                            if (p.trace) w_b += clock64() - tw1;
                             tc_fence_after();
                             bsm = smem_u32(smem + stage * p.stage_bytes);
                         }
@@ -793,6 +799,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (elect_one()) commit(&tfull_bar[buf]);
             __syncwarp();
             if (lane == 0) LIC_TRACE(it, T_MMA_END);
+            if (lane == 0 && p.trace && blockIdx.x == 0 && it < kTraceTiles) {
+                p.trace[(size_t)it * kTraceEv + T_W_HALO] = (unsigned long long)w_halo;
+                p.trace[(size_t)it * kTraceEv + T_W_B] = (unsigned long long)w_b;
+            }
 
             if (kGdn) {
                 // the previous tile's norm must be issued before this one becomes pending

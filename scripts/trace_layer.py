@@ -36,7 +36,7 @@ c.trace(layer, True)
 step()
 t = c.trace_read().astype(np.int64)
 names = ["mma_s", "mma_e", "norm_i", "epi_s", "epi_x2", "epi_n", "epi_e", "prod_s"]
-bnames = ["b_patch", "b_c0_rdy", "b_c0_done", "b_c1_rdy", "b_c1_done", "mma_k0", "mma_kl", "peerB", "b_raw", "epi_p2", "epi_acq", "epi_stg"]
+bnames = ["b_patch", "b_c0_rdy", "b_c0_done", "b_c1_rdy", "b_c1_done", "mma_k0", "mma_kl", "peerB", "b_raw", "epi_p2", "epi_acq", "epi_stg", "w_halo", "w_b"]
 n = int((t[:, 0] > 0).sum())
 t0 = t[0, 0]
 fused = bool((t[:n, 8] > 0).any() or (t[:n, 13] > 0).any())
@@ -44,7 +44,7 @@ cols = names + (bnames if fused else [])
 print(f"{layer}: {n} tiles traced on CTA 0")
 print("tile " + " ".join(f"{x:>9s}" for x in cols) + "   mma_dur epi_dur  gap(mma_s[i]-mma_e[i-1])")
 for i in range(min(n, 40)):
-    row = [(v - t0) if v else -1 for v in t[i, :len(cols)]]
+    row = [(v if name.startswith("w_") else v - t0) if v else -1 for name, v in zip(cols, t[i, :len(cols)])]
     gap = t[i, 0] - t[i - 1, 1] if i else 0
     print(f"{i:4d} " + " ".join(f"{v:9d}" for v in row) + f"   {t[i,1]-t[i,0]:7d} {t[i,6]-t[i,3]:7d} {gap:7d}")
 per_tile = (t[n - 1, 6] - t[0, 0]) / max(n, 1)
