@@ -554,7 +554,13 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.off_ostage = (P.off_par + par_bytes + 1023) / 1024 * 1024;
     P.smem_bytes = (tma_out ? P.off_ostage + ostage_bytes : P.off_par + par_bytes) + 1024;
     // double-buffered staging when it fits without losing pipeline depth below 3 (halo: 2) stages
-    if (tma_out && P.smem_bytes + ostage_bytes <= budget) {
+    static const int ostage_max = [] {                     // env LIC_OSTAGE=1: single staging slot
+        const char* e = std::getenv("LIC_OSTAGE");
+        return (e && e[0] == '1') ? 1 : 2;
+    }();
+    if (ostage_max < 2) {
+        // keep the smem for the operand rings
+    } else if (tma_out && P.smem_bytes + ostage_bytes <= budget) {
         const bool keep = P.fuse_l1 || (P.halo ? (P.wres || P.stages >= 2) : P.stages >= 3);
         if (keep) { P.ostage_slots = 2; P.smem_bytes += ostage_bytes; }
     } else if (tma_out && P.halo && !P.wres && P.stage_bytes) {
