@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 
 # BASELINE.json configs (configs[2] = C3 is the default, headline workload; the others are
 # reported by DESIGN.md from `--config` runs on one GPU)
+CODERS = {"rans32": 0, "rans64": 1}
 CONFIGS = {
     "c2": dict(kind=0, N=128, M=192, H=512, W=768, B=1,
                workload="factorized-prior N=128 M=192, Kodak-shaped 768x512 frames, batch 1, random-init weights"),
@@ -220,6 +221,9 @@ def main():
     ap.add_argument("--inflight", type=int, default=8)
     ap.add_argument("--substreams", type=int, default=32,
                     help="y string as K channel-slab rANS substreams (DESIGN.md R21); 1 = one string")
+    ap.add_argument("--coder", default="rans32", choices=["rans32", "rans64"],
+                    help="host entropy coder: 32-bit rANS over +-L tables (with --substreams), or rans64 + "
+                         "bypass escape with Gaussian tables (DESIGN.md R23; one string per plane)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--serial", action="store_true", help="serial reference pipeline (no overlap)")
     ap.add_argument("--zero-copy", action="store_true", help="kernels touch pinned host planes in place")
@@ -259,7 +263,7 @@ def main():
                       precision=lic.PREC_F16 if args.precision == "f16" else lic.PREC_SPLIT)
     codec.set_zero_copy(args.zero_copy)
     pipe = lic.Pipeline(codec, coder_threads=threads, batch=B, inflight=args.inflight, u8=True,
-                        serial=args.serial, substreams=args.substreams)
+                        serial=args.serial, substreams=args.substreams, coder=CODERS[args.coder])
 
     # synthetic stream: 8 distinct frames per rank, looped (the paper loops one image)
     base = torch.from_numpy(synth_frames_u8(8, H, W, seed=1000 + rank))
@@ -366,7 +370,8 @@ def main():
                    "batch_per_gpu": B, "frames_per_gpu": nfr,
                    "coder_threads_per_gpu": threads, "inflight": args.inflight,
                    "cores_per_rank": len(bound) if bound else ncores,
-                   "y_substreams": args.substreams,
+                   "y_substreams": args.substreams if args.coder == "rans32" else 1,
+                   "entropy_coder": args.coder,
                    "l2": "inputs larger than L2 (activations ~0.36 GB per frame, frame set > 126 MB)",
                    "pipeline": "serial" if args.serial else "overlapped"},
         "latency_ms": {"p50": round(st["latency_p50_ms"], 3), "p95": round(st["latency_p95_ms"], 3),
@@ -391,7 +396,7 @@ def main():
     # for its first frames, ordered by global frame index on rank 0
     from paper_2208_01641_b200.dist import gather_bitstreams, stream_digest
     vp = lic.Pipeline(codec, coder_threads=threads, batch=B, inflight=2, u8=True, keep_bitstreams=True,
-                      substreams=args.substreams)
+                      substreams=args.substreams, coder=CODERS[args.coder])
     vst = vp.run(dev_in, dev_out, 2 * B)
     local = {rank + world * i: vp.bitstream(i) for i in range(2 * B)}
     vp.close()

@@ -175,6 +175,11 @@ lic_status lic_launch_count(const lic_codec* codec, uint64_t* n);
 lic_status lic_cdf(const lic_codec* codec, int which, const uint32_t** rows, uint32_t* n_rows,
                    uint32_t* row_len);
 
+/* The scales those tables are built from: which = 0 sigma_y (factorized, one per y channel),
+ * 1 sigma_z (hyperprior, one per z channel), 2 the 64-entry scale table (hyperprior y rows).
+ * Pointer valid while the codec lives.  LIC_EINVAL if the codec has no such table. */
+lic_status lic_sigmas(const lic_codec* codec, int which, const float** sigmas, uint32_t* n);
+
 /* Build one CDF row per sigma (zero-mean discretised Gaussian over [-L, L], tails folded,
  * 16-bit quantised, every frequency >= 1).  out: n x (2L+2) uint32. */
 lic_status lic_cdf_build(const float* sigmas, uint32_t n, uint32_t L, uint32_t* out);
@@ -212,6 +217,9 @@ typedef struct {
     int serial;               /* 1: no overlap between stages (reference) */
     int keep_bitstreams;      /* 1: keep every frame's strings for lic_pipeline_bitstream */
     uint32_t substreams;      /* y string as K channel-slab substreams (lic_rans_encode_slabs); 0 or 1: one string */
+    uint32_t coder;           /* 0: 32-bit rANS over the codec's +-L tables (above); 1: rans64 + bypass escape
+                                 (lic_rans64_*, R23) with Gaussian tables (tail 1e-9) on the
+                                 codec's scales (lic_sigmas); one string per plane, substreams ignored */
 } lic_pipeline_config;
 typedef struct {
     uint64_t frames;          /* frames completed */

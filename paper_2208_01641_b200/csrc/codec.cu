@@ -970,6 +970,15 @@ extern "C" lic_status lic_cdf(const lic_codec* c, int which, const uint32_t** ro
     return LIC_OK;
 }
 
+extern "C" lic_status lic_sigmas(const lic_codec* c, int which, const float** sig, uint32_t* n) {
+    if (!c || !sig || !n) return LIC_EINVAL;
+    const std::vector<float>* t = which == 0 ? &c->h_sigma_y : which == 1 ? &c->h_sigma_z : which == 2 ? &c->h_table : nullptr;
+    if (!t || t->empty() || (which == 0 && c->kind != 0) || (which == 1 && c->kind == 0)) return LIC_EINVAL;
+    *sig = t->data();
+    *n = (uint32_t)t->size();
+    return LIC_OK;
+}
+
 // ------------------------------------------------------------------ pool
 extern "C" lic_status lic_buf_acquire(lic_codec* c, size_t bytes, void** host_ptr) {
     if (!c || !host_ptr || bytes == 0) return LIC_EINVAL;

@@ -147,8 +147,9 @@ extern "C" lic_status lic_rans64_encode(const int32_t* sym, const int32_t* idx, 
     // chunks 4 bits; an escape adds at most 1 + 2 + 9 chunks (|raw| < 2^33)
     size_t bound_bits = 64;
     for (size_t i = 0; i < n; ++i) bound_bits += kPrec + 12 * kBypassBits;
-    std::vector<uint32_t> buf(bound_bits / 32 + 4);
-    uint32_t* const end = buf.data() + buf.size();
+    static thread_local std::vector<uint32_t> buf;           // reused: no allocation per plane
+    if (buf.size() < bound_bits / 32 + 4) buf.resize(bound_bits / 32 + 4);
+    uint32_t* const end = buf.data() + bound_bits / 32 + 4;
     uint32_t* p = end;
     uint64_t x = kL;
     for (size_t i = n; i-- > 0;) {

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -63,6 +64,27 @@ struct CpuTask { CpuKind kind; int slot; int frame; };
 
 }  // namespace
 
+// rans64 tables (cfg.coder = 1): Gaussian rows on the codec's scales (lic_cdf64_gaussian)
+struct Tab64 {
+    std::vector<uint32_t> cdfs;
+    std::vector<int32_t> sizes, offs;
+    uint32_t n = 0, stride = 0;
+};
+
+static lic_status build_tab64(const lic_codec* codec, int which, Tab64& t) {
+    const float* sig = nullptr;
+    uint32_t n = 0;
+    if (lic_status st = lic_sigmas(codec, which, &sig, &n)) return st;
+    float smax = 0.0f;
+    for (uint32_t i = 0; i < n; ++i) smax = std::max(smax, sig[i]);
+    t.n = n;
+    t.stride = 2 * (uint32_t)std::ceil(smax * 6.2f) + 8;     // m(1e-9) = 6.109
+    t.cdfs.assign((size_t)n * t.stride, 0u);
+    t.sizes.assign(n, 0);
+    t.offs.assign(n, 0);
+    return lic_cdf64_gaussian(sig, n, 1e-9, t.cdfs.data(), t.stride, t.sizes.data(), t.offs.data());
+}
+
 struct lic_pipeline {
     lic_codec* codec = nullptr;
     lic_codec* codec2 = nullptr;            // decoder GPU1 (h_s on decoded z) on its own stream
@@ -78,6 +100,9 @@ struct lic_pipeline {
     int sym_min = 0;
     lic_rans_tables* tab_y = nullptr;       // prepared coder tables (lic_rans_prepare)
     lic_rans_tables* tab_z = nullptr;
+    uint32_t coder = 0;                     // 0: rANS32 (+ substreams), 1: rans64 + bypass
+    Tab64 t64_y, t64_z;
+    std::vector<int32_t> ch_rows_y, ch_rows_z;   // channel row of every element (factorized y, z)
     std::vector<Slot> slots;
     std::vector<void*> pinned;
     std::vector<void*> dev;                 // device slot planes
@@ -108,7 +133,70 @@ struct lic_pipeline {
     std::vector<std::vector<uint8_t>> keep_y, keep_z;
 };
 
+// rans64 on int8 planes: symbols / uint8 rows widened to int32 in per-thread buffers
+static thread_local std::vector<int32_t> tl_sym, tl_idx;
+
+static const int32_t* rows64(const uint8_t* idx8, const std::vector<int32_t>& ch_rows, size_t n) {
+    if (!idx8) return ch_rows.data();
+    tl_idx.resize(n);
+    for (size_t i = 0; i < n; ++i) tl_idx[i] = idx8[i];
+    return tl_idx.data();
+}
+
+static lic_status enc64(const Tab64& t, const int8_t* sym, const int32_t* rows, size_t n, std::vector<uint8_t>& out,
+                        size_t* len) {
+    tl_sym.resize(n);
+    for (size_t i = 0; i < n; ++i) tl_sym[i] = sym[i];
+    return lic_rans64_encode(tl_sym.data(), rows, n, t.cdfs.data(), t.n, t.stride, t.sizes.data(), t.offs.data(),
+                             out.data(), out.size(), len);
+}
+
+static lic_status dec64(const Tab64& t, const uint8_t* in, size_t len, const int32_t* rows, size_t n, int8_t* out) {
+    tl_sym.resize(n);
+    lic_status st = lic_rans64_decode(in, len, rows, n, t.cdfs.data(), t.n, t.stride, t.sizes.data(), t.offs.data(),
+                                      tl_sym.data());
+    if (st) return st;
+    for (size_t i = 0; i < n; ++i) {
+        if (tl_sym[i] < -128 || tl_sym[i] > 127) return LIC_ECORRUPT;
+        out[i] = (int8_t)tl_sym[i];
+    }
+    return LIC_OK;
+}
+
+static void coder_task64(lic_pipeline* p, const CpuTask& t) {
+    Slot& s = p->slots[t.slot];
+    const size_t f = (size_t)t.frame;
+    lic_status st = LIC_OK;
+    uint64_t mism = 0;
+    if (t.kind == C_ONE) {
+        const int32_t* ry = rows64(p->hyper ? s.y_idx + f * p->ny : nullptr, p->ch_rows_y, p->ny);
+        st = enc64(p->t64_y, s.y_sym + f * p->ny, ry, p->ny, s.ystr[f], &s.ylen[f]);
+        if (!st && p->hyper)
+            st = enc64(p->t64_z, s.z_sym + f * p->nz, p->ch_rows_z.data(), p->nz, s.zstr[f], &s.zlen[f]);
+        if (!st && p->hyper) {
+            st = dec64(p->t64_z, s.zstr[f].data(), s.zlen[f], p->ch_rows_z.data(), p->nz, s.z_dec + f * p->nz);
+            if (!st && std::memcmp(s.z_dec + f * p->nz, s.z_sym + f * p->nz, p->nz) != 0) mism += 1;
+        } else if (!st) {
+            st = dec64(p->t64_y, s.ystr[f].data(), s.ylen[f], ry, p->ny, s.y_dec + f * p->ny);
+            if (!st && std::memcmp(s.y_dec + f * p->ny, s.y_sym + f * p->ny, p->ny) != 0) mism += 1;
+        }
+    } else {
+        const int32_t* ry = rows64(s.idx_dec + f * p->ny, p->ch_rows_y, p->ny);
+        st = dec64(p->t64_y, s.ystr[f].data(), s.ylen[f], ry, p->ny, s.y_dec + f * p->ny);
+        if (!st && std::memcmp(s.y_dec + f * p->ny, s.y_sym + f * p->ny, p->ny) != 0) mism += 1;
+    }
+    std::lock_guard<std::mutex> g(p->mu);
+    if (st && !p->err) p->err = st;
+    p->mismatches += mism;
+    if (--s.remaining == 0) {
+        if (t.kind == C_ONE && p->hyper) p->gpu_q.push_back({G_IDX, t.slot});
+        else p->gpu_q.push_back({G_DEC, t.slot});
+        p->cv_gpu.notify_one();
+    }
+}
+
 static void coder_task(lic_pipeline* p, const CpuTask& t) {
+    if (p->coder == 1) { coder_task64(p, t); return; }
     Slot& s = p->slots[t.slot];
     const size_t f = (size_t)t.frame;
     lic_status st = LIC_OK;
@@ -220,6 +308,21 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
         lic_pipeline_close(p);
         return st;
     }
+    p->coder = cfg->coder;
+    if (p->coder > 1) { lic_pipeline_close(p); return LIC_EINVAL; }
+    if (p->coder == 1) {
+        if ((st = build_tab64(codec, p->hyper ? 2 : 0, p->t64_y)) ||
+            (p->hyper && (st = build_tab64(codec, 1, p->t64_z)))) {
+            lic_pipeline_close(p);
+            return st;
+        }
+        auto ch_rows = [](const lic_shape& sh, std::vector<int32_t>& r) {
+            r.resize((size_t)sh.c * sh.h * sh.w);
+            for (size_t i = 0; i < r.size(); ++i) r[i] = (int32_t)(i / ((size_t)sh.h * sh.w));
+        };
+        if (!p->hyper) ch_rows(p->ys, p->ch_rows_y);
+        else ch_rows(p->zs, p->ch_rows_z);
+    }
     const size_t B = cfg->batch;
     auto pin = [&](size_t bytes) -> void* {
         void* q = nullptr;
@@ -264,8 +367,11 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
             lic_pipeline_close(p);
             return LIC_ENOMEM;
         }
-        s.ystr.assign(B, std::vector<uint8_t>(2 * p->ny + 64 + 8 * p->ksub));
-        s.zstr.assign(B, std::vector<uint8_t>(2 * p->nz + 64));
+        // rans64: <= 16 bits per symbol plus <= 12 escape bits (int8 values), words of 4 bytes
+        const size_t ycap = p->coder == 1 ? 4 * p->ny + 64 : 2 * p->ny + 64 + 8 * p->ksub;
+        const size_t zcap = p->coder == 1 ? 4 * p->nz + 64 : 2 * p->nz + 64;
+        s.ystr.assign(B, std::vector<uint8_t>(ycap));
+        s.zstr.assign(B, std::vector<uint8_t>(zcap));
         s.ylen.assign(B, 0);
         s.zlen.assign(B, 0);
     }

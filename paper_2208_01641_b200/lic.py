@@ -82,7 +82,7 @@ _L.lic_trace_read.argtypes = [_P, _P, _sz]
 class PipelineConfig(ctypes.Structure):
     _fields_ = [("coder_threads", ctypes.c_uint32), ("batch", ctypes.c_uint32), ("inflight", ctypes.c_uint32),
                 ("u8", ctypes.c_int), ("serial", ctypes.c_int), ("keep_bitstreams", ctypes.c_int),
-                ("substreams", ctypes.c_uint32)]
+                ("substreams", ctypes.c_uint32), ("coder", ctypes.c_uint32)]
 
 
 class PipelineStats(ctypes.Structure):
@@ -112,6 +112,7 @@ _L.lic_rans_decode_fast.argtypes = [_P, _P, _sz, _P, Shape, _P]
 _L.lic_rans_encode_slabs.argtypes = [_P, _P, _P, Shape, _u32, _P, _sz, ctypes.POINTER(_sz)]
 _L.lic_rans_decode_slabs.argtypes = [_P, _P, _sz, _P, Shape, _u32, _P]
 _L.lic_cdf_quantize.argtypes = [_P, _u32, _P]
+_L.lic_sigmas.argtypes = [_P, _i, ctypes.POINTER(ctypes.POINTER(ctypes.c_float)), ctypes.POINTER(_u32)]
 _L.lic_cdf64_gaussian.argtypes = [_P, _u32, ctypes.c_double, _P, _u32, _P, _P]
 _L.lic_rans64_encode.argtypes = [_P, _P, _sz, _P, _u32, _u32, _P, _P, _P, _sz, ctypes.POINTER(_sz)]
 _L.lic_rans64_decode.argtypes = [_P, _sz, _P, _sz, _P, _u32, _u32, _P, _P, _P]
@@ -354,6 +355,13 @@ class Codec:
         return self._h
 
     # -- tables
+    def sigmas(self, which):
+        """lic_sigmas: 0 sigma_y (factorized), 1 sigma_z, 2 the scale table (hyperprior)."""
+        ptr = ctypes.POINTER(ctypes.c_float)()
+        n = _u32()
+        self._chk(_L.lic_sigmas(self._h, which, ctypes.byref(ptr), ctypes.byref(n)), "lic_sigmas")
+        return np.ctypeslib.as_array(ptr, shape=(n.value,)).copy()
+
     def cdf(self, which):
         rows = ctypes.POINTER(ctypes.c_uint32)()
         n, rl = _u32(), _u32()
@@ -465,11 +473,11 @@ class Pipeline:
     """lic_pipeline: GPU control thread (the caller) + native coder worker pool."""
 
     def __init__(self, codec: Codec, coder_threads: int, batch: int, inflight: int = 2, u8: bool = True,
-                 serial: bool = False, keep_bitstreams: bool = False, substreams: int = 1):
+                 serial: bool = False, keep_bitstreams: bool = False, substreams: int = 1, coder: int = 0):
         self.codec = codec
         self.substreams = substreams
         self.cfg = PipelineConfig(coder_threads, batch, inflight, int(u8), int(serial), int(keep_bitstreams),
-                                  substreams)
+                                  substreams, coder)
         self._h = _P()
         st = _L.lic_pipeline_open(codec.handle, ctypes.byref(self.cfg), ctypes.byref(self._h))
         if st:

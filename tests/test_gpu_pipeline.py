@@ -23,12 +23,12 @@ def lic():
     return L
 
 
-def run_pipeline(lic, codec, frames, serial, inflight=3, threads=3, substreams=1):
+def run_pipeline(lic, codec, frames, serial, inflight=3, threads=3, substreams=1, coder=0):
     import torch
     fin = torch.from_numpy(frames).cuda()
     fout = torch.zeros_like(fin)
     p = lic.Pipeline(codec, coder_threads=threads, batch=B, inflight=inflight, u8=True, serial=serial,
-                     keep_bitstreams=True, substreams=substreams)
+                     keep_bitstreams=True, substreams=substreams, coder=coder)
     st = p.run(fin, fout, NF)
     streams = [p.bitstream(i) for i in range(NF)]
     p.close()
@@ -81,6 +81,42 @@ def test_pipeline_matches_serial_and_direct(lic, kind, K):
                 assert yb == lic.rans_encode(ys[f], tabs_y)
                 assert np.array_equal(O.rans_decode(yb, O.channel_rows(ys[f].shape), tabs_y).reshape(ys[f].shape),
                                       ys[f])
+    codec.close()
+
+
+@pytest.mark.parametrize("kind", [1, 0])
+def test_pipeline_rans64_coder(lic, kind):
+    """coder = 1: the rans64 + bypass coder (R23) inside the pipeline -- lossless,
+    pipelined == serial, every string equal to the direct coder on the GPU planes and, for
+    the first frame, to the oracle's."""
+    from oracle import rans64 as O64
+    spec = ModelSpec(kind=kind, N=128, M=192)
+    w = generate_weights(spec, seed=0)
+    codec = lic.Codec(write_licw(spec, w), H, W, max_batch=B)
+    frames = synth_frames_u8(NF, H, W, seed=23)
+    st, streams, out = run_pipeline(lic, codec, frames, serial=False, coder=1)
+    st_s, streams_s, out_s = run_pipeline(lic, codec, frames, serial=True, coder=1)
+    assert st["frames"] == NF and st["symbol_mismatches"] == 0 and st_s["symbol_mismatches"] == 0
+    assert streams == streams_s and np.array_equal(out, out_s)
+    hyper = kind == 1
+    ty = lic.Rans64Tables.gaussian(codec.sigmas(2 if hyper else 0))
+    tz = lic.Rans64Tables.gaussian(codec.sigmas(1)) if hyper else None
+    for b0 in range(0, NF, B):
+        ys = np.empty((B,) + codec.y_shape, np.int8)
+        yi = np.empty((B,) + codec.y_shape, np.uint8) if hyper else None
+        zs = np.empty((B,) + codec.z_shape, np.int8) if hyper else None
+        codec.encode(np.ascontiguousarray(frames[b0:b0 + B]), ys, yi, zs, u8=True)
+        for f in range(B):
+            yb, zb = streams[b0 + f]
+            ry = yi[f].ravel() if hyper else O.channel_rows(ys[f].shape).ravel()
+            assert yb == ty.encode(ys[f].ravel(), ry)
+            if hyper:
+                rz = O.channel_rows(zs[f].shape).ravel()
+                assert zb == tz.encode(zs[f].ravel(), rz)
+            if b0 + f == 0:
+                assert yb == O64.rans64_encode(ys[f].ravel(), ry, ty.cdfs, ty.sizes, ty.offsets)
+                if hyper:
+                    assert zb == O64.rans64_encode(zs[f].ravel(), rz, tz.cdfs, tz.sizes, tz.offsets)
     codec.close()
 
 
