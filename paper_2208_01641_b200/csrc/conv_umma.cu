@@ -972,15 +972,24 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 tc_fence_after();
                 if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_NORM);
                 __half* out = reinterpret_cast<__half*>(p.out_act);
+                // GC = 2: both norm column blocks in flight at once (one TMEM wait); GC = 3
+                // loads them one by one (three at once would spill)
+                constexpr int kNB = GC == 2 ? 2 : 1;
+                float nall[kNB][16];
+                if constexpr (GC == 2) {
+                    __syncwarp();
+                    tmem_ld32(taddr + p.BN + g * G, nall[0]);
+                }
 #pragma unroll
                 for (int j = 0; j < GC; ++j) {
-                    float n[16];
-                    __syncwarp();
+                    float* n = nall[GC == 2 ? j : 0];
+                    if constexpr (GC != 2) {
+                        __syncwarp();
+                        tmem_ld16(taddr + p.BN + g * G + j * 16, n);
+                    }
                     if (p.dbg_nostore & 4) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) n[i] = x[j][i];
-                    } else {
-                        tmem_ld16(taddr + p.BN + g * G + j * 16, n);
                     }
                     const int cb = g * G + j * 16;
 #pragma unroll
