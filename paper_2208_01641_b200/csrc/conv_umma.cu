@@ -543,7 +543,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             }
             __syncwarp();
         }
-        if (p.pdl) griddep_wait();                // activations below come from the previous kernel
+        // activations below come from the previous kernel; in halo mode this warp streams only
+        // weights (constant), so its ring fills while the previous layer is still finishing
+        if (p.pdl && !p.halo) griddep_wait();
         int stage = 0;
         uint32_t phase = 0;
         int pit = 0;
