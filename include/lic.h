@@ -32,7 +32,10 @@
  *     the stream.
  *   - Device memory is allocated once in lic_open and freed only in lic_close (PAPER.md:105
  *     "we carefully control dynamic memory allocation/deallocation and pool the
- *     allocated memory"); no call allocates or frees device memory in steady state.
+ *     allocated memory"); no call allocates or frees device memory in steady state.  The
+ *     batch-sized part (the workspace) may instead be owned by the caller (e.g. a torch
+ *     allocation): lic_workspace_bytes / lic_bind_workspace.  Test-only exports allocate
+ *     their scratch once, on first use.
  *   - Errors: every call returns lic_status; nothing aborts or throws across the ABI
  *     ("never a panic").  A CUDA failure is sticky for the codec (LIC_ECUDA).
  *   - Concurrency: one lic_codec is driven by one thread at a time; the host coder
@@ -75,7 +78,12 @@ typedef enum {
  * upload the weights to `device`, plan every layer for frames of height x width and up
  * to max_batch frames per call, allocate all device memory.  `licw` is only read during
  * the call.  Errors: LIC_EDIGEST (malformed container), LIC_EINVAL (beta <= 0, gamma < 0,
- * unsupported N/M), LIC_ESHAPE (zero geometry), LIC_ECUDA (no sm_100 device), LIC_ENOMEM. */
+ * unsupported N/M, or a conv / deconv weight or gamma entry that is not exactly
+ * representable in fp16 -- the tensor cores take fp16 operands and the split-FP16 mode
+ * (R16) is exact only for fp16 weights, as the paper's FP16 engines hold them,
+ * PAPER.md:129; round trained weights to fp16 once, then run the oracle on the same
+ * rounded values), LIC_ESHAPE (zero geometry), LIC_ECUDA (no sm_100 device), LIC_ENOMEM.
+ * On failure *out is NULL and lic_last_error(NULL) returns this thread's message. */
 lic_status lic_open(const uint8_t* licw, size_t len, int device, uint32_t height, uint32_t width,
                     uint32_t max_batch, int precision, lic_codec** out);
 void lic_close(lic_codec* codec);
@@ -90,8 +98,30 @@ lic_status lic_shapes(const lic_codec* codec, lic_shape* y, lic_shape* z, int* k
  * (the paper's unified-memory Jetson path). */
 lic_status lic_set_zero_copy(lic_codec* codec, int on);
 
-/* Message for the last error on this codec (owned by the codec). */
+/* Message for the last error on this codec (owned by the codec); codec == NULL: the last
+ * failed lic_open on the calling thread (thread-local). */
 const char* lic_last_error(const lic_codec* codec);
+
+/* ---------------------------------------------------------------- workspace
+ * device memory is allocated once and pooled, never freed while the codec
+ * runs.  The batch-sized device memory of a codec -- activation planes (fp16 hi + lo NHWC
+ * ping-pong buffers of the largest activation, the y- and z-planes), frame staging and
+ * symbol / index staging planes -- is one block, "the workspace".  lic_open allocates it
+ * for max_batch frames; a caller that owns device memory (PyTorch's caching allocator)
+ * may hand the codec its own block instead.
+ *
+ * lic_workspace_bytes: bytes of the workspace for `batch` frames (0: lic_open's
+ *   max_batch); 0 if batch exceeds it or codec is NULL.
+ * lic_bind_workspace: waits for the device, then uses [dev_ptr, dev_ptr + bytes) as the
+ *   workspace from now on and frees the library's own block.  The codec's max_batch
+ *   becomes the largest batch (<= lic_open's) whose workspace fits in `bytes`
+ *   (lic_max_batch).  dev_ptr must be device memory of the codec's device, 256-byte
+ *   aligned; the caller keeps it alive until lic_close or the next bind.  Results are
+ *   bit-identical to the library-owned workspace.  Errors: LIC_EINVAL (NULL, host memory,
+ *   wrong device, misaligned), LIC_ENOSPACE (smaller than one frame's workspace). */
+size_t lic_workspace_bytes(const lic_codec* codec, uint32_t batch);
+lic_status lic_bind_workspace(lic_codec* codec, void* dev_ptr, size_t bytes);
+lic_status lic_max_batch(const lic_codec* codec, uint32_t* max_batch);
 
 /* ---------------------------------------------------------------- pooled pinned buffers */
 
@@ -165,6 +195,15 @@ lic_status lic_trace(lic_codec* codec, int layer_id, int on);
 lic_status lic_trace_read(lic_codec* codec, uint64_t* out, size_t n);
 /* Total kernels this codec has launched (GEMM engine + ingest kernels). */
 lic_status lic_launch_count(const lic_codec* codec, uint64_t* n);
+
+/* Activation range guard (R16d).  Activations are stored as fp16 hi + lo planes
+ * whose range ends at 65504 -- the bound of the paper's FP16 engines.  (The
+ * GDN / IGDN norm operand x^2 is scaled per pixel by an exact power of two, so it has no
+ * such bound.)  An activation beyond +-65504 is stored saturated to +-65504 -- never inf
+ * or NaN -- and counted; a nonzero count means the results of the calls since the last
+ * reset may differ from the fp32 oracle.  Waits for the device (a diagnostic, not a
+ * hot-path call); *n = the count since the last reset; reset != 0 zeroes it. */
+lic_status lic_range_count(lic_codec* codec, uint64_t* n, int reset);
 
 /* ---------------------------------------------------------------- HOST entropy coder */
 

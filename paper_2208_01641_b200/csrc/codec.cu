@@ -134,6 +134,7 @@ struct Layer {
     size_t in_plane = 0;
     __half* out_buf = nullptr;
     size_t out_plane = 0;
+    char in_id = 0, out_id = 0;   // workspace buffer ('A', 'B', 'Y', 'Z'; 0 = none) -- re-bound by lic_bind_workspace
     ConvParams prm{};
     CUtensorMap mapA{}, mapB{}, mapG{}, mapOH{}, mapOL{};
 };
@@ -152,6 +153,7 @@ struct lic_codec {
     size_t planeA = 0, planeY = 0, planeZ = 0;
     float *mu_y = nullptr, *mu_z = nullptr, *table = nullptr;
     unsigned long long* d_sat = nullptr;
+    unsigned long long* d_range = nullptr;   // activations saturated to the fp16 range (R16d)
     void* d_frames = nullptr;           // staging for host frames (f32 CHW size)
     int8_t* d_ysym = nullptr;
     uint8_t* d_yidx = nullptr;
@@ -179,6 +181,12 @@ struct lic_codec {
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
     std::vector<void*> allocs;          // device allocations to free
+    void* ws_own = nullptr;             // library-allocated workspace (nullptr once the caller binds one)
+    void* ws_user = nullptr;            // caller-owned workspace (lic_bind_workspace)
+    size_t ws_bytes = 0;
+    int open_batch = 1;                 // max_batch given to lic_open (a bound workspace may lower max_batch)
+    float* d_test = nullptr;            // test-only scratch (lic_test_sigma_to_index), allocated on first use
+    uint8_t* d_test_idx = nullptr;
     // pinned pool
     std::mutex pool_mu;
     std::map<size_t, std::vector<void*>> free_lists;
@@ -434,7 +442,8 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     // shared memory plan: stage ring | halo ring (halo mode) | gamma (GDN) | mbarriers | constants
     const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)(P.BN / P.cg) * 64 * 2;
     const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
-    const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64 + kMaxTaps) * 4;   // + halo tap offsets
+    // bias / beta / mu, scale table, halo tap offsets (+ GDN: per-pixel norm exponents, 128 x 4 B)
+    const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64 + kMaxTaps) * 4 + (gdn ? 512u : 0u);
     const uint32_t budget = 227u * 1024u;
     // TMA-store epilogue: 4 lane quadrants x 8 KB block slots (1 or 2 slots), when the layer writes an activation and the
     // pipeline keeps >= 3 stages with it (env LIC_TMA_OUT=0 disables)
@@ -696,7 +705,10 @@ static OutBuf route_frames_out(void* user, void* staging, size_t bytes) {
 // ------------------------------------------------------------------ ABI
 extern "C" const char* lic_version(void) { return "lic-b200 0.1 (sm_100a tcgen05)"; }
 
-extern "C" const char* lic_last_error(const lic_codec* c) { return c ? c->err.c_str() : "null codec"; }
+// lic_open's failures have no codec to hold the message: a thread-local one instead
+static thread_local std::string g_open_err;
+
+extern "C" const char* lic_last_error(const lic_codec* c) { return c ? c->err.c_str() : g_open_err.c_str(); }
 
 extern "C" void lic_close(lic_codec* c) {
     if (!c) return;
@@ -704,6 +716,7 @@ extern "C" void lic_close(lic_codec* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     for (void* p : c->allocs) cudaFree(p);
+    if (c->ws_own) cudaFree(c->ws_own);
     {
         std::lock_guard<std::mutex> g(c->pool_mu);
         for (auto& kv : c->owned) cudaFreeHost(kv.first);
@@ -712,20 +725,83 @@ extern "C" void lic_close(lic_codec* c) {
     delete c;
 }
 
+// ------------------------------------------------------------------ workspace
+// Everything whose size follows the batch: the activation ping-pong buffers A / B (fp16 hi +
+// lo NHWC planes of the largest activation, Hp/2 x Wp/2 x N), the y-plane (|y| or y-hat), the
+// z-plane (z-hat), the host-frame staging buffer and the symbol / index staging planes.  One
+// block, carved in this order at 256-byte boundaries; owned by the library (lic_open) or by
+// the caller (lic_bind_workspace).
+struct WsLayout { size_t planeA, planeY, planeZ, off[8], total; };
+static WsLayout ws_layout(const lic_codec* c, int B) {
+    WsLayout L{};
+    const int S = c->split, N = c->N, M = c->M;
+    const size_t Hy = c->Hp / 16, Wy = c->Wp / 16, Hz = std::max(1, c->Hp / 64), Wz = std::max(1, c->Wp / 64);
+    L.planeA = (size_t)B * (c->Hp / 2) * (c->Wp / 2) * N;
+    L.planeY = (size_t)B * Hy * Wy * M;
+    L.planeZ = (size_t)B * Hz * Wz * N;
+    const size_t sz[8] = {L.planeA * S * 2, L.planeA * S * 2, L.planeY * S * 2, L.planeZ * S * 2,
+                          (size_t)B * 3 * c->H * c->W * 4, (size_t)B * M * Hy * Wy, (size_t)B * M * Hy * Wy,
+                          (size_t)B * N * Hz * Wz};
+    size_t o = 0;
+    for (int i = 0; i < 8; ++i) { L.off[i] = o; o += (sz[i] + 255) / 256 * 256; }
+    L.total = o;
+    return L;
+}
+static void ws_carve(lic_codec* c, uint8_t* base, int B) {
+    const WsLayout L = ws_layout(c, B);
+    c->planeA = L.planeA; c->planeY = L.planeY; c->planeZ = L.planeZ;
+    c->bufA = (__half*)(base + L.off[0]);
+    c->bufB = (__half*)(base + L.off[1]);
+    c->bufY = (__half*)(base + L.off[2]);
+    c->bufZ = (__half*)(base + L.off[3]);
+    c->d_frames = base + L.off[4];
+    c->d_ysym = (int8_t*)(base + L.off[5]);
+    c->d_yidx = (uint8_t*)(base + L.off[6]);
+    c->d_zsym = (int8_t*)(base + L.off[7]);
+}
+static __half* ws_buf(const lic_codec* c, char id, size_t* plane) {
+    switch (id) {
+    case 'A': *plane = c->planeA; return c->bufA;
+    case 'B': *plane = c->planeA; return c->bufB;
+    case 'Y': *plane = c->planeY; return c->bufY;
+    case 'Z': *plane = c->planeZ; return c->bufZ;
+    default: *plane = 0; return nullptr;
+    }
+}
+
 static lic_status upload(lic_codec* c, void* dst, const void* src, size_t bytes) {
     CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
     return LIC_OK;
 }
 
+// per-codec epilogue settings of the layer plans (after plan_layer)
+static void finish_plans(lic_codec* c) {
+    for (int l = 0; l < NLAYER; ++l)
+        if (c->layers[l].present) c->layers[l].prm.range_count = c->d_range;
+    c->layers[GA4].prm.mu = c->kind == 0 ? c->mu_y : nullptr;
+    c->layers[GA4].prm.abs_out = c->kind == 1;
+    for (int l : {GA1, GA2, GA3, GS1, GS2, GS3}) c->layers[l].prm.onedn = c->act == 1;
+    if (c->kind == 1) c->layers[HA3].prm.mu = c->mu_z;
+    c->layers[GS4].prm.crop_top = c->top;
+    c->layers[GS4].prm.crop_left = c->left;
+    c->layers[GS4].prm.crop_H = c->H;
+    c->layers[GS4].prm.crop_W = c->W;
+}
+
 extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint32_t height, uint32_t width,
                                uint32_t max_batch, int precision, lic_codec** out) {
+    g_open_err.clear();
     if (!licw || !out || max_batch == 0) return LIC_EINVAL;
     *out = nullptr;
     if (height == 0 || width == 0 || height > 8192 || width > 8192) return LIC_ESHAPE;
     if (precision != LIC_PREC_SPLIT && precision != LIC_PREC_F16) return LIC_EINVAL;
     if (len < 13 || std::memcmp(licw, "LICW", 4) != 0 || licw[4] != 1) return LIC_EDIGEST;
     lic_codec* c = new lic_codec();
-    auto bail = [&](lic_status st) { lic_close(c); return st; };
+    auto bail = [&](lic_status st) {
+        if (g_open_err.empty() && !c->err.empty()) g_open_err = c->err;
+        lic_close(c);
+        return st;
+    };
     c->licw.assign(licw, licw + len);
     c->precision = precision;
     c->kind = licw[5];
@@ -755,6 +831,19 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
             for (float f : v) if (!(f > 0.0f)) return bail(LIC_EINVAL);
         if (b.role == R_GAMMA)
             for (float f : v) if (!(f >= 0.0f)) return bail(LIC_EINVAL);
+        // The tensor cores multiply fp16 operands: conv / deconv weights and gamma must be
+        // exactly representable in fp16 (the split-FP16 precision, R16; the paper's
+        // FP16 engines hold fp16 weights too).  Rounding them here would miss
+        // the oracle's parity bar silently, so a container with other values is rejected.
+        if (b.role == R_CONV || b.role == R_DECONV || b.role == R_GAMMA)
+            for (size_t i = 0; i < v.size(); ++i)
+                if (__half2float(__float2half_rn(v[i])) != v[i]) {
+                    char m[160];
+                    std::snprintf(m, sizeof m, "%s[%zu] = %.9g is not exactly representable in fp16", b.name.c_str(), i,
+                                  (double)v[i]);
+                    g_open_err = m;
+                    return bail(LIC_EINVAL);
+                }
         blk[b.name] = std::move(v);
     }
     if (off != len) return bail(LIC_EDIGEST);
@@ -816,43 +905,42 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
             return bail(LIC_EINVAL);
     }
 
-    // ---- activation buffers (planes of fp16 NHWC)
-    c->planeA = (size_t)B * H2 * W2 * N;
-    c->planeY = (size_t)B * Hy * Wy * M;
-    c->planeZ = (size_t)B * std::max(1, Hz) * std::max(1, Wz) * N;
+    // ---- workspace (activation planes of fp16 NHWC, staging) -- one block, re-bindable
+    c->open_batch = B;
+    c->ws_bytes = ws_layout(c, B).total;
+    if (cudaMalloc(&c->ws_own, c->ws_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        c->ws_own = nullptr;
+        return bail(fail(c, LIC_ENOMEM, "cudaMalloc(%zu) failed (workspace)", c->ws_bytes));
+    }
+    ws_carve(c, (uint8_t*)c->ws_own, B);
     lic_status st;
-    if ((st = dalloc(c, &c->bufA, c->planeA * S * 2)) ||
-        (st = dalloc(c, &c->bufB, c->planeA * S * 2)) || (st = dalloc(c, &c->bufY, c->planeY * S * 2)) ||
-        (st = dalloc(c, &c->bufZ, c->planeZ * S * 2)) || (st = dalloc(c, &c->table, 64 * 4)) ||
-        (st = dalloc(c, &c->mu_y, (size_t)M * 4)) || (st = dalloc(c, &c->mu_z, (size_t)N * 4)) ||
-        (st = dalloc(c, &c->d_sat, 8)) || (st = dalloc(c, &c->d_frames, (size_t)B * 3 * c->H * c->W * 4)) ||
-        (st = dalloc(c, &c->d_ysym, (size_t)B * M * Hy * Wy)) || (st = dalloc(c, &c->d_yidx, (size_t)B * M * Hy * Wy)) ||
-        (st = dalloc(c, &c->d_zsym, (size_t)B * N * std::max(1, Hz) * std::max(1, Wz))))
+    if ((st = dalloc(c, &c->table, 64 * 4)) || (st = dalloc(c, &c->mu_y, (size_t)M * 4)) ||
+        (st = dalloc(c, &c->mu_z, (size_t)N * 4)) || (st = dalloc(c, &c->d_sat, 8)) || (st = dalloc(c, &c->d_range, 8)))
         return bail(st);
     if ((st = upload(c, c->table, tab.data(), 256)) || (st = upload(c, c->mu_y, c->h_mu_y.data(), (size_t)M * 4)))
         return bail(st);
     if (c->kind == 1 && (st = upload(c, c->mu_z, c->h_mu_z.data(), (size_t)N * 4))) return bail(st);
 
     // ---- layers
-    struct Def { int id; bool deconv; int k, s, p, cin, cout, hin, win, hout, wout; EpKind ep; __half* in; size_t inpl;
-                 __half* out; size_t outpl; };
+    struct Def { int id; bool deconv; int k, s, p, cin, cout, hin, win, hout, wout; EpKind ep; char in, out; };
     std::vector<Def> defs = {
-        {GA1, false, 5, 2, 2, 3, N, c->Hp, c->Wp, H2, W2, EP_GDN, nullptr, 0, c->bufA, c->planeA},
-        {GA2, false, 5, 2, 2, N, N, H2, W2, H2 / 2, W2 / 2, EP_GDN, c->bufA, c->planeA, c->bufB, c->planeA},
-        {GA3, false, 5, 2, 2, N, N, H2 / 2, W2 / 2, H2 / 4, W2 / 4, EP_GDN, c->bufB, c->planeA, c->bufA, c->planeA},
-        {GA4, false, 5, 2, 2, N, M, H2 / 4, W2 / 4, Hy, Wy, EP_YQUANT, c->bufA, c->planeA, c->bufY, c->planeY},
-        {GS1, true, 5, 2, 2, M, N, Hy, Wy, Hy * 2, Wy * 2, EP_IGDN, c->bufY, c->planeY, c->bufA, c->planeA},
-        {GS2, true, 5, 2, 2, N, N, Hy * 2, Wy * 2, Hy * 4, Wy * 4, EP_IGDN, c->bufA, c->planeA, c->bufB, c->planeA},
-        {GS3, true, 5, 2, 2, N, N, Hy * 4, Wy * 4, H2, W2, EP_IGDN, c->bufB, c->planeA, c->bufA, c->planeA},
-        {GS4, true, 5, 2, 2, N, 3, H2, W2, c->Hp, c->Wp, EP_FINAL, c->bufA, c->planeA, nullptr, 0},
+        {GA1, false, 5, 2, 2, 3, N, c->Hp, c->Wp, H2, W2, EP_GDN, 0, 'A'},
+        {GA2, false, 5, 2, 2, N, N, H2, W2, H2 / 2, W2 / 2, EP_GDN, 'A', 'B'},
+        {GA3, false, 5, 2, 2, N, N, H2 / 2, W2 / 2, H2 / 4, W2 / 4, EP_GDN, 'B', 'A'},
+        {GA4, false, 5, 2, 2, N, M, H2 / 4, W2 / 4, Hy, Wy, EP_YQUANT, 'A', 'Y'},
+        {GS1, true, 5, 2, 2, M, N, Hy, Wy, Hy * 2, Wy * 2, EP_IGDN, 'Y', 'A'},
+        {GS2, true, 5, 2, 2, N, N, Hy * 2, Wy * 2, Hy * 4, Wy * 4, EP_IGDN, 'A', 'B'},
+        {GS3, true, 5, 2, 2, N, N, Hy * 4, Wy * 4, H2, W2, EP_IGDN, 'B', 'A'},
+        {GS4, true, 5, 2, 2, N, 3, H2, W2, c->Hp, c->Wp, EP_FINAL, 'A', 0},
     };
     if (c->kind == 1) {
-        defs.push_back({HA1, false, 3, 1, 1, M, N, Hy, Wy, Hy, Wy, EP_RELU, c->bufY, c->planeY, c->bufA, c->planeA});
-        defs.push_back({HA2, false, 5, 2, 2, N, N, Hy, Wy, Hy / 2, Wy / 2, EP_RELU, c->bufA, c->planeA, c->bufB, c->planeA});
-        defs.push_back({HA3, false, 5, 2, 2, N, N, Hy / 2, Wy / 2, Hz, Wz, EP_ZQUANT, c->bufB, c->planeA, c->bufZ, c->planeZ});
-        defs.push_back({HS1, true, 5, 2, 2, N, N, Hz, Wz, Hz * 2, Wz * 2, EP_RELU, c->bufZ, c->planeZ, c->bufA, c->planeA});
-        defs.push_back({HS2, true, 5, 2, 2, N, N, Hz * 2, Wz * 2, Hy, Wy, EP_RELU, c->bufA, c->planeA, c->bufB, c->planeA});
-        defs.push_back({HS3, false, 3, 1, 1, N, M, Hy, Wy, Hy, Wy, EP_SIGMA, c->bufB, c->planeA, nullptr, 0});
+        defs.push_back({HA1, false, 3, 1, 1, M, N, Hy, Wy, Hy, Wy, EP_RELU, 'Y', 'A'});
+        defs.push_back({HA2, false, 5, 2, 2, N, N, Hy, Wy, Hy / 2, Wy / 2, EP_RELU, 'A', 'B'});
+        defs.push_back({HA3, false, 5, 2, 2, N, N, Hy / 2, Wy / 2, Hz, Wz, EP_ZQUANT, 'B', 'Z'});
+        defs.push_back({HS1, true, 5, 2, 2, N, N, Hz, Wz, Hz * 2, Wz * 2, EP_RELU, 'Z', 'A'});
+        defs.push_back({HS2, true, 5, 2, 2, N, N, Hz * 2, Wz * 2, Hy, Wy, EP_RELU, 'A', 'B'});
+        defs.push_back({HS3, false, 3, 1, 1, N, M, Hy, Wy, Hy, Wy, EP_SIGMA, 'B', 0});
     }
     size_t dbg = 0;
     for (const Def& d : defs) {
@@ -863,7 +951,9 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
         Ly.Cin_eff = d.id == GA1 ? 128 : d.cin;
         Ly.Hin = d.hin; Ly.Win = d.win; Ly.Hout = d.hout; Ly.Wout = d.wout;
         Ly.ep = d.ep;
-        Ly.in_buf = d.in; Ly.in_plane = d.inpl; Ly.out_buf = d.out; Ly.out_plane = d.outpl;
+        Ly.in_id = d.in; Ly.out_id = d.out;
+        Ly.in_buf = ws_buf(c, d.in, &Ly.in_plane);
+        Ly.out_buf = ws_buf(c, d.out, &Ly.out_plane);
         dbg = std::max(dbg, (size_t)B * d.cout * d.hout * d.wout);
         dbg = std::max(dbg, (size_t)B * d.cin * d.hin * d.win);
         // weights: LICW out x in x k x k (fp32, fp16-exact) -> fp16 [tap][co_pad][ci_eff]
@@ -929,16 +1019,56 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
         }
         if ((st = plan_layer(c, Ly))) return bail(st);
     }
-    c->layers[GA4].prm.mu = c->kind == 0 ? c->mu_y : nullptr;
-    c->layers[GA4].prm.abs_out = c->kind == 1;
-    for (int l : {GA1, GA2, GA3, GS1, GS2, GS3}) c->layers[l].prm.onedn = c->act == 1;
-    if (c->kind == 1) c->layers[HA3].prm.mu = c->mu_z;
-    c->layers[GS4].prm.crop_top = c->top;
-    c->layers[GS4].prm.crop_left = c->left;
-    c->layers[GS4].prm.crop_H = c->H;
-    c->layers[GS4].prm.crop_W = c->W;
+    if (cudaMemset(c->d_range, 0, 8) != cudaSuccess) return bail(LIC_ECUDA);
+    finish_plans(c);
     c->dbg_elems = dbg;
     *out = c;
+    return LIC_OK;
+}
+
+extern "C" size_t lic_workspace_bytes(const lic_codec* c, uint32_t batch) {
+    if (!c) return 0;
+    if (batch == 0) batch = (uint32_t)c->open_batch;
+    if ((int)batch > c->open_batch) return 0;
+    return ws_layout(c, (int)batch).total;
+}
+
+extern "C" lic_status lic_bind_workspace(lic_codec* c, void* dev_ptr, size_t bytes) {
+    if (!c || !dev_ptr) return LIC_EINVAL;
+    if (c->sticky) return LIC_ECUDA;
+    if ((uintptr_t)dev_ptr % 256) return fail(c, LIC_EINVAL, "workspace must be 256-byte aligned");
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, dev_ptr) != cudaSuccess || a.type != cudaMemoryTypeDevice || a.device != c->device) {
+        cudaGetLastError();
+        return fail(c, LIC_EINVAL, "workspace is not device memory of device %d", c->device);
+    }
+    // the largest batch the block holds (planes scale with the batch)
+    int b = c->open_batch;
+    while (b > 0 && ws_layout(c, b).total > bytes) --b;
+    if (b == 0) return fail(c, LIC_ENOSPACE, "workspace of %zu bytes < %zu for one frame", bytes, ws_layout(c, 1).total);
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());                 // nothing may still use the old block
+    const int old_batch = c->max_batch;
+    c->max_batch = b;
+    ws_carve(c, (uint8_t*)dev_ptr, b);
+    for (int l = 0; l < NLAYER; ++l) {
+        Layer& Ly = c->layers[l];
+        if (!Ly.present) continue;
+        Ly.in_buf = ws_buf(c, Ly.in_id, &Ly.in_plane);
+        Ly.out_buf = ws_buf(c, Ly.out_id, &Ly.out_plane);
+        lic_status r = plan_layer(c, Ly);        // tensor maps over the new planes
+        if (r) { c->max_batch = old_batch; c->sticky = true; return r; }
+    }
+    finish_plans(c);
+    if (c->ws_own) { cudaFree(c->ws_own); c->ws_own = nullptr; }
+    c->ws_user = dev_ptr;
+    c->ws_bytes = ws_layout(c, b).total;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_max_batch(const lic_codec* c, uint32_t* max_batch) {
+    if (!c || !max_batch) return LIC_EINVAL;
+    *max_batch = (uint32_t)c->max_batch;
     return LIC_OK;
 }
 
@@ -1261,16 +1391,18 @@ extern "C" lic_status lic_test_layer(lic_codec* c, int id, const float* in, uint
 extern "C" lic_status lic_test_sigma_to_index(lic_codec* c, const float* sigma, size_t n, uint8_t* idx) {
     if (!c || !sigma || !idx) return LIC_EINVAL;
     if (c->sticky) return LIC_ECUDA;
-    float* ds = nullptr;
-    uint8_t* di = nullptr;
-    CK(cudaMalloc(&ds, n * 4 + 16));
-    CK(cudaMalloc(&di, n + 16));
-    CK(cudaMemcpy(ds, sigma, n * 4, cudaMemcpyDefault));
-    CK(launch_sigma_index(ds, n, c->table, di, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    CK(cudaMemcpy(idx, di, n, cudaMemcpyDefault));
-    cudaFree(ds);
-    cudaFree(di);
+    // test-only scratch: allocated once on first use, kept until lic_close; chunks of kTestN
+    constexpr size_t kTestN = (size_t)1 << 20;
+    lic_status r;
+    if (!c->d_test && ((r = dalloc(c, &c->d_test, kTestN * 4)) || (r = dalloc(c, &c->d_test_idx, kTestN)))) return r;
+    CK(cudaSetDevice(c->device));
+    for (size_t o = 0; o < n; o += kTestN) {
+        const size_t m = std::min(kTestN, n - o);
+        CK(cudaMemcpyAsync(c->d_test, sigma + o, m * 4, cudaMemcpyDefault, c->stream));
+        CK(launch_sigma_index(c->d_test, m, c->table, c->d_test_idx, c->stream));
+        CK(cudaMemcpyAsync(idx + o, c->d_test_idx, m, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
     return LIC_OK;
 }
 
@@ -1300,6 +1432,18 @@ extern "C" lic_status lic_profile_read(lic_codec* c, int id, double* ms, uint64_
     prof_flush(c);
     if (ms) *ms = c->prof_ms[id];
     if (n) *n = c->prof_n[id];
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_range_count(lic_codec* c, uint64_t* n, int reset) {
+    if (!c || !n) return LIC_EINVAL;
+    if (c->sticky) return LIC_ECUDA;
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    unsigned long long v = 0;
+    CK(cudaMemcpy(&v, c->d_range, 8, cudaMemcpyDeviceToHost));
+    if (reset) CK(cudaMemset(c->d_range, 0, 8));
+    *n = v;
     return LIC_OK;
 }
 

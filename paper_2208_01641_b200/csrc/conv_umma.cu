@@ -171,6 +171,25 @@ __device__ __forceinline__ void split_store8(__half* hi, __half* lo, const float
     if (lo) *reinterpret_cast<uint4*>(lo) = l;
 }
 
+// Activations are stored as fp16 hi + lo planes, whose range ends at 65504 (the same bound
+// as the paper's FP16 engines): a value beyond it would become hi = inf,
+// lo = -inf and poison the next layer with NaN.  Such values are stored saturated to
+// +-65504 and counted (p.range_count, lic_range_count; R16d).
+constexpr float kF16Max = 65504.0f;
+__device__ __forceinline__ void guard16(float* v, int& ovf) {
+    float m = fabsf(v[0]);
+#pragma unroll
+    for (int j = 1; j < 16; ++j) m = fmaxf(m, fabsf(v[j]));
+    if (m > kF16Max) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (fabsf(v[j]) > kF16Max) { ++ovf; v[j] = copysignf(kF16Max, v[j]); }
+    }
+}
+__device__ __forceinline__ void stsb(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ int round_clamp(float v, int L, int& sat) {
     float r = roundf(v);                 // half away from zero (R4)
     if (r > (float)L) { r = (float)L; ++sat; }
@@ -233,6 +252,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     float* s_mu = s_beta + p.BN * p.n_ntiles;                       // [cout_pad]
     float* s_tab = s_mu + p.BN * p.n_ntiles;                        // [64]
     uint32_t* s_tapoff = reinterpret_cast<uint32_t*>(s_tab + 64);   // [kMaxTaps] halo window offsets
+    // GDN / IGDN: per-pixel exponent of the norm operand, one byte per (pixel, channel group)
+    const uint32_t s_xe = smem_u32(s_tapoff + kMaxTaps);            // [128][4] u8
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -825,6 +846,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         uint32_t norm_phase = 0;
         int it = 0;
         int sat = 0;
+        int ovf = 0;                                // activations saturated to the fp16 range
         for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
             TileCoord tc = decode_tile(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
@@ -910,7 +932,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             };
             // generic epilogues: round k of the channel loop holds block k (warp g: channels
             // 64k + 16g ..) -- one block per round through alternating slots
-            auto emit16 = [&](const float* v16, int cb) {
+            auto emit16 = [&](float* v16, int cb) {
+                guard16(v16, ovf);
                 if (!tma_ok) { direct16(v16, cb); return; }
                 const int blk = (cb - co0) >> 6, slot = blk % qslots;
                 q_acquire(qslots - 1);
@@ -925,11 +948,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                 for (int j = 0; j + 1 < GC; j += 2) tmem_ld32(taddr + g * G + j * 16, x[j]);
                 if constexpr (GC & 1) tmem_ld16(taddr + g * G + (GC - 1) * 16, x[GC - 1]);
-                // x^2 (hi, lo) packed into this group's own accumulator columns:
-                // hi of channel g*G + k at column g*G + k/2, lo at g*G + G/2 + k/2
+                // x = acc (/ 255 for integer u8 samples) + b, and the largest norm operand v of the
+                // pixel (v = x^2, or |x| for 1DN) over this group's channels
+                float vmax = 0.0f;
 #pragma unroll
                 for (int j = 0; j < GC; ++j) {
-                    uint32_t hi[8], lo[8];
                     if (p.l1_int) {
                         // fused g_a L1 on u8 samples: acc = sum W * u exactly; x = acc / 255 + b
 #pragma unroll
@@ -941,14 +964,39 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         x[j][4 * i4 + 0] += bb.x; x[j][4 * i4 + 1] += bb.y;
                         x[j][4 * i4 + 2] += bb.z; x[j][4 * i4 + 3] += bb.w;
                     }
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        vmax = fmaxf(vmax, p.onedn ? fabsf(x[j][i]) : x[j][i] * x[j][i]);
+                }
+                // The norm operand goes to the tensor core as fp16 hi + lo, whose range ends at
+                // 65504 (x^2 overflows from |x| = 256 on).  Every pixel scales its operand by
+                // 2^-e, e = the smallest shift that keeps the pixel's largest v below 2^15 (0 for
+                // v < 2^14: the common case is unscaled, bit for bit), and the epilogue multiplies
+                // the contraction by 2^e -- both exact.  e is shared by the pixel's 4 channel
+                // groups (one byte each in smem, max over the quadrant's 4 warps).
+                {
+                    const int ex = (__float_as_int(vmax) >> 23) - 127;
+                    stsb(s_xe + 4u * (uint32_t)r + (uint32_t)g, (uint32_t)min(max(ex - 13, 0), 100));
+                }
+                named_bar_sync(5 + q, 128);
+                uint32_t xe = ldsu(s_xe + 4u * (uint32_t)r);
+                xe = max(max(xe & 0xffu, (xe >> 8) & 0xffu), max((xe >> 16) & 0xffu, xe >> 24));
+                const float sc_dn = __int_as_float((int)(127u - xe) << 23);
+                const float sc_up = __int_as_float((int)(127u + xe) << 23);
+                // v * 2^-e (hi, lo) packed into this group's own accumulator columns:
+                // hi of channel g*G + k at column g*G + k/2, lo at g*G + G/2 + k/2
+#pragma unroll
+                for (int j = 0; j < GC; ++j) {
+                    uint32_t hi[8], lo[8];
                     if (p.onedn) {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) split2(fabsf(x[j][2 * i]), fabsf(x[j][2 * i + 1]), hi[i], lo[i]);
+                        for (int i = 0; i < 8; ++i)
+                            split2(fabsf(x[j][2 * i]) * sc_dn, fabsf(x[j][2 * i + 1]) * sc_dn, hi[i], lo[i]);
                     } else {
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
                             const float a2 = x[j][2 * i] * x[j][2 * i], b2 = x[j][2 * i + 1] * x[j][2 * i + 1];
-                            split2(a2, b2, hi[i], lo[i]);
+                            split2(a2 * sc_dn, b2 * sc_dn, hi[i], lo[i]);
                         }
                     }
                     tmem_st8(taddr + g * G + j * 8, hi);
@@ -1003,14 +1051,14 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
                                 const int i = 4 * i4 + u;
-                                const float nn = bv[u] + n[i];
+                                const float nn = bv[u] + n[i] * sc_up;
                                 x[j][i] = (p.ep == EP_GDN) ? x[j][i] * rcp_ftz(nn) : x[j][i] * nn;
                             }
                         } else {
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
                                 const int i = 4 * i4 + u;
-                                const float nn = bv[u] + n[i];
+                                const float nn = bv[u] + n[i] * sc_up;
                                 const float rs = (p.dbg_nostore & 2) ? nn : rsqrt_ftz(nn);   // MUFU; sqrt(nn) = nn * rsqrt(nn)
                                 x[j][i] = (p.ep == EP_GDN) ? x[j][i] * rs : x[j][i] * (nn * rs);
                             }
@@ -1020,6 +1068,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
                         for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(cb + i) * HWo] = x[j][i];
                     }
+                    guard16(x[j], ovf);
                 }
                 // the accumulator is in registers: release TMEM before storing
                 tc_fence_before();
@@ -1239,6 +1288,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         if (p.sat_count) {
             for (int o = 16; o > 0; o >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, o);
             if (lane == 0 && sat) atomicAdd(p.sat_count, (unsigned long long)sat);
+        }
+        if (p.range_count) {
+            for (int o = 16; o > 0; o >>= 1) ovf += __shfl_xor_sync(0xffffffffu, ovf, o);
+            if (lane == 0 && ovf) atomicAdd(p.range_count, (unsigned long long)ovf);
         }
     }
 

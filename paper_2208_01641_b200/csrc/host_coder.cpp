@@ -166,6 +166,7 @@ struct lic_rans_tables {
     std::vector<uint32_t> cdf;
     std::vector<EncSym> enc;        // n_rows x nsym
     std::vector<uint8_t> bucket;    // n_rows x 4096: symbol holding slot (u << 4)
+    bool any_zero = false;          // some (row, symbol) has frequency 0 (cannot be encoded)
 };
 
 extern "C" lic_status lic_rans_prepare(const uint32_t* cdf, uint32_t n_rows, uint32_t row_len, int sym_min,
@@ -182,6 +183,7 @@ extern "C" lic_status lic_rans_prepare(const uint32_t* cdf, uint32_t n_rows, uin
         for (uint32_t s = 0; s < t->nsym; ++s) {
             if (c[s + 1] < c[s]) { delete t; return LIC_EINVAL; }
             const uint32_t start = c[s], freq = c[s + 1] - c[s];
+            if (freq == 0) t->any_zero = true;
             EncSym& e = t->enc[(size_t)r * t->nsym + s];
             e.xmax = ((kRansLow >> kProbBits) << 8) * freq;
             e.cmpl = (uint16_t)((kProbScale - freq) & 0xFFFF);
@@ -467,7 +469,9 @@ lic_status dec_group(const lic_rans_tables* tab, const uint8_t* const* in, const
 
 // Range checks hoisted out of the coding loops (vectorisable): every row < n_rows and, for the
 // encoder, every symbol inside the table's support.
-bool validate_planes(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row, size_t n) {
+// rows in range, symbols inside the table, and (tables with zero-frequency entries only)
+// every symbol of nonzero frequency in its row: row[i], or the channel i / hw of the plane
+bool validate_planes(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row, size_t n, size_t hw) {
     uint32_t bad = 0;
     if (row) {
         const uint8_t nr = (uint8_t)std::min<uint32_t>(t->n_rows, 255);
@@ -477,6 +481,12 @@ bool validate_planes(const lic_rans_tables* t, const int8_t* sym, const uint8_t*
     if (sym) {
         const int smin = t->sym_min, ns = (int)t->nsym;
         for (size_t i = 0; i < n; ++i) bad |= (uint32_t)((unsigned)((int)sym[i] - smin) >= (unsigned)ns);
+        if (bad == 0 && t->any_zero) {
+            for (size_t i = 0; i < n && !bad; ++i) {
+                const size_t r = row ? row[i] : (hw ? i / hw : 0);
+                if (r >= t->n_rows || t->enc[r * t->nsym + (size_t)((int)sym[i] - smin)].xmax == 0) bad = 1;
+            }
+        }
     }
     return bad == 0;
 }
@@ -739,7 +749,7 @@ extern "C" lic_status lic_rans_encode_slabs(const lic_rans_tables* t, const int8
     SlabGeom g;
     if (!slab_geom(plane, K, g)) return LIC_EINVAL;
     if (g.hw * plane.c && !sym) return LIC_EINVAL;
-    if (!validate_planes(t, sym, row, g.hw * plane.c)) return LIC_EINVAL;
+    if (!validate_planes(t, sym, row, g.hw * plane.c, g.hw)) return LIC_EINVAL;
     if (!row && plane.c > t->n_rows) return LIC_EINVAL;
     // per-slab scratch regions: 2 bytes per symbol + 8 (renormalisation emits <= 16 bits per symbol)
     thread_local std::vector<uint8_t> scratch;
@@ -796,7 +806,7 @@ extern "C" lic_status lic_rans_decode_slabs(const lic_rans_tables* t, const uint
     SlabGeom g;
     if (!slab_geom(plane, K, g)) return LIC_EINVAL;
     if (g.hw * plane.c && !sym_out) return LIC_EINVAL;
-    if (!validate_planes(t, nullptr, row, g.hw * plane.c)) return LIC_EINVAL;
+    if (!validate_planes(t, nullptr, row, g.hw * plane.c, g.hw)) return LIC_EINVAL;
     if (!row && plane.c > t->n_rows) return LIC_EINVAL;
     if (!in || len < 4 * (size_t)K) return LIC_ECORRUPT;
     const uint8_t* sp[64];

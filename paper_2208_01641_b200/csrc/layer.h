@@ -84,6 +84,8 @@ struct ConvParams {
                                       // phases packed into N: column j = phase (j>>2), channel (j&3)
     int crop_top, crop_left, crop_H, crop_W;
     unsigned long long* sat_count;    // saturation counter (nullable)
+    unsigned long long* range_count;  // activations outside the fp16 range (|x| > 65504), stored
+                                      // saturated to +-65504 (nullable; R16d)
     unsigned long long* trace;        // test-only: per-tile clock64 events of CTA 0 (nullable)
     int dbg_nostore;                  // test-only experiment switch: skip activation stores
     int pdl;                          // launched with programmatic stream serialization: constants and

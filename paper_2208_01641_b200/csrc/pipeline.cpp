@@ -60,6 +60,7 @@ struct Slot {
 
 struct GpuTask { GpuKind kind; int slot; };
 struct Pending { GpuTask task; cudaEvent_t done; double t_issue; };
+constexpr size_t kMaxPendingCap = 16;       // GPU tasks in flight at most (env LIC_MAX_PENDING <= this)
 struct CpuTask { CpuKind kind; int slot; int frame; };
 
 }  // namespace
@@ -110,7 +111,9 @@ struct lic_pipeline {
     cudaStream_t cstream = nullptr;         // host -> device copies
     cudaStream_t dstream = nullptr;         // device -> host copies (the other copy engine)
     bool in_host = false, out_host = false; // caller's frames in host memory (staged per slot)
-    std::vector<cudaEvent_t> events;        // completion events, recycled
+    std::vector<cudaEvent_t> events;        // cross-stream join events, recycled as a ring
+    std::vector<cudaEvent_t> done_events;   // one per in-flight task (kMaxPendingCap), from a free list
+    std::vector<cudaEvent_t> done_free;
     std::deque<Pending> pending;            // issued, not yet completed (FIFO)
     // threading
     std::mutex mu;
@@ -265,6 +268,7 @@ extern "C" void lic_pipeline_close(lic_pipeline* p) {
     if (p->dstream) cudaStreamSynchronize(p->dstream);
     if (p->stream2) cudaStreamSynchronize(p->stream2);
     for (cudaEvent_t e : p->events) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->done_events) cudaEventDestroy(e);
     if (p->stream2) cudaStreamDestroy(p->stream2);
     if (p->codec2) lic_close(p->codec2);
     if (p->stream) cudaStreamDestroy(p->stream);
@@ -395,13 +399,19 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
             }
         }
     }
+    // join events only order streams (a wait captures the event when it is enqueued, so the
+    // ring may recycle them); a task's completion event is waited on later by the control
+    // thread and must not be re-recorded before then: those come from their own free list
     p->events.resize(32);
-    for (auto& e : p->events)
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
-            cudaGetLastError();
-            lic_pipeline_close(p);
-            return LIC_ECUDA;
-        }
+    p->done_events.resize(kMaxPendingCap);
+    for (auto* v : {&p->events, &p->done_events})
+        for (auto& e : *v)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+                cudaGetLastError();
+                lic_pipeline_close(p);
+                return LIC_ECUDA;
+            }
+    p->done_free = p->done_events;
     for (uint32_t i = 0; i < cfg->coder_threads; ++i) p->workers.emplace_back(worker_main, p);
     *out = p;
     return LIC_OK;
@@ -517,7 +527,9 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
     // oldest issued task is retired by waiting on its event, which then releases its
     // coder tasks (ENC, IDX) or its slot (DEC).
     size_t kMaxPending = 5;
-    if (const char* e = std::getenv("LIC_MAX_PENDING")) kMaxPending = (size_t)std::max(1, std::min(16, atoi(e)));
+    if (const char* e = std::getenv("LIC_MAX_PENDING"))
+        kMaxPending = (size_t)std::max(1, std::min((int)kMaxPendingCap, atoi(e)));
+    p->done_free = p->done_events;
     size_t ev_next = 0;
     for (;;) {
         GpuTask t{};
@@ -555,7 +567,8 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         }
         if (issue) {
             const double g0 = now_s();
-            cudaEvent_t ev = next_event(p, ev_next);
+            cudaEvent_t ev = p->done_free.back();          // pending.size() < kMaxPending <= cap
+            p->done_free.pop_back();
             lic_status st = gpu_call(p, t, ev, ev_next);
             std::lock_guard<std::mutex> g(p->mu);
             if (st) { p->err = st; break; }
@@ -573,6 +586,7 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         const cudaError_t ce = cudaEventSynchronize(pd.done);
         const double g1 = now_s();
         std::lock_guard<std::mutex> g(p->mu);
+        p->done_free.push_back(pd.done);
         p->gpu_busy += g1 - std::max(w0, pd.t_issue);
         if (ce != cudaSuccess) { p->err = LIC_ECUDA; break; }
         t = pd.task;

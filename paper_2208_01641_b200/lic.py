@@ -76,6 +76,11 @@ _L.lic_launch_count.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64)]
 _L.lic_set_zero_copy.argtypes = [_P, _i]
 _L.lic_trace.argtypes = [_P, _i, _i]
 _L.lic_trace_read.argtypes = [_P, _P, _sz]
+_L.lic_workspace_bytes.argtypes = [_P, _u32]
+_L.lic_workspace_bytes.restype = _sz
+_L.lic_bind_workspace.argtypes = [_P, _P, _sz]
+_L.lic_max_batch.argtypes = [_P, ctypes.POINTER(_u32)]
+_L.lic_range_count.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64), _i]
 
 
 
@@ -328,7 +333,8 @@ class Codec:
         buf = (ctypes.c_uint8 * len(licw)).from_buffer_copy(licw)
         st = _L.lic_open(buf, len(licw), device, height, width, max_batch, precision, ctypes.byref(self._h))
         if st:
-            raise LicError(st, "lic_open")
+            msg = _L.lic_last_error(None)
+            raise LicError(st, "lic_open" + (f": {msg.decode()}" if msg else ""))
         self.height, self.width, self.max_batch = height, width, max_batch
         y, z, k = Shape(), Shape(), _i()
         _L.lic_shapes(self._h, ctypes.byref(y), ctypes.byref(z), ctypes.byref(k))
@@ -398,6 +404,30 @@ class Codec:
         a, r = ctypes.c_uint64(), ctypes.c_uint64()
         _L.lic_buf_stats(self._h, ctypes.byref(a), ctypes.byref(r))
         return a.value, r.value
+
+    # -- workspace (PAPER.md:105 pooled device memory; the caller may own it)
+    def workspace_bytes(self, batch=0):
+        return int(_L.lic_workspace_bytes(self._h, batch))
+
+    def bind_workspace(self, buf, nbytes=None):
+        """Use caller-owned device memory (a torch tensor or a device address) as the
+        codec's workspace; returns the resulting max batch.  The caller keeps `buf` alive."""
+        if nbytes is None:
+            nbytes = buf.numel() * buf.element_size()
+        self._ws = buf                                  # keep the owner alive with the codec
+        self._chk(_L.lic_bind_workspace(self._h, _ptr(buf), nbytes), "lic_bind_workspace")
+        return self.max_batch_now()
+
+    def max_batch_now(self):
+        b = _u32()
+        self._chk(_L.lic_max_batch(self._h, ctypes.byref(b)), "lic_max_batch")
+        return b.value
+
+    def range_count(self, reset=True):
+        """Activations stored saturated to the fp16 range since the last reset (lic_range_count)."""
+        n = ctypes.c_uint64()
+        self._chk(_L.lic_range_count(self._h, ctypes.byref(n), int(reset)), "lic_range_count")
+        return n.value
 
     def set_zero_copy(self, on=True):
         self._chk(_L.lic_set_zero_copy(self._h, int(on)), "lic_set_zero_copy")

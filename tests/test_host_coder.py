@@ -206,3 +206,24 @@ def test_slab_substreams_simd_corrupt_fuzz(lic, K):
             t.decode(bytes(bb), sym.shape, rows=idx, substreams=K)
         except lic.CorruptStream:
             pass
+
+
+@pytest.mark.parametrize("K", [1, 2, 16])
+def test_zero_frequency_symbol_rejected(lic, K):
+    """A table may hold zero-frequency entries (lic_rans_prepare accepts them), but a symbol
+    with frequency 0 cannot be coded: every encoder (plain, slabs, AVX-512 lanes) returns
+    LIC_EINVAL, like lic_rans_encode, instead of a stream that does not decode."""
+    L = 2
+    row = np.array([0, 100, 100, 65000, 65436, 65536], np.uint32)          # symbol -1 has frequency 0
+    cdf = np.stack([row] * 16)
+    t = lic.RansTables(cdf, sym_min=-L)
+    sym = np.zeros((16, 4, 4), np.int8)
+    sym[3, 1, 2] = -1
+    with pytest.raises(lic.LicError) as e:
+        t.encode(sym, substreams=K)
+    assert e.value.status == lic.LIC_EINVAL
+    with pytest.raises(lic.LicError):
+        lic.rans_encode(sym, cdf, sym_min=-L)
+    sym[3, 1, 2] = 1                                                        # nonzero frequency: fine
+    data = t.encode(sym, substreams=K)
+    assert np.array_equal(t.decode(data, sym.shape, substreams=K), sym)
