@@ -259,11 +259,17 @@ typedef struct {
     uint32_t coder;           /* 0: 32-bit rANS over the codec's +-L tables (above); 1: rans64 + bypass escape
                                  (lic_rans64_*, R23) with Gaussian tables (tail 1e-9) on the
                                  codec's scales (lic_sigmas); one string per plane, substreams ignored */
+    float pace_fps;           /* > 0: paced source -- batch i is submitted at t0 + i * batch / pace_fps and its
+                                 latency counts from that submission (queueing included);
+                                 0: every frame is available at the start, latency counts from the
+                                 batch's admission into a slot */
+    uint32_t timeline;        /* 1: record lic_pipeline_timeline events for the run */
 } lic_pipeline_config;
 typedef struct {
     uint64_t frames;          /* frames completed */
     double seconds;           /* wall time of the run */
-    double latency_p50_ms, latency_p95_ms, latency_max_ms; /* per batch: encode start -> decode end */
+    double latency_p50_ms, latency_p95_ms, latency_max_ms; /* per batch: submission (paced) or slot admission
+                                                              (unpaced) -> decode complete */
     uint64_t y_bytes, z_bytes;/* total bitstream bytes */
     uint64_t symbol_mismatches; /* decoded != encoded symbols (must be 0: lossless) */
     double gpu_busy_s, coder_busy_s; /* summed busy time of the GPU thread / coder threads */
@@ -275,6 +281,20 @@ void lic_pipeline_close(lic_pipeline* p);
  * nframes must be a multiple of cfg->batch. */
 lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, uint32_t nframes, void* frames_out,
                             lic_pipeline_stats* stats);
+/* Timeline of the last run (cfg.timeline = 1), the evidence for the overlap the paper's
+ * architecture is built on ("the GPU and CPU workloads ... are executed
+ * concurrently").  One record per GPU task (kind 0 encode, 1 decoder GPU1, 2 decoder GPU2;
+ * lane = the stream: 0 main, 1 GPU1's own stream; start / end = device time of the task's
+ * first / last kernel from CUDA events) and per coder task (kind 3 = E(y), E(z) and decoder
+ * CPU1, kind 4 = decoder CPU2; lane = worker thread; host clock).  t_ready = when the task
+ * could have started (slot free / submitted, or its inputs decoded).  Times in ms since the
+ * run started.  *n = the number of records; LIC_ENOSPACE if cap is smaller (out holds cap). */
+typedef struct {
+    uint32_t kind, lane;
+    int32_t batch, frame;     /* frame within the batch; -1 for GPU tasks */
+    double t_ready_ms, t_start_ms, t_end_ms;
+} lic_timeline_event;
+lic_status lic_pipeline_timeline(const lic_pipeline* p, lic_timeline_event* out, size_t cap, size_t* n);
 /* strings of frame i of the last run (keep_bitstreams = 1); z is NULL/0 for factorized. */
 lic_status lic_pipeline_bitstream(const lic_pipeline* p, uint32_t frame, const uint8_t** y, size_t* y_len,
                                   const uint8_t** z, size_t* z_len);

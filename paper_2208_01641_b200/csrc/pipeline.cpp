@@ -58,10 +58,10 @@ struct Slot {
     double t_start = 0;
 };
 
-struct GpuTask { GpuKind kind; int slot; };
+struct GpuTask { GpuKind kind; int slot; double t_ready; };
 struct Pending { GpuTask task; cudaEvent_t done; double t_issue; };
 constexpr size_t kMaxPendingCap = 16;       // GPU tasks in flight at most (env LIC_MAX_PENDING <= this)
-struct CpuTask { CpuKind kind; int slot; int frame; };
+struct CpuTask { CpuKind kind; int slot; int frame; double t_ready; };
 
 }  // namespace
 
@@ -115,6 +115,13 @@ struct lic_pipeline {
     std::vector<cudaEvent_t> done_events;   // one per in-flight task (kMaxPendingCap), from a free list
     std::vector<cudaEvent_t> done_free;
     std::deque<Pending> pending;            // issued, not yet completed (FIFO)
+    // timeline (cfg.timeline): one record per GPU task / coder task of the last run
+    std::vector<lic_timeline_event> tl;
+    std::vector<cudaEvent_t> tl_ev;         // timing events: base, then [start, end] per GPU task
+    std::vector<std::pair<size_t, size_t>> tl_gpu;   // (record, first event) of every GPU task
+    size_t tl_ev_next = 0;
+    double t_run0 = 0;
+    std::vector<double> slot_free_t;        // when each slot was last released
     // threading
     std::mutex mu;
     std::condition_variable cv_gpu, cv_cpu;
@@ -192,8 +199,8 @@ static void coder_task64(lic_pipeline* p, const CpuTask& t) {
     if (st && !p->err) p->err = st;
     p->mismatches += mism;
     if (--s.remaining == 0) {
-        if (t.kind == C_ONE && p->hyper) p->gpu_q.push_back({G_IDX, t.slot});
-        else p->gpu_q.push_back({G_DEC, t.slot});
+        if (t.kind == C_ONE && p->hyper) p->gpu_q.push_back({G_IDX, t.slot, now_s()});
+        else p->gpu_q.push_back({G_DEC, t.slot, now_s()});
         p->cv_gpu.notify_one();
     }
 }
@@ -229,13 +236,13 @@ static void coder_task(lic_pipeline* p, const CpuTask& t) {
     if (st && !p->err) p->err = st;
     p->mismatches += mism;
     if (--s.remaining == 0) {
-        if (t.kind == C_ONE && p->hyper) p->gpu_q.push_back({G_IDX, t.slot});
-        else p->gpu_q.push_back({G_DEC, t.slot});
+        if (t.kind == C_ONE && p->hyper) p->gpu_q.push_back({G_IDX, t.slot, now_s()});
+        else p->gpu_q.push_back({G_DEC, t.slot, now_s()});
         p->cv_gpu.notify_one();
     }
 }
 
-static void worker_main(lic_pipeline* p) {
+static void worker_main(lic_pipeline* p, int widx) {
     for (;;) {
         CpuTask t;
         {
@@ -247,10 +254,14 @@ static void worker_main(lic_pipeline* p) {
             ++p->active;
         }
         const double t0 = now_s();
+        const int batch = p->slots[t.slot].batch;
         coder_task(p, t);
-        const double dt = now_s() - t0;
+        const double t1 = now_s(), dt = t1 - t0;
         std::lock_guard<std::mutex> g(p->mu);
         p->coder_busy += dt;
+        if (p->cfg.timeline)
+            p->tl.push_back({3u + (uint32_t)t.kind, (uint32_t)widx, batch, t.frame, (t.t_ready - p->t_run0) * 1e3,
+                             (t0 - p->t_run0) * 1e3, (t1 - p->t_run0) * 1e3});
         if (--p->active == 0) p->cv_idle.notify_all();
     }
 }
@@ -269,6 +280,7 @@ extern "C" void lic_pipeline_close(lic_pipeline* p) {
     if (p->stream2) cudaStreamSynchronize(p->stream2);
     for (cudaEvent_t e : p->events) cudaEventDestroy(e);
     for (cudaEvent_t e : p->done_events) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->tl_ev) cudaEventDestroy(e);
     if (p->stream2) cudaStreamDestroy(p->stream2);
     if (p->codec2) lic_close(p->codec2);
     if (p->stream) cudaStreamDestroy(p->stream);
@@ -412,7 +424,7 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
                 return LIC_ECUDA;
             }
     p->done_free = p->done_events;
-    for (uint32_t i = 0; i < cfg->coder_threads; ++i) p->workers.emplace_back(worker_main, p);
+    for (uint32_t i = 0; i < cfg->coder_threads; ++i) p->workers.emplace_back(worker_main, p, (int)i);
     *out = p;
     return LIC_OK;
 }
@@ -438,16 +450,26 @@ static lic_status gpu_call(lic_pipeline* p, const GpuTask& t, cudaEvent_t done, 
         if (!st && cudaMemcpyAsync(dst, src, n, k, cs) != cudaSuccess) st = LIC_ECUDA;
     };
     auto to_k = [&]() { if (!st && !join(p, p->cstream, p->stream, ev_next)) st = LIC_ECUDA; };
+    // timeline: device timestamps around the task's kernels on the stream they run on
+    const bool tl = p->cfg.timeline && p->tl_ev_next + 2 <= p->tl_ev.size();
+    size_t ev0 = 0;
+    auto mark = [&](cudaStream_t ks, int end) {
+        if (!tl || st) return;
+        if (!end) ev0 = p->tl_ev_next;
+        if (cudaEventRecord(p->tl_ev[p->tl_ev_next++], ks) != cudaSuccess) st = LIC_ECUDA;
+    };
     auto to_c = [&]() { if (!st && !join(p, p->stream, p->dstream, ev_next)) st = LIC_ECUDA; };
     switch (t.kind) {
     case G_ENC: {
         const uint8_t* fr = p->in + b * fb;
         if (p->in_host) { cp(s.d_fin, fr, fb, cudaMemcpyHostToDevice); to_k(); fr = s.d_fin; }
+        mark(p->stream, 0);
         if (!st)
             st = p->cfg.u8 ? lic_encode_u8(p->codec, fr, B, s.d_ysym, p->hyper ? s.d_yidx : nullptr,
                                            p->hyper ? s.d_zsym : nullptr, nullptr, p->stream)
                            : lic_encode(p->codec, (const float*)fr, B, s.d_ysym, p->hyper ? s.d_yidx : nullptr,
                                         p->hyper ? s.d_zsym : nullptr, nullptr, p->stream);
+        mark(p->stream, 1);
         to_c();
         cp(s.y_sym, s.d_ysym, B * p->ny, cudaMemcpyDeviceToHost);
         if (p->hyper) {
@@ -461,7 +483,9 @@ static lic_status gpu_call(lic_pipeline* p, const GpuTask& t, cudaEvent_t done, 
         cudaStream_t ks = p->codec2 ? p->stream2 : p->stream;
         cp(s.d_zdec, s.z_dec, B * p->nz, cudaMemcpyHostToDevice);
         if (!st && !join(p, p->cstream, ks, ev_next)) st = LIC_ECUDA;
+        mark(ks, 0);
         if (!st) st = lic_hyper_indexes(cc, s.d_zdec, B, s.d_idxdec, ks);
+        mark(ks, 1);
         if (!st && !join(p, ks, p->dstream, ev_next)) st = LIC_ECUDA;
         cp(s.idx_dec, s.d_idxdec, B * p->ny, cudaMemcpyDeviceToHost);
         break;
@@ -471,9 +495,11 @@ static lic_status gpu_call(lic_pipeline* p, const GpuTask& t, cudaEvent_t done, 
         to_k();
         uint8_t* fr = p->out + b * fb;
         uint8_t* dst = p->out_host ? s.d_fout : fr;
+        mark(p->stream, 0);
         if (!st)
             st = p->cfg.u8 ? lic_decode_u8(p->codec, s.d_ydec, B, dst, p->stream)
                            : lic_decode(p->codec, s.d_ydec, B, (float*)dst, p->stream);
+        mark(p->stream, 1);
         to_c();
         if (p->out_host) cp(fr, s.d_fout, fb, cudaMemcpyDeviceToHost);
         break;
@@ -481,6 +507,12 @@ static lic_status gpu_call(lic_pipeline* p, const GpuTask& t, cudaEvent_t done, 
     }
     // every task ends with kernels -> dstream (possibly no copies after them)
     if (!st && cudaEventRecord(done, p->dstream) != cudaSuccess) st = LIC_ECUDA;
+    if (tl && !st) {
+        std::lock_guard<std::mutex> g(p->mu);
+        p->tl_gpu.push_back({p->tl.size(), ev0});
+        p->tl.push_back({(uint32_t)t.kind, (uint32_t)(t.kind == G_IDX && p->codec2 ? 1 : 0), s.batch, -1,
+                         (t.t_ready - p->t_run0) * 1e3, 0.0, 0.0});
+    }
     return st;
 }
 
@@ -521,7 +553,30 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         }
     }
     const uint64_t launches0 = lic_internal_launches(p->codec) + lic_internal_launches(p->codec2);
+    // timeline: a base event, then two timing events per GPU task
+    p->tl.clear();
+    p->tl_gpu.clear();
+    p->tl_ev_next = 0;
+    if (p->cfg.timeline) {
+        const size_t need = 1 + 2 * (size_t)p->nbatches * (p->hyper ? 3 : 2);
+        while (p->tl_ev.size() < need) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); return LIC_ECUDA; }
+            p->tl_ev.push_back(e);
+        }
+    }
+    p->slot_free_t.assign(p->slots.size(), 0.0);
     const double t_run0 = now_s();
+    p->t_run0 = t_run0;
+    if (p->cfg.timeline) {
+        if (cudaEventRecord(p->tl_ev[0], p->stream) != cudaSuccess) return LIC_ECUDA;
+        p->tl_ev_next = 1;
+    }
+    // paced submission (cfg.pace_fps > 0): batch i is submitted at t_run0 + i * batch / pace_fps
+    // and its latency counts from then (queueing included); unpaced, every frame is there
+    // at the start and latency counts from the batch's admission into a slot
+    const double pace = p->cfg.pace_fps > 0 ? (double)p->cfg.pace_fps : 0.0;
+    auto t_submit = [&](int i) { return t_run0 + (double)i * (double)B / pace; };
     // GPU control loop.  GPU tasks are issued asynchronously on p->stream (at most
     // kMaxPending in flight, env LIC_MAX_PENDING) so the device never idles while ready work exists; the
     // oldest issued task is retired by waiting on its event, which then releases its
@@ -538,12 +593,20 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
             std::unique_lock<std::mutex> lk(p->mu);
             auto can_enc = [&] {
                 if (p->next_enc >= p->nbatches || p->free_slots.empty()) return false;
+                if (pace > 0 && now_s() < t_submit(p->next_enc)) return false;
                 return !p->cfg.serial || p->done == p->next_enc;
             };
             auto have_ready = [&] { return !p->gpu_q.empty() || can_enc(); };
-            p->cv_gpu.wait(lk, [&] {
-                return p->err || p->done == p->nbatches || !p->pending.empty() || have_ready();
-            });
+            auto wake = [&] { return p->err || p->done == p->nbatches || !p->pending.empty() || have_ready(); };
+            if (pace > 0 && p->next_enc < p->nbatches) {
+                // sleep at most until the next submission is due
+                const auto due = clk::time_point(std::chrono::duration_cast<clk::duration>(
+                    std::chrono::duration<double>(t_submit(p->next_enc))));
+                p->cv_gpu.wait_until(lk, due, wake);
+                if (!wake()) continue;
+            } else {
+                p->cv_gpu.wait(lk, wake);
+            }
             if (p->err || p->done == p->nbatches) break;
             if (p->pending.size() < kMaxPending && have_ready()) {
                 issue = true;
@@ -559,9 +622,10 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
                 } else {
                     const int s = p->free_slots.back();
                     p->free_slots.pop_back();
-                    p->slots[s].batch = p->next_enc++;
-                    p->slots[s].t_start = now_s();
-                    t = {G_ENC, s};
+                    const int bi = p->next_enc++;
+                    p->slots[s].batch = bi;
+                    p->slots[s].t_start = pace > 0 ? t_submit(bi) : now_s();
+                    t = {G_ENC, s, std::max(pace > 0 ? t_submit(bi) : t_run0, p->slot_free_t[s])};
                 }
             }
         }
@@ -593,7 +657,7 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         Slot& s = p->slots[t.slot];
         if (t.kind == G_ENC || t.kind == G_IDX) {
             s.remaining = (int)B;
-            for (uint32_t f = 0; f < B; ++f) p->cpu_q.push_back({t.kind == G_ENC ? C_ONE : C_TWO, t.slot, (int)f});
+            for (uint32_t f = 0; f < B; ++f) p->cpu_q.push_back({t.kind == G_ENC ? C_ONE : C_TWO, t.slot, (int)f, g1});
             p->cv_cpu.notify_all();
         } else {
             for (uint32_t f = 0; f < B; ++f) {
@@ -606,6 +670,7 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
                 }
             }
             p->lat.push_back((g1 - s.t_start) * 1e3);
+            p->slot_free_t[t.slot] = g1;
             p->free_slots.push_back(t.slot);
             ++p->done;
         }
@@ -616,6 +681,15 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
     cudaStreamSynchronize(p->cstream);
     cudaStreamSynchronize(p->dstream);
     const double t_run1 = now_s();
+    if (p->cfg.timeline && !p->err) {
+        for (const auto& g : p->tl_gpu) {
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, p->tl_ev[0], p->tl_ev[g.second]);
+            cudaEventElapsedTime(&b, p->tl_ev[0], p->tl_ev[g.second + 1]);
+            p->tl[g.first].t_start_ms = a;
+            p->tl[g.first].t_end_ms = b;
+        }
+    }
     // error path: drop queued coder work and wait for tasks already running
     std::unique_lock<std::mutex> g(p->mu);
     p->cpu_q.clear();
@@ -639,6 +713,14 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         stats->gpu_launches = lic_internal_launches(p->codec) + lic_internal_launches(p->codec2) - launches0;
     }
     return p->err;
+}
+
+extern "C" lic_status lic_pipeline_timeline(const lic_pipeline* p, lic_timeline_event* out, size_t cap, size_t* n) {
+    if (!p || !n) return LIC_EINVAL;
+    if (!p->cfg.timeline) return LIC_EINVAL;
+    *n = p->tl.size();
+    if (out) std::memcpy(out, p->tl.data(), std::min(cap, p->tl.size()) * sizeof(lic_timeline_event));
+    return cap < p->tl.size() && out ? LIC_ENOSPACE : LIC_OK;
 }
 
 extern "C" lic_status lic_pipeline_bitstream(const lic_pipeline* p, uint32_t frame, const uint8_t** y, size_t* y_len,

@@ -48,3 +48,15 @@ def stream_digest(ordered) -> str:
         h.update(len(z).to_bytes(8, "little"))
         h.update(z)
     return h.hexdigest()
+
+
+def verify_frames(rank: int, world: int, batch: int, n_global: int):
+    """Frames of the end-of-run bitstream gather: global frames 0 .. n_global-1 whoever holds
+    them, so the gathered, ordered set is the same for every G.  Rank r's local frame i is
+    global frame t = r + G * i; it runs `nv` local frames (whole batches, at least one) and
+    keeps [(i, t)] for t < n_global.  Returns (nv, keep)."""
+    if world < 1 or not 0 <= rank < world or batch < 1:
+        raise ValueError("bad rank/world/batch")
+    keep = [(i, rank + world * i) for i in range(n_global) if rank + world * i < n_global]
+    nv = max(batch, -(-len(keep) // batch) * batch)
+    return nv, keep

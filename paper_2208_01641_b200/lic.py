@@ -87,7 +87,17 @@ _L.lic_range_count.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64), _i]
 class PipelineConfig(ctypes.Structure):
     _fields_ = [("coder_threads", ctypes.c_uint32), ("batch", ctypes.c_uint32), ("inflight", ctypes.c_uint32),
                 ("u8", ctypes.c_int), ("serial", ctypes.c_int), ("keep_bitstreams", ctypes.c_int),
-                ("substreams", ctypes.c_uint32), ("coder", ctypes.c_uint32)]
+                ("substreams", ctypes.c_uint32), ("coder", ctypes.c_uint32), ("pace_fps", ctypes.c_float),
+                ("timeline", ctypes.c_uint32)]
+
+
+class TimelineEvent(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_uint32), ("lane", ctypes.c_uint32), ("batch", ctypes.c_int32),
+                ("frame", ctypes.c_int32), ("t_ready_ms", ctypes.c_double), ("t_start_ms", ctypes.c_double),
+                ("t_end_ms", ctypes.c_double)]
+
+
+TIMELINE_KINDS = ["gpu_encode", "gpu_hyper_indexes", "gpu_decode", "coder_enc+dec_z", "coder_dec_y"]
 
 
 class PipelineStats(ctypes.Structure):
@@ -105,6 +115,7 @@ _L.lic_pipeline_open.argtypes = [_P, ctypes.POINTER(PipelineConfig), ctypes.POIN
 _L.lic_pipeline_close.argtypes = [_P]
 _L.lic_pipeline_close.restype = None
 _L.lic_pipeline_run.argtypes = [_P, _P, _u32, _P, ctypes.POINTER(PipelineStats)]
+_L.lic_pipeline_timeline.argtypes = [_P, ctypes.POINTER(TimelineEvent), _sz, ctypes.POINTER(_sz)]
 _L.lic_pipeline_bitstream.argtypes = [_P, _u32, ctypes.POINTER(ctypes.POINTER(ctypes.c_uint8)),
                                       ctypes.POINTER(_sz), ctypes.POINTER(ctypes.POINTER(ctypes.c_uint8)),
                                       ctypes.POINTER(_sz)]
@@ -503,11 +514,12 @@ class Pipeline:
     """lic_pipeline: GPU control thread (the caller) + native coder worker pool."""
 
     def __init__(self, codec: Codec, coder_threads: int, batch: int, inflight: int = 2, u8: bool = True,
-                 serial: bool = False, keep_bitstreams: bool = False, substreams: int = 1, coder: int = 0):
+                 serial: bool = False, keep_bitstreams: bool = False, substreams: int = 1, coder: int = 0,
+                 pace_fps: float = 0.0, timeline: bool = False):
         self.codec = codec
         self.substreams = substreams
         self.cfg = PipelineConfig(coder_threads, batch, inflight, int(u8), int(serial), int(keep_bitstreams),
-                                  substreams, coder)
+                                  substreams, coder, float(pace_fps), int(timeline))
         self._h = _P()
         st = _L.lic_pipeline_open(codec.handle, ctypes.byref(self.cfg), ctypes.byref(self._h))
         if st:
@@ -520,6 +532,20 @@ class Pipeline:
         if rc:
             raise LicError(rc, "lic_pipeline_run: " + (_L.lic_last_error(self.codec.handle) or b"").decode())
         return st.as_dict()
+
+    def timeline(self):
+        """lic_pipeline_timeline: list of dicts (kind name, lane, batch, frame, ready / start / end ms)."""
+        n = _sz()
+        self._chk_rc(_L.lic_pipeline_timeline(self._h, None, 0, ctypes.byref(n)), "lic_pipeline_timeline")
+        buf = (TimelineEvent * max(1, n.value))()
+        self._chk_rc(_L.lic_pipeline_timeline(self._h, buf, n.value, ctypes.byref(n)), "lic_pipeline_timeline")
+        return [dict(kind=TIMELINE_KINDS[e.kind], lane=e.lane, batch=e.batch, frame=e.frame, ready=e.t_ready_ms,
+                     start=e.t_start_ms, end=e.t_end_ms) for e in buf[:n.value]]
+
+    @staticmethod
+    def _chk_rc(rc, what):
+        if rc:
+            raise LicError(rc, what)
 
     def bitstream(self, i):
         y, z = ctypes.POINTER(ctypes.c_uint8)(), ctypes.POINTER(ctypes.c_uint8)()

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2208_01641_b200.dist import frames_for_rank, gather_bitstreams, stream_digest
+from paper_2208_01641_b200.dist import frames_for_rank, gather_bitstreams, stream_digest, verify_frames
 
 N_FRAMES = 7
 
@@ -32,12 +32,19 @@ def _frame_strings(t):
     return y, z
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, bench_path=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    local = {t: _frame_strings(t) for t in frames_for_rank(N_FRAMES, rank, world)}
+    if bench_path:
+        # bench.py's end-of-run gather: local frame i of rank r is global frame r + G*i, the
+        # verification run covers global frames 0..7 whoever holds them (batch 4)
+        nv, keep = verify_frames(rank, world, 4, 8)
+        assert nv % 4 == 0 and all(t < 8 for _, t in keep)
+        local = {t: _frame_strings(t) for _, t in keep}
+    else:
+        local = {t: _frame_strings(t) for t in frames_for_rank(N_FRAMES, rank, world)}
     merged = gather_bitstreams(local, rank, world)
     if rank == 0:
         q.put(([i for i, _, _ in merged], stream_digest(merged)))
@@ -76,3 +83,36 @@ def test_gather_world2_matches_world1():
         assert p.exitcode == 0
     assert idx == list(range(N_FRAMES))
     assert digest == ref_digest
+
+
+def test_verify_frames_cover_the_same_set_for_every_world():
+    """bench.py's gather set (global frames 0..7) is the same for G = 1, 2, 4, 8, so the
+    gathered digest is G-invariant."""
+    ref = stream_digest(gather_bitstreams({t: _frame_strings(t) for t in range(8)}, 0, 1))
+    for world in (1, 2, 4, 8):
+        merged = {}
+        for r in range(world):
+            nv, keep = verify_frames(r, world, 4, 8)
+            assert nv >= 4 and nv % 4 == 0 and len(keep) <= nv
+            for i, t in keep:
+                assert t == r + world * i and t not in merged
+                merged[t] = _frame_strings(t)
+        assert sorted(merged) == list(range(8))
+        assert stream_digest(gather_bitstreams(merged, 0, 1)) == ref
+
+
+def test_bench_gather_world2_matches_world1():
+    """The same path with two gloo processes (the NCCL path of bench.py uses the same calls)."""
+    ref = stream_digest(gather_bitstreams({t: _frame_strings(t) for t in range(8)}, 0, 1))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    idx, digest = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert idx == list(range(8))
+    assert digest == ref

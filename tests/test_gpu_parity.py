@@ -198,7 +198,7 @@ def test_bitstreams_bit_exact(codec, hyper, lic):
         # every build bitstream decodes losslessly with the oracle decoder (c19 iii)
         assert np.array_equal(O.rans_decode(yb, yi[b].astype(np.int32), tabs.gauss).reshape(ys[b].shape), ys[b])
     print(f"frames whose planes differ from the oracle's: {len(plane_mismatch)} of {B}")
-    assert plane_mismatch == [], f"frames {plane_mismatch}: GPU planes != oracle planes
+    assert plane_mismatch == [], f"frames {plane_mismatch}: GPU planes != oracle planes"
 
 
 def test_factorized_c1(lic):
