@@ -1070,6 +1070,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     }
                     guard16(x[j], ovf);
                 }
+                if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_P2);
                 // the accumulator is in registers: release TMEM before storing
                 tc_fence_before();
                 __syncwarp();
@@ -1083,11 +1084,13 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         const int nblk = p.BN >> 6;
                         for (int b0 = 0; b0 < nblk; b0 += qslots) {
                             q_acquire(0);
+                            if (threadIdx.x == 128 && b0 == 0) LIC_TRACE(it, T_EPI_ACQ);
 #pragma unroll
                             for (int j = 0; j < GC; ++j) {
                                 const int cb = g * G + j * 16, blk = cb >> 6;
                                 if (blk >= b0 && blk < b0 + qslots) stage16(x[j], cb, blk - b0);
                             }
+                            if (threadIdx.x == 128 && b0 == 0) LIC_TRACE(it, T_EPI_STAGED);
                             q_flush(b0, min(qslots, nblk - b0), 0);
                         }
                     } else {

@@ -39,7 +39,7 @@ names = ["mma_s", "mma_e", "norm_i", "epi_s", "epi_x2", "epi_n", "epi_e", "prod_
 bnames = ["b_patch", "b_c0_rdy", "b_c0_done", "b_c1_rdy", "b_c1_done", "mma_k0", "mma_kl", "peerB", "b_raw", "epi_p2", "epi_acq", "epi_stg", "w_halo", "w_b"]
 n = int((t[:, 0] > 0).sum())
 t0 = t[0, 0]
-fused = bool((t[:n, 8] > 0).any() or (t[:n, 13] > 0).any())
+fused = True
 cols = names + (bnames if fused else [])
 print(f"{layer}: {n} tiles traced on CTA 0")
 print("tile " + " ".join(f"{x:>9s}" for x in cols) + "   mma_dur epi_dur  gap(mma_s[i]-mma_e[i-1])")
