@@ -245,8 +245,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     uint64_t* hempty_bar = hfull_bar + 4;           // [4]
     uint64_t* xsq_bar = hempty_bar + 4;             // epilogue -> MMA warp: x^2 written to TMEM
     uint64_t* wres_bar = xsq_bar + 1;               // resident weights landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wres_bar + 1);
-    uint32_t* xsq_cnt = tmem_slot + 1;              // epilogue warps that wrote x^2 (cumulative)
+    // the TMEM base address written by tcgen05.alloc, in a 16-byte granule of its own
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ((p.off_bar + 8u * 34u + 15u) & ~15u));
+    uint32_t* xsq_cnt = tmem_slot + 4;              // epilogue warps that wrote x^2 (cumulative)
     float* s_bias = reinterpret_cast<float*>(smem + p.off_par);   // [cout_pad]
     float* s_beta = s_bias + p.BN * p.n_ntiles;                     // [cout_pad]
     float* s_mu = s_beta + p.BN * p.n_ntiles;                       // [cout_pad]
@@ -403,7 +404,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 // words -> one 16-byte store); the lo plane holds a copy shifted by 4 bytes so
                 // that every K-row segment below is two 8-byte-aligned loads
                 cp_async_wait_all();
-                named_bar_sync(4, kL1Builders);                          // raw[it & 1] complete
+                named_bar_sync_na(4, kL1Builders);                          // raw[it & 1] complete
                 if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_RAW);
                 const uint32_t rw = raw_s + (uint32_t)(it & 1) * kL1RawBytes;
                 const uint32_t sel = 0x3210u + (uint32_t)((3 * ix0) & 3) * 0x1111u;
@@ -423,7 +424,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 }
             } else if (fast) {
                 cp_async_wait_all();
-                named_bar_sync(4, kL1Builders);                          // raw[it & 1] complete
+                named_bar_sync_na(4, kL1Builders);                          // raw[it & 1] complete
                 if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_RAW);
                 const uint32_t rb = raw_s + (uint32_t)(it & 1) * kL1RawBytes + (uint32_t)((3 * ix0) & 3);
 #pragma unroll 4
@@ -487,7 +488,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     }
                 }
             }
-            named_bar_sync(4, kL1Builders);
+            named_bar_sync_na(4, kL1Builders);
             if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_PATCH);
             // next tile's raw bytes (its buffer was last read converting tile it-1, before the
             // raw barrier of this tile)

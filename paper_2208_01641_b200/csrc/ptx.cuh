@@ -122,6 +122,11 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     __syncwarp();
     asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
 }
+// the non-.aligned form: defined for lanes arriving separately (the fused-L1 builders, whose
+// ragged per-lane loops the compiler may leave unconverged at the barrier)
+__device__ __forceinline__ void named_bar_sync_na(uint32_t id, uint32_t nthreads) {
+    asm volatile("barrier.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
+}
 
 // ------------------------------------------------------------------ tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {

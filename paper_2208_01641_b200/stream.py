@@ -203,6 +203,7 @@ class ReceiverStats:
     latency_ms: list = field(default_factory=list)
     handshake: Handshake | None = None
     y_symbols: list = field(default_factory=list)
+    payloads: dict = field(default_factory=dict)        # sequence -> frame payload (keep_payloads)
 
     @property
     def fps(self):
@@ -251,7 +252,7 @@ def run_sender(coder: FrameCoder, frames, sock, target_fps: float, keep_symbols=
     return st
 
 
-def run_receiver(coder: FrameCoder, sock, sink=None, keep_symbols=False):
+def run_receiver(coder: FrameCoder, sock, sink=None, keep_symbols=False, keep_payloads=()):
     """PAPER.md:187 server side: validate the handshake against the local weights, decode every
     frame message, deliver (sequence, frame) to `sink` in order; gaps and reordering are
     counted, a frame that fails to decode is counted and skipped (the stream continues)."""
@@ -281,6 +282,8 @@ def run_receiver(coder: FrameCoder, sock, sink=None, keep_symbols=False):
             else:
                 st.gaps += m.sequence - expect
         expect = max(expect, m.sequence + 1)
+        if m.sequence in keep_payloads:
+            st.payloads[m.sequence] = m.payload
         try:
             k, y, z = unpack_frame(m.payload)
             frame, ys = coder.decode(y, z, k)
@@ -298,7 +301,7 @@ def run_receiver(coder: FrameCoder, sock, sink=None, keep_symbols=False):
 
 
 def loopback(licw: bytes, frames, height: int, width: int, target_fps: float, device: int = 0,
-             substreams: int = 4, keep_symbols=False, corrupt_seq=None, sink=None):
+             substreams: int = 4, keep_symbols=False, corrupt_seq=None, sink=None, keep_payloads=()):
     """Sender and receiver on 127.0.0.1 in one process (two threads, one codec each)."""
     srv = socket.socket(socket.AF_INET, socket.SOCK_STREAM)
     srv.bind(("127.0.0.1", 0))
@@ -310,7 +313,8 @@ def loopback(licw: bytes, frames, height: int, width: int, target_fps: float, de
     def rx():
         conn, _ = srv.accept()
         try:
-            result["rx"] = run_receiver(rx_coder, conn, sink=sink, keep_symbols=keep_symbols)
+            result["rx"] = run_receiver(rx_coder, conn, sink=sink, keep_symbols=keep_symbols,
+                                        keep_payloads=keep_payloads)
         except Exception as e:          # surfaced to the caller below
             result["rx_err"] = e
         finally:

@@ -100,3 +100,34 @@ def test_corrupted_frame_is_counted(S):
     H, W, n = 128, 192, 8
     tx, rx = S.loopback(_blob(), list(synth_frames_u8(n, H, W, seed=9)), H, W, 200.0, corrupt_seq=3)
     assert rx.decode_failures == 1 and rx.frames_received == n - 1 and rx.gaps == 0
+
+
+def test_received_stream_decodes_with_the_oracle(S):
+    """PAPER.md:187-189 end to end against the oracle: the paper's demo codec (factorized +
+    1DN, 1280x720) streamed at 30 FPS; one received frame's wire payload is decoded by the
+    ORACLE (its rANS decoder over the 4 channel-slab substreams, R21, then g_s with
+    1DN) and equals the receiver's frame (u8 +-1); the sender's symbols of that frame are the
+    oracle encoder's (c18 tie rule)."""
+    from oracle import oracle as O
+    from parity import check_symbols
+    from lic_synth import u8_to_f32_chw
+    H, W, n, pick = 720, 1280, 6, 2
+    spec = ModelSpec(kind=0, N=128, M=192, activation=ACT_1DN)
+    w = generate_weights(spec, 0)
+    frames = list(synth_frames_u8(n, H, W, seed=78))
+    got = {}
+    tx, rx = S.loopback(write_licw(spec, w), frames, H, W, 30.0, keep_symbols=True, keep_payloads=(pick,),
+                        sink=lambda s, f: got.__setitem__(s, f))
+    assert rx.frames_received == n and rx.gaps == 0 and rx.frames_out_of_order == 0
+    k, ystr, zstr = S.unpack_frame(rx.payloads[pick])
+    assert zstr is None
+    tabs = O.build_tables(w, False, 32)
+    xp, crop = O.pad_chw(u8_to_f32_chw(frames[pick][None])[0], hyper=False)
+    y_shape = (192, xp.shape[1] // 16, xp.shape[2] // 16)
+    xhat, ys = O.decode_strings(ystr, None, w, tabs, False, y_shape, None, crop, H, W, substreams=k, act=1)
+    assert np.array_equal(ys, tx.y_symbols[pick])
+    ref8 = np.floor(np.moveaxis(xhat, 0, -1).astype(np.float64) * 255 + 0.5)
+    assert np.max(np.abs(got[pick].astype(np.int32) - ref8)) <= 1
+    p = O.encode_planes(xp, w, False, 32, act=1)
+    n_flip = check_symbols(tx.y_symbols[pick], p["y_sym"], p["y"] - w["mu_y"][:, None, None], what="stream y_sym")
+    print(f"oracle decode of received frame {pick}: {len(ystr)} bytes, K = {k}, symbol flips vs oracle encode {n_flip}")
