@@ -90,6 +90,8 @@ struct lic_pipeline {
     lic_codec* codec = nullptr;
     lic_codec* codec2 = nullptr;            // decoder GPU1 (h_s on decoded z) on its own stream
     cudaStream_t stream2 = nullptr;
+    lic_codec* codec3 = nullptr;            // decoder GPU2 (g_s) on its own stream (env LIC_DEC_STREAM=1)
+    cudaStream_t stream3 = nullptr;
     lic_pipeline_config cfg{};
     int hyper = 0;
     lic_shape ys{}, zs{};
@@ -278,11 +280,14 @@ extern "C" void lic_pipeline_close(lic_pipeline* p) {
     if (p->cstream) cudaStreamSynchronize(p->cstream);
     if (p->dstream) cudaStreamSynchronize(p->dstream);
     if (p->stream2) cudaStreamSynchronize(p->stream2);
+    if (p->stream3) cudaStreamSynchronize(p->stream3);
     for (cudaEvent_t e : p->events) cudaEventDestroy(e);
     for (cudaEvent_t e : p->done_events) cudaEventDestroy(e);
     for (cudaEvent_t e : p->tl_ev) cudaEventDestroy(e);
     if (p->stream2) cudaStreamDestroy(p->stream2);
     if (p->codec2) lic_close(p->codec2);
+    if (p->stream3) cudaStreamDestroy(p->stream3);
+    if (p->codec3) lic_close(p->codec3);
     if (p->stream) cudaStreamDestroy(p->stream);
     if (p->cstream) cudaStreamDestroy(p->cstream);
     if (p->dstream) cudaStreamDestroy(p->dstream);
@@ -411,6 +416,19 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
             }
         }
     }
+    // decoder GPU2 on a third codec and stream: its kernels may share the GPU with the next
+    // batches' encode kernels (env LIC_DEC_STREAM=1: on)
+    {
+        const char* e = std::getenv("LIC_DEC_STREAM");
+        if (!p->cfg.serial && e && e[0] == '1') {
+            if ((st = lic_internal_clone(codec, &p->codec3)) != LIC_OK ||
+                cudaStreamCreateWithFlags(&p->stream3, cudaStreamNonBlocking) != cudaSuccess) {
+                cudaGetLastError();
+                lic_pipeline_close(p);
+                return st ? st : LIC_ECUDA;
+            }
+        }
+    }
     // join events only order streams (a wait captures the event when it is enqueued, so the
     // ring may recycle them); a task's completion event is waited on later by the control
     // thread and must not be re-recorded before then: those come from their own free list
@@ -491,16 +509,18 @@ static lic_status gpu_call(lic_pipeline* p, const GpuTask& t, cudaEvent_t done, 
         break;
     }
     case G_DEC: {
+        lic_codec* cc = p->codec3 ? p->codec3 : p->codec;
+        cudaStream_t ks = p->codec3 ? p->stream3 : p->stream;
         cp(s.d_ydec, s.y_dec, B * p->ny, cudaMemcpyHostToDevice);
-        to_k();
+        if (!st && !join(p, p->cstream, ks, ev_next)) st = LIC_ECUDA;
         uint8_t* fr = p->out + b * fb;
         uint8_t* dst = p->out_host ? s.d_fout : fr;
-        mark(p->stream, 0);
+        mark(ks, 0);
         if (!st)
-            st = p->cfg.u8 ? lic_decode_u8(p->codec, s.d_ydec, B, dst, p->stream)
-                           : lic_decode(p->codec, s.d_ydec, B, (float*)dst, p->stream);
-        mark(p->stream, 1);
-        to_c();
+            st = p->cfg.u8 ? lic_decode_u8(cc, s.d_ydec, B, dst, ks)
+                           : lic_decode(cc, s.d_ydec, B, (float*)dst, ks);
+        mark(ks, 1);
+        if (!st && !join(p, ks, p->dstream, ev_next)) st = LIC_ECUDA;
         if (p->out_host) cp(fr, s.d_fout, fb, cudaMemcpyDeviceToHost);
         break;
     }
@@ -510,7 +530,7 @@ static lic_status gpu_call(lic_pipeline* p, const GpuTask& t, cudaEvent_t done, 
     if (tl && !st) {
         std::lock_guard<std::mutex> g(p->mu);
         p->tl_gpu.push_back({p->tl.size(), ev0});
-        p->tl.push_back({(uint32_t)t.kind, (uint32_t)(t.kind == G_IDX && p->codec2 ? 1 : 0), s.batch, -1,
+        p->tl.push_back({(uint32_t)t.kind, (uint32_t)(t.kind == G_IDX && p->codec2 ? 1 : (t.kind == G_DEC && p->codec3 ? 2 : 0)), s.batch, -1,
                          (t.t_ready - p->t_run0) * 1e3, 0.0, 0.0});
     }
     return st;
@@ -552,7 +572,8 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
             p->keep_z.assign(nframes, {});
         }
     }
-    const uint64_t launches0 = lic_internal_launches(p->codec) + lic_internal_launches(p->codec2);
+    const uint64_t launches0 = lic_internal_launches(p->codec) + lic_internal_launches(p->codec2) +
+                               lic_internal_launches(p->codec3);
     // timeline: a base event, then two timing events per GPU task
     p->tl.clear();
     p->tl_gpu.clear();
@@ -678,6 +699,7 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
     // leave nothing running on the streams
     cudaStreamSynchronize(p->stream);
     if (p->stream2) cudaStreamSynchronize(p->stream2);
+    if (p->stream3) cudaStreamSynchronize(p->stream3);
     cudaStreamSynchronize(p->cstream);
     cudaStreamSynchronize(p->dstream);
     const double t_run1 = now_s();
@@ -710,7 +732,8 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         stats->symbol_mismatches = p->mismatches;
         stats->gpu_busy_s = p->gpu_busy;
         stats->coder_busy_s = p->coder_busy;
-        stats->gpu_launches = lic_internal_launches(p->codec) + lic_internal_launches(p->codec2) - launches0;
+        stats->gpu_launches = lic_internal_launches(p->codec) + lic_internal_launches(p->codec2) +
+                              lic_internal_launches(p->codec3) - launches0;
     }
     return p->err;
 }
