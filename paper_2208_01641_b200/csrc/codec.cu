@@ -29,7 +29,8 @@
 
 namespace lic {
 cudaError_t launch_conv_umma(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
-                             const CUtensorMap&, const ConvParams&, int, cudaStream_t);
+                             const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const ConvParams&, int,
+                             cudaStream_t);
 cudaError_t launch_sym_ingest(const int8_t*, const float*, int, int, int, int, __half*, size_t, int, cudaStream_t);
 cudaError_t launch_pack_chw(const float*, int, int, int, int, __half*, size_t, int, cudaStream_t);
 cudaError_t launch_sigma_index(const float*, size_t, const float*, uint8_t*, cudaStream_t);
@@ -136,7 +137,7 @@ struct Layer {
     size_t out_plane = 0;
     char in_id = 0, out_id = 0;   // workspace buffer ('A', 'B', 'Y', 'Z'; 0 = none) -- re-bound by lic_bind_workspace
     ConvParams prm{};
-    CUtensorMap mapA{}, mapB{}, mapG{}, mapOH{}, mapOL{};
+    CUtensorMap mapA{}, mapB{}, mapG{}, mapOH{}, mapOL{}, mapO2{}, mapO3{};
 };
 
 struct lic_codec {
@@ -178,6 +179,7 @@ struct lic_codec {
     int l1_conv_enabled = 1;       // ... converted arithmetically, 8 per item, no LUT (env LIC_L1_CONV=0: LUT)
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
+    int wstage_enabled = 1;        // per-warp output staging in the GDN epilogue (env LIC_WSTAGE=0: quadrant blocks)
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
     std::vector<void*> allocs;          // device allocations to free
@@ -282,30 +284,62 @@ static bool encode_w_map(CUtensorMap* m, const __half* base, int K, int rows, in
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// TMA-store maps of an NHWC fp16 plane, box = one epilogue warp's 32 px x 16 ch
-static bool encode_out_conv_map(CUtensorMap* m, const __half* base, int C, int W, int H, int B, int bw, int bh) {
+// TMA-store maps of an NHWC fp16 plane, box = bc channels x one epilogue quadrant's 32 px:
+// bc = 64 (128-byte rows, 128B swizzle: quadrant blocks) or 32 / 16 (64B / 32B swizzle:
+// per-warp staging rounds)
+static CUtensorMapSwizzle swz_for(int bc) {
+    return bc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : bc == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+}
+static bool encode_out_conv_map(CUtensorMap* m, const __half* base, int C, int W, int H, int B, int bw, int bh,
+                                int bc = 64) {
     EncodeTiledFn enc = get_encode_fn();
     if (!enc) return false;
     cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
     cuuint64_t str[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, 1};      // 64-channel blocks, 128-byte rows
+    cuuint32_t box[4] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, (void*)base, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+               swz_for(bc), CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // sub-pixel phase view of a stride-2 transposed conv output (NHWC, H = 2 Hin, W = 2 Win):
 // dims (C, px, qx = x/2, py, qyb = b*Hin + y/2)
-static bool encode_out_phase_map(CUtensorMap* m, const __half* base, int C, int W, int H, int B, int bw, int bh) {
+static bool encode_out_phase_map(CUtensorMap* m, const __half* base, int C, int W, int H, int B, int bw, int bh,
+                                 int bc = 64) {
     EncodeTiledFn enc = get_encode_fn();
     if (!enc) return false;
     cuuint64_t dims[5] = {(cuuint64_t)C, 2, (cuuint64_t)(W / 2), 2, (cuuint64_t)B * (H / 2)};
     cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)2 * C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)2 * W * C * 2};
-    cuuint32_t box[5] = {64, 1, (cuuint32_t)bw, 1, (cuuint32_t)bh};
+    cuuint32_t box[5] = {(cuuint32_t)bc, 1, (cuuint32_t)bw, 1, (cuuint32_t)bh};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, (void*)base, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+               swz_for(bc), CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Per-warp staging (P.wst_ch): one bulk tensor store writes both planes (hi, lo) of a warp's
+// 32 px x bc channels.  conv: (C, W, H, B, plane); stride-2 transposed conv: one map per
+// sub-pixel phase (py, px), based at output pixel (py, px): (C, W/2 [2C], B*H/2 [2WC], plane)
+static bool encode_out_conv_map_pl(CUtensorMap* m, const __half* base, int C, int W, int H, int B, size_t plane,
+                                   int planes, int bw, int bh, int bc) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B, (cuuint64_t)planes};
+    cuuint64_t str[4] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2, (cuuint64_t)plane * 2};
+    cuuint32_t box[5] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh, 1, (cuuint32_t)planes};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, (void*)base, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swz_for(bc), CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static bool encode_out_phase_map_pl(CUtensorMap* m, const __half* base, int C, int W, int H, int B, size_t plane,
+                                    int planes, int ph, int bw, int bh, int bc) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    const __half* b0 = base + ((size_t)(ph >> 1) * W + (ph & 1)) * C;
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)(W / 2), (cuuint64_t)B * (H / 2), (cuuint64_t)planes};
+    cuuint64_t str[3] = {(cuuint64_t)2 * C * 2, (cuuint64_t)2 * W * C * 2, (cuuint64_t)plane * 2};
+    cuuint32_t box[4] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)planes};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, (void*)b0, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swz_for(bc), CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // choose Wt x Ht = 128 minimising padded tiles over the grid
@@ -594,6 +628,15 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.n_accbuf = (2 * per <= 512) ? 2 : 1;
     P.acc_stride = per;
     P.tmem_cols = pow2_cols(P.n_accbuf * per);
+    // per-warp staging of the GDN / IGDN epilogue when 64 KB of staging fit: rounds of 32 channels
+    // (BN = 128: one round, one 4 KB slot per warp) or 16 (BN = 192: three rounds, two 2 KB slots)
+    P.wst_ch = 0;
+    P.wst_slots = 0;
+    if (gdn && tma_out && P.ostage_slots == 2 && c->wstage_enabled) {
+        const int G = P.BN / 4;                                         // channels per epilogue warp
+        P.wst_ch = (G % 32 == 0) ? 32 : 16;
+        P.wst_slots = P.wst_ch == 32 ? 1 : 2;
+    }
     P.L = c->L;
     // tensor maps
     const int ntaps_w = (gemm_l1 || P.gather) ? 1 : (P.pack4 ? 9 : Ly.k * Ly.k);
@@ -612,15 +655,29 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     }
     Ly.mapOH = Ly.mapB;
     Ly.mapOL = Ly.mapB;
+    Ly.mapO2 = Ly.mapB;
+    Ly.mapO3 = Ly.mapB;
     if (P.tma_out) {
         const int bw = P.Wt < 32 ? P.Wt : 32, bh = 32 / bw;
+        const int bc = P.wst_ch ? P.wst_ch : 64;
         bool ok;
-        if (P.nphase == 1)
-            ok = encode_out_conv_map(&Ly.mapOH, Ly.out_buf, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh) &&
-                 encode_out_conv_map(&Ly.mapOL, Ly.out_buf + Ly.out_plane, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh);
+        if (P.wst_ch && P.nphase == 1)
+            ok = encode_out_conv_map_pl(&Ly.mapOH, Ly.out_buf, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, Ly.out_plane,
+                                        P.split, bw, bh, bc);
+        else if (P.wst_ch) {
+            CUtensorMap* pm[4] = {&Ly.mapOH, &Ly.mapOL, &Ly.mapO2, &Ly.mapO3};
+            ok = true;
+            for (int ph = 0; ph < 4 && ok; ++ph)
+                ok = encode_out_phase_map_pl(pm[ph], Ly.out_buf, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, Ly.out_plane,
+                                             P.split, ph, bw, bh, bc);
+        } else if (P.nphase == 1)
+            ok = encode_out_conv_map(&Ly.mapOH, Ly.out_buf, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh, bc) &&
+                 encode_out_conv_map(&Ly.mapOL, Ly.out_buf + Ly.out_plane, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh,
+                                     bc);
         else
-            ok = encode_out_phase_map(&Ly.mapOH, Ly.out_buf, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh) &&
-                 encode_out_phase_map(&Ly.mapOL, Ly.out_buf + Ly.out_plane, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh);
+            ok = encode_out_phase_map(&Ly.mapOH, Ly.out_buf, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw, bh, bc) &&
+                 encode_out_phase_map(&Ly.mapOL, Ly.out_buf + Ly.out_plane, Ly.Cout, Ly.Wout, Ly.Hout, c->max_batch, bw,
+                                      bh, bc);
         if (!ok) return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (output) failed");
     }
     // epilogue constants
@@ -635,9 +692,9 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.crop_top = 0; P.crop_left = 0; P.crop_H = Ly.Hout; P.crop_W = Ly.Wout;
     if (std::getenv("LIC_PLAN_DEBUG"))
         std::fprintf(stderr, "plan layer %d: BN %d cg %d ntiles %d halo %d sub4 %d tps %d stages %d slots %d wres %d "
-                     "tma_out %d ostage %d smem %u kchunks %d\n", (int)(&Ly - c->layers), P.BN, P.cg, P.n_ntiles,
-                     P.halo, P.sub4, P.tps, P.stages, P.halo_slots, P.wres, P.tma_out, P.ostage_slots, P.smem_bytes,
-                     P.kchunks);
+                     "tma_out %d ostage %d smem %u kchunks %d wst %d/%d\n", (int)(&Ly - c->layers), P.BN, P.cg,
+                     P.n_ntiles, P.halo, P.sub4, P.tps, P.stages, P.halo_slots, P.wres, P.tma_out, P.ostage_slots,
+                     P.smem_bytes, P.kchunks, P.wst_ch, P.wst_slots);
     return LIC_OK;
 }
 
@@ -660,7 +717,8 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
         CK(cudaEventRecord(c->ev[2 * c->ev_used], st));
     }
     {
-        const cudaError_t e = launch_conv_umma(Ly.mapA, Ly.mapB, Ly.mapG, Ly.mapOH, Ly.mapOL, P, grid, st);
+        const cudaError_t e = launch_conv_umma(Ly.mapA, Ly.mapB, Ly.mapG, Ly.mapOH, Ly.mapOL, Ly.mapO2, Ly.mapO3, P,
+                                               grid, st);
         if (e != cudaSuccess)
             return fail(c, LIC_ECUDA, "launch of layer %d (grid %d, cg %d, smem %u, tiles %d, stages %d, halo %d): %s",
                         lid, grid, P.cg, P.smem_bytes, P.total_tiles, P.stages, P.halo, cudaGetErrorString(e));
@@ -879,6 +937,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_SMALL_BN")) c->small_bn = atoi(e) == 64 || atoi(e) == 128 ? atoi(e) : 0;
     if (const char* e = std::getenv("LIC_NO_WRES")) c->wres_enabled = (e[0] != '1');
+    if (const char* e = std::getenv("LIC_WSTAGE")) c->wstage_enabled = (e[0] != '0');
     c->max_batch = (int)max_batch;
     c->H = (int)height; c->W = (int)width;
     const int P = c->kind == 1 ? 64 : 16;

@@ -230,6 +230,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                  const __grid_constant__ CUtensorMap mapG,
                  const __grid_constant__ CUtensorMap mapOH,
                  const __grid_constant__ CUtensorMap mapOL,
+                 const __grid_constant__ CUtensorMap mapO2,
+                 const __grid_constant__ CUtensorMap mapO3,
                  const __grid_constant__ ConvParams p)
 {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -848,6 +850,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         int it = 0;
         int sat = 0;
         int ovf = 0;                                // activations saturated to the fp16 range
+        int wround = 0;                             // per-warp staging: rounds this warp has stored
         for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
             TileCoord tc = decode_tile(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
@@ -1081,7 +1084,61 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 }
                 released = true;
                 if (out && !(p.dbg_nostore & 1)) {
-                    if (tma_ok) {
+                    if (tma_ok && p.wst_ch) {
+                        // per-warp staging: this warp's 32 pixels x its G channels in
+                        // rounds of wst_ch channels (rows of 2 * wst_ch bytes, swizzled like the
+                        // out maps), each round written by the warp's own bulk tensor stores --
+                        // no cross-warp barrier; wst_slots slots per warp, reused round-robin
+                        const int rch = p.wst_ch, per = rch / 16, nsl = p.wst_slots;
+                        const uint32_t rows_b = 2u * (uint32_t)rch, slot_bytes = 128u * (uint32_t)rch;
+                        const uint32_t sw_mask = rows_b / 16u - 1u;
+                        const uint32_t sw = (((uint32_t)lane * rows_b) >> 7) & sw_mask;
+                        const uint32_t wbase = (uint32_t)p.off_ostage + (uint32_t)(warp - 4) * (uint32_t)nsl * slot_bytes;
+                        if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_ACQ);
+#pragma unroll
+                        for (int j = 0; j < GC; ++j) {
+                            const int kk = j % per;
+                            const uint32_t sl = wbase + (uint32_t)(wround % nsl) * slot_bytes;
+                            if (kk == 0) {
+                                // the stores nsl rounds ago (same slot) have read it
+                                if (lane == 0) { if (nsl == 2) bulk_wait_read1(); else bulk_wait_read0(); }
+                                __syncwarp();
+                            }
+                            if (threadIdx.x == 128 && !p.fuse_l1 && j == 0) LIC_TRACE(it, T_B_PATCH);
+                            const uint32_t rowa = smem_u32(smem) + sl + (uint32_t)lane * rows_b;
+#pragma unroll
+                            for (int k = 0; k < 2; ++k) {                    // 16-byte chunks (8 channels)
+                                uint4 hv, lv;
+                                const float* v8 = x[j] + 8 * k;
+                                split2(v8[0], v8[1], hv.x, lv.x); split2(v8[2], v8[3], hv.y, lv.y);
+                                split2(v8[4], v8[5], hv.z, lv.z); split2(v8[6], v8[7], hv.w, lv.w);
+                                const uint32_t o = ((((uint32_t)(2 * kk + k)) ^ sw) & sw_mask) << 4;
+                                stsu4(rowa + o, hv);
+                                if (p.split == 2) stsu4(rowa + 32u * rows_b + o, lv);
+                            }
+                            if (kk == per - 1 || j == GC - 1) {
+                                if (threadIdx.x == 128 && !p.fuse_l1 && j == GC - 1) LIC_TRACE(it, T_B_C0_READY);
+                                fence_proxy_async_smem();
+                                __syncwarp();
+                                if (threadIdx.x == 128 && !p.fuse_l1 && j == GC - 1) LIC_TRACE(it, T_B_C0_DONE);
+                                if (lane == 0) {
+                                    // one store writes both planes (the map's last dimension)
+                                    const int cb = co0 + g * G + 16 * (j - kk);
+                                    const uint8_t* hs = smem + sl;
+                                    if (p.nphase == 1) {
+                                        tma_store_5d(&mapOH, hs, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b, 0);
+                                    } else {
+                                        const int ph = py * 2 + px;
+                                        const CUtensorMap* om = ph == 0 ? &mapOH : ph == 1 ? &mapOL : ph == 2 ? &mapO2 : &mapO3;
+                                        tma_store_4d(om, hs, cb, tc.gx0 + tx0, tc.b * p.Hg + tc.gy0 + ty0, 0);
+                                    }
+                                    bulk_commit();
+                                }
+                                ++wround;
+                            }
+                        }
+                        if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_STAGED);
+                    } else if (tma_ok) {
                         const int nblk = p.BN >> 6;
                         for (int b0 = 0; b0 < nblk; b0 += qslots) {
                             q_acquire(0);
@@ -1288,7 +1345,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             }
             if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_END);
         }
-        if (p.tma_out && lane == 0 && g == 0) bulk_wait0();
+        if (p.tma_out && lane == 0 && (g == 0 || p.wst_ch)) bulk_wait0();
         if (p.sat_count) {
             for (int o = 16; o > 0; o >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, o);
             if (lane == 0 && sat) atomicAdd(p.sat_count, (unsigned long long)sat);
@@ -1311,8 +1368,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 
 template <int GC, int CG>
 static cudaError_t launch_t(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
-                            const CUtensorMap& mapOH, const CUtensorMap& mapOL, const ConvParams& p, int grid,
-                            cudaStream_t stream) {
+                            const CUtensorMap& mapOH, const CUtensorMap& mapOL, const CUtensorMap& mapO2,
+                            const CUtensorMap& mapO3, const ConvParams& p, int grid, cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<GC, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1341,25 +1398,25 @@ static cudaError_t launch_t(const CUtensorMap& mapA, const CUtensorMap& mapB, co
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, conv_umma_kernel<GC, CG>, mapA, mapB, mapG, mapOH, mapOL, p);
+    return cudaLaunchKernelEx(&cfg, conv_umma_kernel<GC, CG>, mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p);
 }
 
 cudaError_t launch_conv_umma(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
-                             const CUtensorMap& mapOH, const CUtensorMap& mapOL, const ConvParams& p, int grid,
-                             cudaStream_t stream) {
+                             const CUtensorMap& mapOH, const CUtensorMap& mapOL, const CUtensorMap& mapO2,
+                             const CUtensorMap& mapO3, const ConvParams& p, int grid, cudaStream_t stream) {
     const bool gdn = (p.ep == EP_GDN || p.ep == EP_IGDN);
     if (p.cg == 2) {
-        if (!gdn) return launch_t<0, 2>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+        if (!gdn) return launch_t<0, 2>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
         switch (p.BN) {
-        case 128: return launch_t<2, 2>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
-        case 192: return launch_t<3, 2>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+        case 128: return launch_t<2, 2>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
+        case 192: return launch_t<3, 2>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
         default: return cudaErrorInvalidValue;
         }
     }
-    if (!gdn) return launch_t<0, 1>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+    if (!gdn) return launch_t<0, 1>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
     switch (p.BN) {      // GDN channel counts of the configs: N = 128, 192
-    case 128: return launch_t<2, 1>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
-    case 192: return launch_t<3, 1>(mapA, mapB, mapG, mapOH, mapOL, p, grid, stream);
+    case 128: return launch_t<2, 1>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
+    case 192: return launch_t<3, 1>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
     default: return cudaErrorInvalidValue;
     }
 }

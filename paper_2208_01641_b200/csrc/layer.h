@@ -112,6 +112,10 @@ struct ConvParams {
     // (C, px, W/2, py, B*H/2) of the NHWC output, one map per plane
     int tma_out, ostage_slots;        // staging buffers per warp (1 or 2, 2 KB each)
     uint32_t off_ostage;
+    // GDN / IGDN layers with 64 KB of staging: every epilogue warp stages its own 32 pixels in
+    // rounds of wst_ch channels (32: 4 KB slots, 64-byte rows; 16: 2 KB) in wst_slots private
+    // slots and stores them itself (out maps with a wst_ch-channel box); 0: quadrant blocks
+    int wst_ch, wst_slots;
     // gather mode (g_s L4, stride-2 transposed conv N -> 3): the 9 input offsets go into N instead
     // of K -- P[p][t][j] = A[p] . W_t[j] over a 16 x 8 input tile (one A read per pixel, N = 9 x 16),
     // then out[g][j] = sum_t P[g + off_t][t][j] gathered through shared memory for the 14 x 6
