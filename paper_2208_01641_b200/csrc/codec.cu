@@ -1525,6 +1525,7 @@ lic_status lic_internal_clone(const lic_codec* c, lic_codec** out) {
 }
 
 uint64_t lic_internal_launches(const lic_codec* c) { return c ? c->launches : 0; }
+int lic_internal_zero_copy(const lic_codec* c) { return c ? c->zero_copy : 0; }
 
 extern "C" lic_status lic_set_zero_copy(lic_codec* c, int on) {
     if (!c) return LIC_EINVAL;

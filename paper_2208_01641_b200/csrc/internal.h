@@ -10,3 +10,4 @@ size_t lic_internal_frame_pixels(const lic_codec* c);
 lic_status lic_internal_clone(const lic_codec* c, lic_codec** out);
 // kernels this codec has launched
 uint64_t lic_internal_launches(const lic_codec* c);
+int lic_internal_zero_copy(const lic_codec* c);   // kernels touch pinned host planes in place

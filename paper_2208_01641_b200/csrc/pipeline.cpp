@@ -113,6 +113,7 @@ struct lic_pipeline {
     cudaStream_t cstream = nullptr;         // host -> device copies
     cudaStream_t dstream = nullptr;         // device -> host copies (the other copy engine)
     bool in_host = false, out_host = false; // caller's frames in host memory (staged per slot)
+    bool zc = false;                        // codec in zero-copy mode: kernels use the pinned slot planes
     std::vector<cudaEvent_t> events;        // cross-stream join events, recycled as a ring
     std::vector<cudaEvent_t> done_events;   // one per in-flight task (kMaxPendingCap), from a free list
     std::vector<cudaEvent_t> done_free;
@@ -309,6 +310,7 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
     lic_status st = lic_shapes(codec, &p->ys, &p->zs, &p->hyper);
     if (st) { delete p; return st; }
     p->ksub = cfg->substreams ? cfg->substreams : 1;
+    p->zc = lic_internal_zero_copy(codec) != 0;
     if (p->ksub > 64 || p->ksub > p->ys.c) { delete p; return LIC_EINVAL; }
     p->ny = (size_t)p->ys.c * p->ys.h * p->ys.w;
     p->nz = (size_t)p->zs.c * p->zs.h * p->zs.w;
@@ -481,44 +483,52 @@ static lic_status gpu_call(lic_pipeline* p, const GpuTask& t, cudaEvent_t done, 
     case G_ENC: {
         const uint8_t* fr = p->in + b * fb;
         if (p->in_host) { cp(s.d_fin, fr, fb, cudaMemcpyHostToDevice); to_k(); fr = s.d_fin; }
+        // zero-copy: the epilogues write the pinned slot planes in place
+        int8_t* ys = p->zc ? s.y_sym : s.d_ysym;
+        uint8_t* yi = p->zc ? s.y_idx : s.d_yidx;
+        int8_t* zs = p->zc ? s.z_sym : s.d_zsym;
         mark(p->stream, 0);
         if (!st)
-            st = p->cfg.u8 ? lic_encode_u8(p->codec, fr, B, s.d_ysym, p->hyper ? s.d_yidx : nullptr,
-                                           p->hyper ? s.d_zsym : nullptr, nullptr, p->stream)
-                           : lic_encode(p->codec, (const float*)fr, B, s.d_ysym, p->hyper ? s.d_yidx : nullptr,
-                                        p->hyper ? s.d_zsym : nullptr, nullptr, p->stream);
+            st = p->cfg.u8 ? lic_encode_u8(p->codec, fr, B, ys, p->hyper ? yi : nullptr, p->hyper ? zs : nullptr,
+                                           nullptr, p->stream)
+                           : lic_encode(p->codec, (const float*)fr, B, ys, p->hyper ? yi : nullptr,
+                                        p->hyper ? zs : nullptr, nullptr, p->stream);
         mark(p->stream, 1);
         to_c();
-        cp(s.y_sym, s.d_ysym, B * p->ny, cudaMemcpyDeviceToHost);
-        if (p->hyper) {
-            cp(s.y_idx, s.d_yidx, B * p->ny, cudaMemcpyDeviceToHost);
-            cp(s.z_sym, s.d_zsym, B * p->nz, cudaMemcpyDeviceToHost);
+        if (!p->zc) {
+            cp(s.y_sym, s.d_ysym, B * p->ny, cudaMemcpyDeviceToHost);
+            if (p->hyper) {
+                cp(s.y_idx, s.d_yidx, B * p->ny, cudaMemcpyDeviceToHost);
+                cp(s.z_sym, s.d_zsym, B * p->nz, cudaMemcpyDeviceToHost);
+            }
         }
         break;
     }
     case G_IDX: {
         lic_codec* cc = p->codec2 ? p->codec2 : p->codec;
         cudaStream_t ks = p->codec2 ? p->stream2 : p->stream;
-        cp(s.d_zdec, s.z_dec, B * p->nz, cudaMemcpyHostToDevice);
+        if (!p->zc) cp(s.d_zdec, s.z_dec, B * p->nz, cudaMemcpyHostToDevice);
         if (!st && !join(p, p->cstream, ks, ev_next)) st = LIC_ECUDA;
         mark(ks, 0);
-        if (!st) st = lic_hyper_indexes(cc, s.d_zdec, B, s.d_idxdec, ks);
+        if (!st)
+            st = lic_hyper_indexes(cc, p->zc ? s.z_dec : s.d_zdec, B, p->zc ? s.idx_dec : s.d_idxdec, ks);
         mark(ks, 1);
         if (!st && !join(p, ks, p->dstream, ev_next)) st = LIC_ECUDA;
-        cp(s.idx_dec, s.d_idxdec, B * p->ny, cudaMemcpyDeviceToHost);
+        if (!p->zc) cp(s.idx_dec, s.d_idxdec, B * p->ny, cudaMemcpyDeviceToHost);
         break;
     }
     case G_DEC: {
         lic_codec* cc = p->codec3 ? p->codec3 : p->codec;
         cudaStream_t ks = p->codec3 ? p->stream3 : p->stream;
-        cp(s.d_ydec, s.y_dec, B * p->ny, cudaMemcpyHostToDevice);
+        if (!p->zc) cp(s.d_ydec, s.y_dec, B * p->ny, cudaMemcpyHostToDevice);
         if (!st && !join(p, p->cstream, ks, ev_next)) st = LIC_ECUDA;
         uint8_t* fr = p->out + b * fb;
         uint8_t* dst = p->out_host ? s.d_fout : fr;
+        const int8_t* yd = p->zc ? s.y_dec : s.d_ydec;
         mark(ks, 0);
         if (!st)
-            st = p->cfg.u8 ? lic_decode_u8(cc, s.d_ydec, B, dst, ks)
-                           : lic_decode(cc, s.d_ydec, B, (float*)dst, ks);
+            st = p->cfg.u8 ? lic_decode_u8(cc, yd, B, dst, ks)
+                           : lic_decode(cc, yd, B, (float*)dst, ks);
         mark(ks, 1);
         if (!st && !join(p, ks, p->dstream, ev_next)) st = LIC_ECUDA;
         if (p->out_host) cp(fr, s.d_fout, fb, cudaMemcpyDeviceToHost);
