@@ -288,7 +288,8 @@ def measure(args, name, rank, world, local, threads, full):
     codec = lic.Codec(blob, H, W, max_batch=B, device=local,
                       precision=lic.PREC_F16 if args.precision == "f16" else lic.PREC_SPLIT)
     codec.set_zero_copy(args.zero_copy)
-    mk = dict(coder_threads=threads, batch=B, u8=True, substreams=args.substreams, coder=CODERS[args.coder])
+    mk = dict(coder_threads=threads, batch=B, u8=True, substreams=args.substreams, coder=CODERS[args.coder],
+              coder_parts=args.coder_parts)
     pipe = lic.Pipeline(codec, inflight=args.inflight, **mk)
 
     # the stream: local frame i of rank r is global frame t = r + G*i (frame t mod 8 of seed 1000)
@@ -520,6 +521,8 @@ def main():
     ap.add_argument("--inflight", type=int, default=8)
     ap.add_argument("--substreams", type=int, default=32,
                     help="y string as K channel-slab rANS substreams (DESIGN.md R21); 1 = one string")
+    ap.add_argument("--coder-parts", type=int, default=2,
+                    help="coder tasks per frame: the y string's slab ranges on separate threads (same bitstream)")
     ap.add_argument("--coder", default="rans32", choices=["rans32", "rans64"],
                     help="host entropy coder: 32-bit rANS over +-L tables (with --substreams), or rans64 + "
                          "bypass escape with Gaussian tables (DESIGN.md R23; one string per plane)")
@@ -570,6 +573,7 @@ def main():
                    "batch_per_gpu": r["B"], "frames_per_gpu": r["nfr"], "world": world,
                    "coder_threads_per_gpu": threads, "cores_per_rank": cores, "inflight": args.inflight,
                    "y_substreams": args.substreams if args.coder == "rans32" else 1, "entropy_coder": args.coder,
+                   "coder_parts": args.coder_parts,
                    "l2": "inputs larger than L2 (activations ~0.36 GB per frame, frame set > 126 MB)",
                    "pipeline": "overlapped"},
         "latency_ms": {"p50": round(r["paced"]["latency_p50_ms"], 3), "p95": round(r["paced"]["latency_p95_ms"], 3),

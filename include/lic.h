@@ -264,6 +264,9 @@ typedef struct {
                                  0: every frame is available at the start, latency counts from the
                                  batch's admission into a slot */
     uint32_t timeline;        /* 1: record lic_pipeline_timeline events for the run */
+    uint32_t coder_parts;     /* hyperprior, coder 0, substreams K: each frame's y string is coded (and decoded) as
+                                 this many slab ranges on separate coder threads (lic_rans_encode_slab_range) --
+                                 the same bitstream, 1/parts of the per-frame coder latency; 0 or 1: one task */
 } lic_pipeline_config;
 typedef struct {
     uint64_t frames;          /* frames completed */
@@ -326,6 +329,18 @@ lic_status lic_rans_encode_slabs(const lic_rans_tables* t, const int8_t* sym, co
                                  uint32_t K, uint8_t* out, size_t cap, size_t* out_len);
 lic_status lic_rans_decode_slabs(const lic_rans_tables* t, const uint8_t* in, size_t len, const uint8_t* row,
                                  lic_shape plane, uint32_t K, int8_t* sym_out);
+/* The same coder split across threads: slabs [k_begin, k_end) of the K-slab plane only.
+ * encode: the range's strings back to back in `out` (no header), their lengths in
+ * lens[0 .. k_end-k_begin); a caller that concatenates the ranges of 0..K in order behind the
+ * K big-endian lengths has exactly lic_rans_encode_slabs' stream.  decode: `in` is the whole
+ * framed stream (header + K strings); only the range's channels of sym_out are written.
+ * sym / row / sym_out are whole-plane arrays.  Errors as lic_rans_encode_slabs /
+ * lic_rans_decode_slabs; LIC_EINVAL for an empty or out-of-range slab range. */
+lic_status lic_rans_encode_slab_range(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row, lic_shape plane,
+                                      uint32_t K, uint32_t k_begin, uint32_t k_end, uint8_t* out, size_t cap,
+                                      uint32_t* lens, size_t* out_len);
+lic_status lic_rans_decode_slab_range(const lic_rans_tables* t, const uint8_t* in, size_t len, const uint8_t* row,
+                                      lic_shape plane, uint32_t K, uint32_t k_begin, uint32_t k_end, int8_t* sym_out);
 
 /* ---------------------------------------------------------------- rans64 + bypass escape
  * the coder the paper's implementations link ("simply integrate

@@ -742,25 +742,19 @@ inline uint32_t get_be32(const uint8_t* q) {
 
 }  // namespace
 
-extern "C" lic_status lic_rans_encode_slabs(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row,
-                                            lic_shape plane, uint32_t K, uint8_t* out, size_t cap, size_t* out_len) {
-    if (!t || !out || !out_len) return LIC_EINVAL;
-    if (K <= 1) return lic_rans_encode_fast(t, sym, row, plane, out, cap, out_len);
-    SlabGeom g;
-    if (!slab_geom(plane, K, g)) return LIC_EINVAL;
-    if (g.hw * plane.c && !sym) return LIC_EINVAL;
-    if (!validate_planes(t, sym, row, g.hw * plane.c, g.hw)) return LIC_EINVAL;
-    if (!row && plane.c > t->n_rows) return LIC_EINVAL;
+namespace {
+
+// Slabs [kb, ke) of a K-slab plane: the strings (in the per-thread scratch, start[k]..hi[k])
+lic_status encode_slab_range(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row, const SlabGeom& g,
+                             uint32_t kb, uint32_t ke, std::vector<uint8_t>& scratch, uint8_t** start, uint8_t** hi) {
     // per-slab scratch regions: 2 bytes per symbol + 8 (renormalisation emits <= 16 bits per symbol)
-    thread_local std::vector<uint8_t> scratch;
     size_t need = 0;
     size_t off[64];
-    for (uint32_t k = 0; k < K; ++k) { off[k] = need; need += 2 * g.count[k] + 8; }
+    for (uint32_t k = kb; k < ke; ++k) { off[k] = need; need += 2 * g.count[k] + 8; }
     if (scratch.size() < need) scratch.resize(need);
-    uint8_t* hi[64]; uint8_t* start[64];
-    for (uint32_t k = 0; k < K; ++k) hi[k] = scratch.data() + off[k] + 2 * g.count[k] + 8;
-    for (uint32_t k0 = 0; k0 < K;) {
-        const uint32_t left = K - k0;
+    for (uint32_t k = kb; k < ke; ++k) hi[k] = scratch.data() + off[k] + 2 * g.count[k] + 8;
+    for (uint32_t k0 = kb; k0 < ke;) {
+        const uint32_t left = ke - k0;
 #if defined(__x86_64__) && defined(__GNUC__)
         if (const int nl = simd_lanes(g, k0, left)) {
             const lic_status st = nl == 64 ? enc_avx512<4>(t, sym, row, g, (int)k0, scratch.data(), hi + k0, start + k0)
@@ -785,42 +779,13 @@ extern "C" lic_status lic_rans_encode_slabs(const lic_rans_tables* t, const int8
         if (st) return st;
         k0 += (uint32_t)G;
     }
-    size_t total = 4 * (size_t)K;
-    for (uint32_t k = 0; k < K; ++k) total += (size_t)(hi[k] - start[k]);
-    if (total > cap) return LIC_ENOSPACE;
-    uint8_t* w = out + 4 * (size_t)K;
-    for (uint32_t k = 0; k < K; ++k) {
-        const size_t n = (size_t)(hi[k] - start[k]);
-        put_be32(out + 4 * k, (uint32_t)n);
-        std::memcpy(w, start[k], n);
-        w += n;
-    }
-    *out_len = total;
     return LIC_OK;
 }
 
-extern "C" lic_status lic_rans_decode_slabs(const lic_rans_tables* t, const uint8_t* in, size_t len, const uint8_t* row,
-                                            lic_shape plane, uint32_t K, int8_t* sym_out) {
-    if (!t) return LIC_EINVAL;
-    if (K <= 1) return lic_rans_decode_fast(t, in, len, row, plane, sym_out);
-    SlabGeom g;
-    if (!slab_geom(plane, K, g)) return LIC_EINVAL;
-    if (g.hw * plane.c && !sym_out) return LIC_EINVAL;
-    if (!validate_planes(t, nullptr, row, g.hw * plane.c, g.hw)) return LIC_EINVAL;
-    if (!row && plane.c > t->n_rows) return LIC_EINVAL;
-    if (!in || len < 4 * (size_t)K) return LIC_ECORRUPT;
-    const uint8_t* sp[64];
-    size_t sl[64];
-    size_t pos = 4 * (size_t)K;
-    for (uint32_t k = 0; k < K; ++k) {
-        sl[k] = get_be32(in + 4 * k);
-        if (sl[k] > len - pos) return LIC_ECORRUPT;
-        sp[k] = in + pos;
-        pos += sl[k];
-    }
-    if (pos != len) return LIC_ECORRUPT;
-    for (uint32_t k0 = 0; k0 < K;) {
-        const uint32_t left = K - k0;
+lic_status decode_slab_range(const lic_rans_tables* t, const uint8_t* in, const uint8_t* const* sp, const size_t* sl,
+                             const uint8_t* row, const SlabGeom& g, uint32_t kb, uint32_t ke, int8_t* sym_out) {
+    for (uint32_t k0 = kb; k0 < ke;) {
+        const uint32_t left = ke - k0;
 #if defined(__x86_64__) && defined(__GNUC__)
         if (const int nl = simd_lanes(g, k0, left)) {
             const lic_status st = nl == 64 ? dec_avx512<4>(t, in, sp + k0, sl + k0, row, g, (int)k0, sym_out)
@@ -846,4 +811,96 @@ extern "C" lic_status lic_rans_decode_slabs(const lic_rans_tables* t, const uint
         k0 += (uint32_t)G;
     }
     return LIC_OK;
+}
+
+// the K big-endian lengths of a framed slab string -> string pointers / lengths
+lic_status parse_slab_frame(const uint8_t* in, size_t len, uint32_t K, const uint8_t** sp, size_t* sl) {
+    if (!in || len < 4 * (size_t)K) return LIC_ECORRUPT;
+    size_t pos = 4 * (size_t)K;
+    for (uint32_t k = 0; k < K; ++k) {
+        sl[k] = get_be32(in + 4 * k);
+        if (sl[k] > len - pos) return LIC_ECORRUPT;
+        sp[k] = in + pos;
+        pos += sl[k];
+    }
+    return pos == len ? LIC_OK : LIC_ECORRUPT;
+}
+
+}  // namespace
+
+extern "C" lic_status lic_rans_encode_slabs(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row,
+                                            lic_shape plane, uint32_t K, uint8_t* out, size_t cap, size_t* out_len) {
+    if (!t || !out || !out_len) return LIC_EINVAL;
+    if (K <= 1) return lic_rans_encode_fast(t, sym, row, plane, out, cap, out_len);
+    SlabGeom g;
+    if (!slab_geom(plane, K, g)) return LIC_EINVAL;
+    if (g.hw * plane.c && !sym) return LIC_EINVAL;
+    if (!validate_planes(t, sym, row, g.hw * plane.c, g.hw)) return LIC_EINVAL;
+    if (!row && plane.c > t->n_rows) return LIC_EINVAL;
+    thread_local std::vector<uint8_t> scratch;
+    uint8_t* hi[64]; uint8_t* start[64];
+    if (lic_status st = encode_slab_range(t, sym, row, g, 0, K, scratch, start, hi)) return st;
+    size_t total = 4 * (size_t)K;
+    for (uint32_t k = 0; k < K; ++k) total += (size_t)(hi[k] - start[k]);
+    if (total > cap) return LIC_ENOSPACE;
+    uint8_t* w = out + 4 * (size_t)K;
+    for (uint32_t k = 0; k < K; ++k) {
+        const size_t n = (size_t)(hi[k] - start[k]);
+        put_be32(out + 4 * k, (uint32_t)n);
+        std::memcpy(w, start[k], n);
+        w += n;
+    }
+    *out_len = total;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_rans_encode_slab_range(const lic_rans_tables* t, const int8_t* sym, const uint8_t* row,
+                                                 lic_shape plane, uint32_t K, uint32_t k_begin, uint32_t k_end,
+                                                 uint8_t* out, size_t cap, uint32_t* lens, size_t* out_len) {
+    if (!t || !out || !out_len || !lens || K < 1 || k_begin >= k_end || k_end > K) return LIC_EINVAL;
+    SlabGeom g;
+    if (!slab_geom(plane, K, g)) return LIC_EINVAL;
+    if (g.hw * plane.c && !sym) return LIC_EINVAL;
+    // the range's channels only (row[] and sym[] are whole-plane arrays)
+    const size_t b0 = g.begin[k_begin], n = g.begin[k_end - 1] + g.count[k_end - 1] - b0;
+    if (!validate_planes(t, sym + b0, row ? row + b0 : nullptr, n, g.hw)) return LIC_EINVAL;
+    if (!row && (uint32_t)((uint64_t)k_end * plane.c / K) > t->n_rows) return LIC_EINVAL;
+    thread_local std::vector<uint8_t> scratch;
+    uint8_t* hi[64]; uint8_t* start[64];
+    if (lic_status st = encode_slab_range(t, sym, row, g, k_begin, k_end, scratch, start, hi)) return st;
+    size_t total = 0;
+    for (uint32_t k = k_begin; k < k_end; ++k) total += (size_t)(hi[k] - start[k]);
+    if (total > cap) return LIC_ENOSPACE;
+    uint8_t* w = out;
+    for (uint32_t k = k_begin; k < k_end; ++k) {
+        const size_t m = (size_t)(hi[k] - start[k]);
+        lens[k - k_begin] = (uint32_t)m;
+        std::memcpy(w, start[k], m);
+        w += m;
+    }
+    *out_len = total;
+    return LIC_OK;
+}
+
+extern "C" lic_status lic_rans_decode_slabs(const lic_rans_tables* t, const uint8_t* in, size_t len, const uint8_t* row,
+                                            lic_shape plane, uint32_t K, int8_t* sym_out) {
+    if (!t) return LIC_EINVAL;
+    if (K <= 1) return lic_rans_decode_fast(t, in, len, row, plane, sym_out);
+    return lic_rans_decode_slab_range(t, in, len, row, plane, K, 0, K, sym_out);
+}
+
+extern "C" lic_status lic_rans_decode_slab_range(const lic_rans_tables* t, const uint8_t* in, size_t len,
+                                                 const uint8_t* row, lic_shape plane, uint32_t K, uint32_t k_begin,
+                                                 uint32_t k_end, int8_t* sym_out) {
+    if (!t || K < 2 || k_begin >= k_end || k_end > K) return LIC_EINVAL;
+    SlabGeom g;
+    if (!slab_geom(plane, K, g)) return LIC_EINVAL;
+    if (g.hw * plane.c && !sym_out) return LIC_EINVAL;
+    const size_t b0 = g.begin[k_begin], n = g.begin[k_end - 1] + g.count[k_end - 1] - b0;
+    if (!validate_planes(t, nullptr, row ? row + b0 : nullptr, n, g.hw)) return LIC_EINVAL;
+    if (!row && (uint32_t)((uint64_t)k_end * plane.c / K) > t->n_rows) return LIC_EINVAL;
+    const uint8_t* sp[64];
+    size_t sl[64];
+    if (lic_status st = parse_slab_frame(in, len, K, sp, sl)) return st;
+    return decode_slab_range(t, in, sp, sl, row, g, k_begin, k_end, sym_out);
 }

@@ -53,6 +53,11 @@ struct Slot {
     uint8_t* d_fin = nullptr; uint8_t* d_fout = nullptr;
     std::vector<std::vector<uint8_t>> ystr, zstr;
     std::vector<size_t> ylen, zlen;
+    // y coded as `parts` slab ranges on separate coder tasks (lic_rans_encode_slab_range)
+    std::vector<std::vector<std::vector<uint8_t>>> ypart;   // [frame][part] strings of the part's slabs
+    std::vector<std::vector<size_t>> ypart_len;              // [frame][part] bytes
+    std::vector<std::vector<uint32_t>> ylens;                // [frame][K] string lengths
+    std::vector<int> parts_left;                             // [frame] C_ONE parts still running
     int batch = -1;
     int remaining = 0;
     double t_start = 0;
@@ -61,7 +66,7 @@ struct Slot {
 struct GpuTask { GpuKind kind; int slot; double t_ready; };
 struct Pending { GpuTask task; cudaEvent_t done; double t_issue; };
 constexpr size_t kMaxPendingCap = 16;       // GPU tasks in flight at most (env LIC_MAX_PENDING <= this)
-struct CpuTask { CpuKind kind; int slot; int frame; double t_ready; };
+struct CpuTask { CpuKind kind; int slot; int frame; double t_ready; int part = 0; };
 
 }  // namespace
 
@@ -100,6 +105,7 @@ struct lic_pipeline {
     const uint32_t* cdf_z = nullptr; uint32_t rows_z = 0;
     uint32_t row_len = 0;
     uint32_t ksub = 1;                      // y substreams (channel slabs, lic_rans_encode_slabs)
+    uint32_t parts = 1;                     // coder tasks per frame and kind (slab ranges of the y string)
     int sym_min = 0;
     lic_rans_tables* tab_y = nullptr;       // prepared coder tables (lic_rans_prepare)
     lic_rans_tables* tab_z = nullptr;
@@ -214,7 +220,53 @@ static void coder_task(lic_pipeline* p, const CpuTask& t) {
     const size_t f = (size_t)t.frame;
     lic_status st = LIC_OK;
     uint64_t mism = 0;
-    if (t.kind == C_ONE) {
+    bool frame_done = true;                 // this task completes the frame's work of its kind
+    if (p->parts > 1) {
+        // one slab range [kb, ke) of the y string; part 0 also codes z (encoder) / nothing more
+        const uint32_t K = p->ksub, kb = (uint32_t)t.part * K / p->parts, ke = (uint32_t)(t.part + 1) * K / p->parts;
+        const size_t hw = (size_t)p->ys.h * p->ys.w;
+        const size_t c0 = (size_t)kb * p->ys.c / K, c1 = (size_t)ke * p->ys.c / K;
+        if (t.kind == C_ONE) {
+            // E(y) of the slabs, and (part 0) E(z) + decoder CPU1 E^-1(z)
+            st = lic_rans_encode_slab_range(p->tab_y, s.y_sym + f * p->ny, s.y_idx + f * p->ny, p->ys, K, kb, ke,
+                                            s.ypart[f][t.part].data(), s.ypart[f][t.part].size(),
+                                            s.ylens[f].data() + kb, &s.ypart_len[f][t.part]);
+            if (!st && t.part == 0) {
+                st = lic_rans_encode_fast(p->tab_z, s.z_sym + f * p->nz, nullptr, p->zs, s.zstr[f].data(),
+                                          s.zstr[f].size(), &s.zlen[f]);
+                if (!st) st = lic_rans_decode_fast(p->tab_z, s.zstr[f].data(), s.zlen[f], nullptr, p->zs,
+                                                   s.z_dec + f * p->nz);
+                if (!st && std::memcmp(s.z_dec + f * p->nz, s.z_sym + f * p->nz, p->nz) != 0) mism += 1;
+            }
+            bool last = false;
+            {
+                std::lock_guard<std::mutex> g(p->mu);
+                last = --s.parts_left[f] == 0;
+            }
+            frame_done = last;
+            if (last && !st) {
+                // the framed string: K big-endian lengths, then the parts in slab order
+                uint8_t* w = s.ystr[f].data();
+                for (uint32_t k = 0; k < K; ++k) {
+                    const uint32_t n = s.ylens[f][k];
+                    w[4 * k] = (uint8_t)(n >> 24); w[4 * k + 1] = (uint8_t)(n >> 16);
+                    w[4 * k + 2] = (uint8_t)(n >> 8); w[4 * k + 3] = (uint8_t)n;
+                }
+                size_t pos = 4 * (size_t)K;
+                for (uint32_t q = 0; q < p->parts; ++q) {
+                    std::memcpy(w + pos, s.ypart[f][q].data(), s.ypart_len[f][q]);
+                    pos += s.ypart_len[f][q];
+                }
+                s.ylen[f] = pos;
+            }
+        } else {
+            // decoder CPU2: E^-1(y) of the slabs with the indexes from decoder GPU1
+            st = lic_rans_decode_slab_range(p->tab_y, s.ystr[f].data(), s.ylen[f], s.idx_dec + f * p->ny, p->ys, K,
+                                            kb, ke, s.y_dec + f * p->ny);
+            if (!st && std::memcmp(s.y_dec + f * p->ny + c0 * hw, s.y_sym + f * p->ny + c0 * hw, (c1 - c0) * hw) != 0)
+                mism += 1;
+        }
+    } else if (t.kind == C_ONE) {
         // encoder CPU workload: E(y) (and E(z)); then decoder CPU1: E^-1(z) (hyper) or E^-1(y)
         st = lic_rans_encode_slabs(p->tab_y, s.y_sym + f * p->ny, p->hyper ? s.y_idx + f * p->ny : nullptr, p->ys,
                                    p->ksub, s.ystr[f].data(), s.ystr[f].size(), &s.ylen[f]);
@@ -235,6 +287,7 @@ static void coder_task(lic_pipeline* p, const CpuTask& t) {
                                    s.y_dec + f * p->ny);
         if (!st && std::memcmp(s.y_dec + f * p->ny, s.y_sym + f * p->ny, p->ny) != 0) mism += 1;
     }
+    (void)frame_done;
     std::lock_guard<std::mutex> g(p->mu);
     if (st && !p->err) p->err = st;
     p->mismatches += mism;
@@ -310,6 +363,10 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
     lic_status st = lic_shapes(codec, &p->ys, &p->zs, &p->hyper);
     if (st) { delete p; return st; }
     p->ksub = cfg->substreams ? cfg->substreams : 1;
+    // coder tasks per frame: slab ranges of the y string on separate threads (hyperprior,
+    // 32-bit rANS with substreams; each range a multiple of 16 slabs keeps the AVX-512 lanes)
+    p->parts = cfg->coder_parts ? cfg->coder_parts : 1;
+    if (p->parts > 1 && (!p->hyper || cfg->coder != 0 || p->ksub < 2 * p->parts || p->ksub % p->parts)) p->parts = 1;
     p->zc = lic_internal_zero_copy(codec) != 0;
     if (p->ksub > 64 || p->ksub > p->ys.c) { delete p; return LIC_EINVAL; }
     p->ny = (size_t)p->ys.c * p->ys.h * p->ys.w;
@@ -394,6 +451,10 @@ extern "C" lic_status lic_pipeline_open(lic_codec* codec, const lic_pipeline_con
         const size_t ycap = p->coder == 1 ? 4 * p->ny + 64 : 2 * p->ny + 64 + 8 * p->ksub;
         const size_t zcap = p->coder == 1 ? 4 * p->nz + 64 : 2 * p->nz + 64;
         s.ystr.assign(B, std::vector<uint8_t>(ycap));
+        s.ypart.assign(B, std::vector<std::vector<uint8_t>>(p->parts, std::vector<uint8_t>(ycap)));
+        s.ypart_len.assign(B, std::vector<size_t>(p->parts, 0));
+        s.ylens.assign(B, std::vector<uint32_t>(p->ksub, 0));
+        s.parts_left.assign(B, 0);
         s.zstr.assign(B, std::vector<uint8_t>(zcap));
         s.ylen.assign(B, 0);
         s.zlen.assign(B, 0);
@@ -687,8 +748,12 @@ extern "C" lic_status lic_pipeline_run(lic_pipeline* p, const void* frames_in, u
         t = pd.task;
         Slot& s = p->slots[t.slot];
         if (t.kind == G_ENC || t.kind == G_IDX) {
-            s.remaining = (int)B;
-            for (uint32_t f = 0; f < B; ++f) p->cpu_q.push_back({t.kind == G_ENC ? C_ONE : C_TWO, t.slot, (int)f, g1});
+            s.remaining = (int)(B * p->parts);
+            for (uint32_t f = 0; f < B; ++f) {
+                if (t.kind == G_ENC) s.parts_left[f] = (int)p->parts;
+                for (uint32_t q = 0; q < p->parts; ++q)
+                    p->cpu_q.push_back({t.kind == G_ENC ? C_ONE : C_TWO, t.slot, (int)f, g1, (int)q});
+            }
             p->cv_cpu.notify_all();
         } else {
             for (uint32_t f = 0; f < B; ++f) {

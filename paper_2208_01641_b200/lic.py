@@ -88,7 +88,7 @@ class PipelineConfig(ctypes.Structure):
     _fields_ = [("coder_threads", ctypes.c_uint32), ("batch", ctypes.c_uint32), ("inflight", ctypes.c_uint32),
                 ("u8", ctypes.c_int), ("serial", ctypes.c_int), ("keep_bitstreams", ctypes.c_int),
                 ("substreams", ctypes.c_uint32), ("coder", ctypes.c_uint32), ("pace_fps", ctypes.c_float),
-                ("timeline", ctypes.c_uint32)]
+                ("timeline", ctypes.c_uint32), ("coder_parts", ctypes.c_uint32)]
 
 
 class TimelineEvent(ctypes.Structure):
@@ -127,6 +127,8 @@ _L.lic_rans_encode_fast.argtypes = [_P, _P, _P, Shape, _P, _sz, ctypes.POINTER(_
 _L.lic_rans_decode_fast.argtypes = [_P, _P, _sz, _P, Shape, _P]
 _L.lic_rans_encode_slabs.argtypes = [_P, _P, _P, Shape, _u32, _P, _sz, ctypes.POINTER(_sz)]
 _L.lic_rans_decode_slabs.argtypes = [_P, _P, _sz, _P, Shape, _u32, _P]
+_L.lic_rans_encode_slab_range.argtypes = [_P, _P, _P, Shape, _u32, _u32, _u32, _P, _sz, _P, ctypes.POINTER(_sz)]
+_L.lic_rans_decode_slab_range.argtypes = [_P, _P, _sz, _P, Shape, _u32, _u32, _u32, _P]
 _L.lic_cdf_quantize.argtypes = [_P, _u32, _P]
 _L.lic_sigmas.argtypes = [_P, _i, ctypes.POINTER(ctypes.POINTER(ctypes.c_float)), ctypes.POINTER(_u32)]
 _L.lic_cdf64_gaussian.argtypes = [_P, _u32, ctypes.c_double, _P, _u32, _P, _P]
@@ -311,6 +313,33 @@ class RansTables:
         if st:
             raise LicError(st, "rans_encode_fast")
         return out[: n.value].tobytes()
+
+    def encode_range(self, sym, K, k_begin, k_end, rows=None):
+        """lic_rans_encode_slab_range: (strings of slabs [k_begin, k_end) back to back, their lengths)."""
+        sym = np.ascontiguousarray(sym, np.int8)
+        rows = None if rows is None else np.ascontiguousarray(rows, np.uint8)
+        cap = 2 * sym.size + 64 * K
+        out = np.empty(cap, np.uint8)
+        lens = np.zeros(k_end - k_begin, np.uint32)
+        n = ctypes.c_size_t(0)
+        st = _L.lic_rans_encode_slab_range(self._h, _ptr(sym), _ptr(rows), Shape(*sym.shape), K, k_begin, k_end,
+                                           _ptr(out), cap, _ptr(lens), ctypes.byref(n))
+        if st:
+            raise LicError(st, "rans_encode_slab_range")
+        return out[: n.value].tobytes(), lens
+
+    def decode_range(self, data, shape, K, k_begin, k_end, rows=None, out=None):
+        """lic_rans_decode_slab_range: slabs [k_begin, k_end) of the framed stream into `out`."""
+        rows = None if rows is None else np.ascontiguousarray(rows, np.uint8)
+        out = np.zeros(shape, np.int8) if out is None else out
+        buf = np.frombuffer(bytes(data), np.uint8) if len(data) else np.zeros(1, np.uint8)
+        st = _L.lic_rans_decode_slab_range(self._h, _ptr(buf), len(data), _ptr(rows), Shape(*shape), K, k_begin, k_end,
+                                           _ptr(out))
+        if st == LIC_ECORRUPT:
+            raise CorruptStream(st, "corrupt stream")
+        if st:
+            raise LicError(st, "rans_decode_slab_range")
+        return out
 
     def decode(self, data, shape, rows=None, substreams=1):
         shp = Shape(*shape) if len(shape) == 3 else Shape(1, 1, int(np.prod(shape)))
@@ -515,11 +544,11 @@ class Pipeline:
 
     def __init__(self, codec: Codec, coder_threads: int, batch: int, inflight: int = 2, u8: bool = True,
                  serial: bool = False, keep_bitstreams: bool = False, substreams: int = 1, coder: int = 0,
-                 pace_fps: float = 0.0, timeline: bool = False):
+                 pace_fps: float = 0.0, timeline: bool = False, coder_parts: int = 1):
         self.codec = codec
         self.substreams = substreams
         self.cfg = PipelineConfig(coder_threads, batch, inflight, int(u8), int(serial), int(keep_bitstreams),
-                                  substreams, coder, float(pace_fps), int(timeline))
+                                  substreams, coder, float(pace_fps), int(timeline), coder_parts)
         self._h = _P()
         st = _L.lic_pipeline_open(codec.handle, ctypes.byref(self.cfg), ctypes.byref(self._h))
         if st:

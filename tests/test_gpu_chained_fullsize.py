@@ -142,14 +142,16 @@ def test_c3_decode_from_oracle_symbols(codec, c3):
         assert np.max(np.abs(o8[b].astype(np.int32) - ref8)) <= 1
 
 
-def test_c3_pipeline_bitstreams_bit_exact(lic, codec, c3):
-    """c19 through the bench's own pipeline (batch 4, 32 y substreams, frames in HBM)."""
+@pytest.mark.parametrize("parts", [2, 1])
+def test_c3_pipeline_bitstreams_bit_exact(lic, codec, c3, parts):
+    """c19 through the bench's own pipeline (batch 4, 32 y substreams, frames in HBM; each frame's
+    y string coded as 2 slab ranges on separate coder threads as bench.py runs it, or as 1)."""
     import torch
     dev_in = torch.from_numpy(c3["frames"]).cuda()
     dev_out = torch.empty_like(dev_in)
     ys, yi, zs, _ = _encode(codec, dev_in, B)          # the planes the pipeline codes (deterministic)
     pipe = lic.Pipeline(codec, coder_threads=4, batch=B, inflight=2, u8=True, keep_bitstreams=True,
-                        substreams=K_SUB)
+                        substreams=K_SUB, coder_parts=parts)
     st = pipe.run(dev_in, dev_out, B)
     assert st["symbol_mismatches"] == 0
     tabs, w = c3["tabs"], c3["w"]

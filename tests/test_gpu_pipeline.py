@@ -23,12 +23,12 @@ def lic():
     return L
 
 
-def run_pipeline(lic, codec, frames, serial, inflight=3, threads=3, substreams=1, coder=0):
+def run_pipeline(lic, codec, frames, serial, inflight=3, threads=3, substreams=1, coder=0, parts=1):
     import torch
     fin = torch.from_numpy(frames).cuda()
     fout = torch.zeros_like(fin)
     p = lic.Pipeline(codec, coder_threads=threads, batch=B, inflight=inflight, u8=True, serial=serial,
-                     keep_bitstreams=True, substreams=substreams, coder=coder)
+                     keep_bitstreams=True, substreams=substreams, coder=coder, coder_parts=parts)
     st = p.run(fin, fout, NF)
     streams = [p.bitstream(i) for i in range(NF)]
     p.close()
@@ -173,4 +173,19 @@ def test_errors_are_status_codes(lic):
     with pytest.raises(lic.LicError) as e:                  # truncated weights container
         lic.Codec(bytes(bad[:-10]), 128, 128)
     assert e.value.status == lic.LIC_EDIGEST
+    codec.close()
+
+
+@pytest.mark.parametrize("K,parts", [(32, 2), (32, 4), (16, 2)])
+def test_coder_parts_same_bitstreams(lic, K, parts):
+    """Each frame's y string coded as `parts` slab ranges on separate coder threads
+    (lic_rans_encode_slab_range / lic_rans_decode_slab_range): the same strings, frames and
+    lossless round trip as one coder task per frame."""
+    spec = ModelSpec(kind=1, N=128, M=192)
+    codec = lic.Codec(write_licw(spec, generate_weights(spec, seed=0)), H, W, max_batch=B)
+    frames = synth_frames_u8(NF, H, W, seed=23)
+    st1, s1, o1 = run_pipeline(lic, codec, frames, serial=False, substreams=K, threads=4, parts=1)
+    st2, s2, o2 = run_pipeline(lic, codec, frames, serial=False, substreams=K, threads=4, parts=parts)
+    assert st1["symbol_mismatches"] == 0 and st2["symbol_mismatches"] == 0
+    assert s1 == s2 and np.array_equal(o1, o2)
     codec.close()

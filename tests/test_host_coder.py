@@ -227,3 +227,32 @@ def test_zero_frequency_symbol_rejected(lic, K):
     sym[3, 1, 2] = 1                                                        # nonzero frequency: fine
     data = t.encode(sym, substreams=K)
     assert np.array_equal(t.decode(data, sym.shape, substreams=K), sym)
+
+
+@pytest.mark.parametrize("K,parts", [(32, 2), (32, 4), (16, 2), (7, 3)])
+def test_slab_ranges_compose_the_slab_stream(lic, K, parts):
+    """lic_rans_encode_slab_range over a partition of the K slabs, concatenated in order behind
+    the K big-endian lengths, is exactly lic_rans_encode_slabs' stream; lic_rans_decode_slab_range
+    of every part restores the plane (the pipeline codes one frame's slabs on several threads)."""
+    from lic_synth import scale_table
+    rng = np.random.default_rng(K * 10 + parts)
+    C, H, W = 64, 12, 20
+    cdf = lic.cdf_build(scale_table(), 32)
+    idx = rng.integers(0, 30, (C, H, W)).astype(np.uint8)
+    sym = np.clip(np.round(rng.standard_normal((C, H, W)) * scale_table()[idx]), -32, 32).astype(np.int8)
+    t = lic.RansTables(cdf)
+    ref = t.encode(sym, idx, substreams=K)
+    bounds = [round(p * K / parts) for p in range(parts + 1)]
+    strings, lens = [], []
+    for kb, ke in zip(bounds[:-1], bounds[1:]):
+        s, l = t.encode_range(sym, K, kb, ke, rows=idx)
+        strings.append(s)
+        lens.extend(int(x) for x in l)
+    framed = b"".join(n.to_bytes(4, "big") for n in lens) + b"".join(strings)
+    assert framed == ref
+    out = np.zeros_like(sym)
+    for kb, ke in zip(bounds[:-1], bounds[1:]):
+        t.decode_range(ref, sym.shape, K, kb, ke, rows=idx, out=out)
+    assert np.array_equal(out, sym)
+    with pytest.raises(lic.LicError):
+        t.encode_range(sym, K, 3, 3, rows=idx)
