@@ -471,7 +471,7 @@ def measure(args, name, rank, world, local, threads, full):
     # ---- 8. paced source: submit -> complete latency at 80 % of the measured per-GPU rate
     pace = 0.8 * value / world
     pp = lic.Pipeline(codec, inflight=args.inflight, pace_fps=pace, **mk)
-    npace = max(B * 16, min(nfr, int(pace * 1.0) // B * B))
+    npace = min(nloc, max(B * 4, int(pace * 1.0) // B * B))     # ~1 s of frames, within the device set
     stp = pp.run(dev_in, dev_out, npace)
     pp.close()
 
