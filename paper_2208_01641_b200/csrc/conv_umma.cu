@@ -851,6 +851,29 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         int sat = 0;
         int ovf = 0;                                // activations saturated to the fp16 range
         int wround = 0;                             // per-warp staging: rounds this warp has stored
+        // GDN / IGDN with per-warp staging of one 32-channel round (BN = 128): a tile's y is staged
+        // into the warp's slot right away, but its bulk tensor store -- whose issue stalls on the
+        // TMA queue for ~1-2k cycles -- is issued while the NEXT tile waits for its norm MMAs
+        // (DESIGN.md §7); d_* hold the deferred store's coordinates
+        const bool defer = GC == 2 && p.wst_ch == 32 && p.wst_slots == 1;
+        bool d_pending = false;
+        int d_cb = 0, d_x = 0, d_y = 0, d_b = 0, d_ph = 0;
+        auto flush_deferred = [&]() {
+            if (!d_pending) return;
+            d_pending = false;
+            fence_proxy_async_smem();                  // the slot's generic writes -> the async proxy
+            __syncwarp();
+            if (lane == 0) {
+                const uint8_t* hs = smem + p.off_ostage + (uint32_t)(warp - 4) * 4096u;
+                if (p.nphase == 1) {
+                    tma_store_5d(&mapOH, hs, d_cb, d_x, d_y, d_b, 0);
+                } else {
+                    const CUtensorMap* om = d_ph == 0 ? &mapOH : d_ph == 1 ? &mapOL : d_ph == 2 ? &mapO2 : &mapO3;
+                    tma_store_4d(om, hs, d_cb, d_x, d_y, 0);
+                }
+                bulk_commit();
+            }
+        };
         for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
             TileCoord tc = decode_tile(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
@@ -1020,6 +1043,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     }
                 }
                 if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_XSQ);
+                if (defer) flush_deferred();             // the previous tile's y, under the norm MMAs
                 if (threadIdx.x == 128) mbar_wait(norm_bar, norm_phase);
                 norm_phase ^= 1;
                 named_bar_sync(3, 32 * kEpiWarps);
@@ -1084,7 +1108,34 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 }
                 released = true;
                 if (out && !(p.dbg_nostore & 1)) {
-                    if (tma_ok && p.wst_ch) {
+                    if (defer && tma_ok) {
+                        // stage now (the slot's previous store has been issued and read), store
+                        // during the next tile's norm wait (or at the end)
+                        const uint32_t rows_b = 64u;
+                        const uint32_t sw = (((uint32_t)lane * rows_b) >> 7) & 3u;
+                        const uint32_t rowa = smem_u32(smem) + (uint32_t)p.off_ostage + (uint32_t)(warp - 4) * 4096u +
+                                              (uint32_t)lane * rows_b;
+                        if (lane == 0) bulk_wait_read0();
+                        __syncwarp();
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+#pragma unroll
+                            for (int k = 0; k < 2; ++k) {
+                                uint4 hv, lv;
+                                const float* v8 = x[j] + 8 * k;
+                                split2(v8[0], v8[1], hv.x, lv.x); split2(v8[2], v8[3], hv.y, lv.y);
+                                split2(v8[4], v8[5], hv.z, lv.z); split2(v8[6], v8[7], hv.w, lv.w);
+                                const uint32_t o = ((((uint32_t)(2 * j + k)) ^ sw) & 3u) << 4;
+                                stsu4(rowa + o, hv);
+                                if (p.split == 2) stsu4(rowa + 32u * rows_b + o, lv);
+                            }
+                        d_cb = co0 + g * G;
+                        d_ph = py * 2 + px;
+                        d_x = tc.gx0 + tx0;
+                        d_y = p.nphase == 1 ? tc.gy0 + ty0 : tc.b * p.Hg + tc.gy0 + ty0;
+                        d_b = tc.b;
+                        d_pending = true;
+                    } else if (tma_ok && p.wst_ch) {
                         // per-warp staging: this warp's 32 pixels x its G channels in
                         // rounds of wst_ch channels (rows of 2 * wst_ch bytes, swizzled like the
                         // out maps), each round written by the warp's own bulk tensor stores --
@@ -1345,6 +1396,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             }
             if (threadIdx.x == 128) LIC_TRACE(it, T_EPI_END);
         }
+        if (defer) flush_deferred();
         if (p.tma_out && lane == 0 && (g == 0 || p.wst_ch)) bulk_wait0();
         if (p.sat_count) {
             for (int o = 16; o > 0; o >>= 1) sat += __shfl_xor_sync(0xffffffffu, sat, o);
