@@ -175,6 +175,9 @@ struct lic_codec {
     int small_bn = 0;              // N tile of the h_a / h_s layers (env LIC_SMALL_BN=64|128; 0 = whole Cout: measured no gain)
     int s2halo_enabled = 1;        // 5x5/s2 convs in parity-sub-grid halo mode (env LIC_S2HALO=0: per-tap tiles)
     int a_hi_only_enabled = 1;     // g_s L1 skips the zero lo plane of the integer y-hat (env LIC_YHAT_HI=0: off)
+    int raw_tma_enabled = 1;       // u8 frames: raw patches by TMA (env LIC_RAW_TMA=0: cp.async)
+    int l1_stage_split = 1;        // u8 frames: hi-only A stages, twice as many (env LIC_L1_STAGES=0: off)
+    int g2_enabled = 1;            // two-group GDN epilogue for g_a L1 (env LIC_G2=0: off)
     int l1_int_enabled = 1;        // u8 frames: integer samples into g_a L1, one MMA pass (env LIC_L1_INT=0: off)
     int l1_conv_enabled = 1;       // ... converted arithmetically, 8 per item, no LUT (env LIC_L1_CONV=0: LUT)
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
@@ -269,6 +272,19 @@ static bool encode_act_map(CUtensorMap* m, const __half* base, int C, int W, int
     cuuint32_t es5[5] = {1, (cuuint32_t)es, (cuuint32_t)es, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, (void*)base, dims, str, box, es5, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// the u8 HWC frames as a 3-D byte tensor (3W, H, B), box = one fused-L1 raw patch (128 B x 19 rows)
+static bool encode_u8_frame_map(CUtensorMap* m, const void* base, int W, int H, int B) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)W * 3, (cuuint64_t)H, (cuuint64_t)B};
+    cuuint64_t str[2] = {(cuuint64_t)W * 3, (cuuint64_t)W * 3 * H};
+    cuuint32_t box[3] = {128, 19, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, str, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -477,7 +493,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     const uint32_t a_bytes = 128 * 64 * 2, b_bytes = (uint32_t)(P.BN / P.cg) * 64 * 2;
     const uint32_t gamma_bytes = gdn ? (uint32_t)(P.BN / 64) * b_bytes : 0;
     // bias / beta / mu, scale table, halo tap offsets (+ GDN: per-pixel norm exponents, 128 x 4 B)
-    const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64 + kMaxTaps) * 4 + (gdn ? 512u : 0u);
+    const uint32_t par_bytes = (uint32_t)(3 * P.BN * P.n_ntiles + 64 + kMaxTaps) * 4 + (gdn ? 1024u : 0u);
     const uint32_t budget = 227u * 1024u;
     // TMA-store epilogue: 4 lane quadrants x 8 KB block slots (1 or 2 slots), when the layer writes an activation and the
     // pipeline keeps >= 3 stages with it (env LIC_TMA_OUT=0 disables)
@@ -513,8 +529,8 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         const uint32_t patch_bytes = 2u * 19u * 112u * 2u;           // hi + lo planes
         P.off_lut = P.off_patch + 2 * patch_bytes;
         P.off_halo = 0;
-        P.off_raw = (P.off_lut + 257 * 4 + 15) / 16 * 16;
-        P.off_gamma = (P.off_raw + 2 * 19 * 112 + 1023) / 1024 * 1024;
+        P.off_raw = (P.off_lut + 257 * 4 + 127) / 128 * 128;
+        P.off_gamma = (P.off_raw + 2 * 19 * 128 + 1023) / 1024 * 1024;     // raw: 2 x 19 rows x 128 B
     } else if (gs4g) {
         P.halo = 0;
         P.halo_slots = 0;
@@ -637,6 +653,11 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.wst_ch = (G % 32 == 0) ? 32 : 16;
         P.wst_slots = P.wst_ch == 32 ? 1 : 2;
     }
+    // two-group GDN epilogue (env LIC_G2=0: off): the fused g_a L1, whose tiles are short (K = 80)
+    // and whose time is the GDN epilogue's
+    P.g2 = 0;
+    if (gdn && P.BN == 128 && P.wst_ch == 32 && P.wst_slots == 1 && P.n_accbuf == 2 && gemm_l1 && c->g2_enabled)
+        P.g2 = 1;
     P.L = c->L;
     // tensor maps
     const int ntaps_w = (gemm_l1 || P.gather) ? 1 : (P.pack4 ? 9 : Ly.k * Ly.k);
@@ -698,7 +719,8 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     return LIC_OK;
 }
 
-static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int batch, cudaStream_t st) {
+static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int batch, cudaStream_t st,
+                            const CUtensorMap* mapA = nullptr) {
     ConvParams P = P0;
     P.batch = batch;
     const int txs = (P.tiles_x + P.cg - 1) / P.cg;          // tiles (or CTA-pair tiles) along x
@@ -717,7 +739,7 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
         CK(cudaEventRecord(c->ev[2 * c->ev_used], st));
     }
     {
-        const cudaError_t e = launch_conv_umma(Ly.mapA, Ly.mapB, Ly.mapG, Ly.mapOH, Ly.mapOL, Ly.mapO2, Ly.mapO3, P,
+        const cudaError_t e = launch_conv_umma(mapA ? *mapA : Ly.mapA, Ly.mapB, Ly.mapG, Ly.mapOH, Ly.mapOL, Ly.mapO2, Ly.mapO3, P,
                                                grid, st);
         if (e != cudaSuccess)
             return fail(c, LIC_ECUDA, "launch of layer %d (grid %d, cg %d, smem %u, tiles %d, stages %d, halo %d): %s",
@@ -932,6 +954,9 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_PDL")) c->pdl_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_GS4_GATHER")) c->gs4_gather = (e[0] != '0');
     if (const char* e = std::getenv("LIC_L1_INT")) c->l1_int_enabled = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_G2")) c->g2_enabled = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_L1_STAGES")) c->l1_stage_split = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_RAW_TMA")) c->raw_tma_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
@@ -1268,7 +1293,19 @@ static lic_status encode_impl(lic_codec* c, const void* frames, int hwc, uint32_
         ConvParams p = c->layers[GA1].prm;             // fused im2col: reads the frames directly
         p.frame = fdev; p.fr_u8 = hwc; p.fr_H = c->H; p.fr_W = c->W; p.fr_top = c->top; p.fr_left = c->left;
         p.l1_int = (hwc && c->l1_int_enabled) ? (c->l1_conv_enabled ? 2 : 1) : 0;
-        if ((r = run_layer(c, c->layers[GA1], p, B, st))) return r;
+        if (p.l1_int && p.split == 2 && p.stage_bytes == 2u * 128u * 64u * 2u && c->l1_stage_split) {
+            // integer u8 samples have no lo plane: the same shared memory holds twice as many
+            // (hi-only) A stages, so the builders run a tile further ahead of the MMA warp
+            p.stage_bytes /= 2;
+            p.stages *= 2;
+        }
+        // u8 frames with 16-byte rows: each tile's raw patch is one TMA box of the frame
+        CUtensorMap fmap{};
+        p.raw_tma = 0;
+        if (hwc && c->raw_tma_enabled && (3 * c->W) % 16 == 0 && ((uintptr_t)fdev & 15) == 0 &&
+            encode_u8_frame_map(&fmap, fdev, c->W, c->H, B))
+            p.raw_tma = 1;
+        if ((r = run_layer(c, c->layers[GA1], p, B, st, p.raw_tma ? &fmap : nullptr))) return r;
     }
     for (int id : {GA2, GA3})
         if ((r = run_layer(c, c->layers[id], c->layers[id].prm, B, st))) return r;

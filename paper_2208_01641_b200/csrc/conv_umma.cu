@@ -28,6 +28,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "layer.h"
 #include "ptx.cuh"
 
@@ -137,8 +139,9 @@ constexpr int kL1Pitch = 112;                                        // halves p
 constexpr uint32_t kL1PlaneBytes = kL1PH * kL1Pitch * 2;             // one fp16 plane of a patch
 constexpr int kL1K = 80;                                             // K = 16*ky + 3*kx + c, 5 rows of 16
 constexpr int kL1Builders = 96;                                      // warps 0, 2, 3
-constexpr int kL1RawWords = 28;                                      // >= (3 + 105) / 4 words per raw row
-constexpr uint32_t kL1RawBytes = kL1PH * kL1RawWords * 4;           // one raw u8 patch
+constexpr int kL1RawWords = 28;                                      // >= (3 + 105) / 4 words loaded per raw row (cp.async)
+constexpr int kL1RawPitch = 128;                                     // bytes per raw row (TMA box: 16-byte aligned start + 105 B)
+constexpr uint32_t kL1RawBytes = kL1PH * kL1RawPitch;               // one raw u8 patch (2432 B, a multiple of 128)
 static_assert(kL1Wt == 16, "build_l1 decodes r -> (r >> 4, r & 15)");
 
 // MUFU.RSQ without the denormal-input fix-up (GDN/IGDN: beta + n >= beta > 0, normal)
@@ -153,13 +156,29 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
     return y;
 }
 __device__ __forceinline__ float hround(float v) { return __half2float(__float2half_rn(v)); }
-// (a, b) -> packed fp16 hi = rn(a, b) and lo = rn(a - hi, b - hi): one pack per plane, the hi
-// values unpacked from the pack itself (no second rounding of a and b)
+// (a, b) -> packed fp16 hi = rn(a, b) and lo = rn(a - hi, b - hi): one pack per plane; the
+// residuals a - hi are mixed-precision adds of the packed halves (add.f32.f16: one FHADD each,
+// exact -- the same values as converting hi to f32 and subtracting)
 __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
     const __half2 h = __floats2half2_rn(a, b);
-    const float2 hf = __half22float2(h);
     hi = *reinterpret_cast<const uint32_t*>(&h);
-    lo = h2_bits(a - hf.x, b - hf.y);
+    float ra, rb;
+    asm("{\n\t.reg .f16 l, u;\n\tmov.b32 {l, u}, %2;\n\tneg.f16 l, l;\n\tneg.f16 u, u;\n\t"
+        "add.rn.f32.f16 %0, l, %3;\n\tadd.rn.f32.f16 %1, u, %4;\n\t}"
+        : "=f"(ra), "=f"(rb) : "r"(hi), "f"(a), "f"(b));
+    lo = h2_bits(ra, rb);
+}
+// hi + lo of one packed (hi, lo) fp16 split value pair, half SEL (0 low, 1 high), in f32
+template <int SEL>
+__device__ __forceinline__ float join_h(uint32_t hi2, uint32_t lo2) {
+    float r;
+    if constexpr (SEL == 0)
+        asm("{\n\t.reg .f16 a, b, c, d;\n\tmov.b32 {a, b}, %1;\n\tmov.b32 {c, d}, %2;\n\t"
+            ".reg .f32 t;\n\tcvt.f32.f16 t, c;\n\tadd.rn.f32.f16 %0, a, t;\n\t}" : "=f"(r) : "r"(hi2), "r"(lo2));
+    else
+        asm("{\n\t.reg .f16 a, b, c, d;\n\tmov.b32 {a, b}, %1;\n\tmov.b32 {c, d}, %2;\n\t"
+            ".reg .f32 t;\n\tcvt.f32.f16 t, d;\n\tadd.rn.f32.f16 %0, b, t;\n\t}" : "=f"(r) : "r"(hi2), "r"(lo2));
+    return r;
 }
 
 // 8 consecutive channels -> one 16-byte fp16 hi vector (+ one lo vector)
@@ -205,7 +224,7 @@ enum TraceEv { T_MMA_START = 0, T_MMA_END = 1, T_NORM_ISSUE = 2, T_EPI_START = 3
                T_B_PATCH = 8, T_B_C0_READY = 9, T_B_C0_DONE = 10, T_B_C1_READY = 11, T_B_C1_DONE = 12,
                T_MMA_K0 = 13, T_MMA_KL = 14, T_PEER_B_DONE = 15, T_B_RAW = 16,
                T_EPI_P2 = 17, T_EPI_ACQ = 18, T_EPI_STAGED = 19,
-               T_W_HALO = 20, T_W_B = 21 };
+               T_W_HALO = 20, T_W_B = 21, T_B_RAWISS = 22 };
 #define LIC_TRACE(it, ev)                                                                         \
     do {                                                                                          \
         if (p.trace && blockIdx.x == 0 && (it) < kTraceTiles)                                     \
@@ -250,6 +269,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     // the TMEM base address written by tcgen05.alloc, in a 16-byte granule of its own
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ((p.off_bar + 8u * 34u + 15u) & ~15u));
     uint32_t* xsq_cnt = tmem_slot + 4;              // epilogue warps that wrote x^2 (cumulative)
+    // two-group GDN epilogue (p.g2): per accumulator buffer, x^2 written / norm MMAs complete
+    uint64_t* xsq2_bar = reinterpret_cast<uint64_t*>(smem + p.off_bar + 320u);    // [2]
+    uint64_t* norm2_bar = xsq2_bar + 2;                                            // [2]
+    uint64_t* rawfull_bar = norm2_bar + 2;          // [2] fused L1: raw u8 patch landed (TMA)
     float* s_bias = reinterpret_cast<float*>(smem + p.off_par);   // [cout_pad]
     float* s_beta = s_bias + p.BN * p.n_ntiles;                     // [cout_pad]
     float* s_mu = s_beta + p.BN * p.n_ntiles;                       // [cout_pad]
@@ -261,6 +284,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     constexpr bool kGdn = GC > 0;
+    // two-group GDN epilogue (BN = 128): epilogue warps 4-11 take the even tiles of this CTA,
+    // 12-19 the odd ones, each warp 32 pixels x 64 channels; the groups' norm round trips overlap
+    const bool g2 = GC == 2 && p.g2;
+    const uint32_t epi_arrivals = (g2 ? kEpiWarps / 2 : kEpiWarps) * CG;   // per tile
     const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
     const bool leader = rank == 0;
     const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;     // pair (or CTA) index and count
@@ -271,7 +298,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         // fused L1: the 3 builder warps of each CTA arrive on the leader's full barrier
         const uint32_t full_cnt = p.fuse_l1 ? 3u * CG : 1u;
         for (int s = 0; s < p.stages; ++s) { mbar_init(&full_bar[s], full_cnt); mbar_init(&empty_bar[s], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], kEpiWarps * CG); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], epi_arrivals); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&xsq2_bar[i], epi_arrivals); mbar_init(&norm2_bar[i], 1); }
+        for (int i = 0; i < 2; ++i) mbar_init(&rawfull_bar[i], 1);
         mbar_init(norm_bar, 1);
         mbar_init(gamma_bar, 1);
         for (int i = 0; i < 4; ++i) { mbar_init(&hfull_bar[i], 1); mbar_init(&hempty_bar[i], 1); }
@@ -312,6 +341,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             stsu4(smem_u32(smem) + 16 * i, make_uint4(0, 0, 0, 0));
         for (uint32_t i = threadIdx.x; i < 4 * kL1PlaneBytes / 16; i += kThreads)
             stsu4(smem_u32(smem + p.off_patch) + 16 * i, make_uint4(0, 0, 0, 0));
+        for (uint32_t i = threadIdx.x; i < 2 * kL1RawBytes / 16; i += kThreads)    // (cp.async fills 112 of 128 B per row)
+            stsu4(smem_u32(smem + p.off_raw) + 16 * i, make_uint4(0, 0, 0, 0));
         uint32_t* lut = reinterpret_cast<uint32_t*>(smem + p.off_lut);
         for (int u = threadIdx.x; u < 257; u += kThreads) {
             uint32_t h = 0, l = 0;
@@ -371,8 +402,21 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         const bool fast = p.fr_u8 && (p.fr_W & 3) == 0;
         const bool lo_on = p.split == 2 && !p.l1_int;     // the lo planes of patch and A tiles
         const bool int_fast = fast && p.l1_int == 2;            // integer samples, no LUT, shifted copy
+        // p.raw_tma: the raw patch is one TMA box (128 B x 19 rows of the u8 frame, mapA) starting at
+        // the 16-byte boundary at or below the patch's first byte (a TMA start coordinate must be
+        // 16-byte aligned in the innermost dimension: scripts/probes/u8_tma_probe.cu), zero fill
+        // outside the frame, completing on rawfull_bar
+        const bool raw_tma = fast && p.raw_tma;
         auto raw_issue = [&](int tt, int buf) {
             const TileCoord tn = decode_tile(p, tt, rank);
+            if (raw_tma) {
+                if (bw == 0 && lane == 0) {
+                    mbar_arrive_expect_tx(&rawfull_bar[buf], kL1RawBytes);
+                    tma_load_3d(smem + p.off_raw + (uint32_t)buf * kL1RawBytes, &mapA, &rawfull_bar[buf],
+                                (3 * (2 * tn.gx0 - 2 - p.fr_left)) & ~15, 2 * tn.gy0 - 2 - p.fr_top, tn.b);
+                }
+                return;
+            }
             const uint8_t* fr = reinterpret_cast<const uint8_t*>(p.frame);
             const int rowb = 3 * p.fr_W;
             const int iyn = 2 * tn.gy0 - 2 - p.fr_top, ws = (3 * (2 * tn.gx0 - 2 - p.fr_left)) >> 2;   // floor
@@ -382,7 +426,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 const int iy = iyn + r, gw = 4 * (ws + w);
                 const bool ok = iy >= 0 && iy < p.fr_H && gw >= 0 && gw < rowb;
                 const uint8_t* src = ok ? fr + ((size_t)tn.b * p.fr_H + iy) * rowb + gw : fr;
-                cp_async4(rb + 4u * q, src, ok ? 4u : 0u);
+                cp_async4(rb + (uint32_t)(r * kL1RawPitch + 4 * w), src, ok ? 4u : 0u);
             }
             cp_async_commit();
         };
@@ -405,14 +449,21 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 // integer samples (l1_int): u8 -> f16 arithmetically, 8 values per item (3 raw
                 // words -> one 16-byte store); the lo plane holds a copy shifted by 4 bytes so
                 // that every K-row segment below is two 8-byte-aligned loads
-                cp_async_wait_all();
-                named_bar_sync_na(4, kL1Builders);                          // raw[it & 1] complete
+                if (raw_tma) {
+                    mbar_wait(&rawfull_bar[it & 1], (uint32_t)(it >> 1) & 1u);
+                } else {
+                    cp_async_wait_all();
+                    named_bar_sync_na(4, kL1Builders);                      // raw[it & 1] complete
+                }
                 if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_RAW);
-                const uint32_t rw = raw_s + (uint32_t)(it & 1) * kL1RawBytes;
-                const uint32_t sel = 0x3210u + (uint32_t)((3 * ix0) & 3) * 0x1111u;
+                // the patch's first byte: at (3 ix0) mod 4 of the raw row (cp.async, word-aligned
+                // start) or (3 ix0) mod 16 (TMA, 16-byte aligned start)
+                const uint32_t sh = (uint32_t)(3 * ix0) & (raw_tma ? 15u : 3u);
+                const uint32_t rw = raw_s + (uint32_t)(it & 1) * kL1RawBytes + (sh & ~3u);
+                const uint32_t sel = 0x3210u + (sh & 3u) * 0x1111u;
                 for (int q = bt; q < kL1PH * 14; q += kL1Builders) {
                     const int r = q / 14, m = q - 14 * r;
-                    const uint32_t src = rw + (uint32_t)(r * (4 * kL1RawWords) + 8 * m);
+                    const uint32_t src = rw + (uint32_t)(r * kL1RawPitch + 8 * m);
                     const uint2 w01 = ldsu2(src);
                     const uint32_t w2 = ldsu(src + 8);
                     const uint32_t b0 = __byte_perm(w01.x, w01.y, sel), b1 = __byte_perm(w01.y, w2, sel);
@@ -425,17 +476,21 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     if (m < 13) stsu(pbl + d + 16, h3);                    // (values 110, 111: unused)
                 }
             } else if (fast) {
-                cp_async_wait_all();
-                named_bar_sync_na(4, kL1Builders);                          // raw[it & 1] complete
+                if (raw_tma) {
+                    mbar_wait(&rawfull_bar[it & 1], (uint32_t)(it >> 1) & 1u);
+                } else {
+                    cp_async_wait_all();
+                    named_bar_sync_na(4, kL1Builders);                      // raw[it & 1] complete
+                }
                 if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_RAW);
-                const uint32_t rb = raw_s + (uint32_t)(it & 1) * kL1RawBytes + (uint32_t)((3 * ix0) & 3);
+                const uint32_t rb = raw_s + (uint32_t)(it & 1) * kL1RawBytes + ((uint32_t)(3 * ix0) & (raw_tma ? 15u : 3u));
 #pragma unroll 4
                 for (int r = 0; r < kL1PH; ++r) {
-                    const uint32_t w0 = ldsu(lut_s + 4u * ldsb(rb + r * (4 * kL1RawWords) + e0));
+                    const uint32_t w0 = ldsu(lut_s + 4u * ldsb(rb + r * kL1RawPitch + e0));
                     stsh(pbh + 2u * (r * kL1Pitch + e0), w0);
                     if (lo_on) stsh(pbl + 2u * (r * kL1Pitch + e0), w0 >> 16);
                     if (has1) {
-                        const uint32_t w1 = ldsu(lut_s + 4u * ldsb(rb + r * (4 * kL1RawWords) + e1));
+                        const uint32_t w1 = ldsu(lut_s + 4u * ldsb(rb + r * kL1RawPitch + e1));
                         stsh(pbh + 2u * (r * kL1Pitch + e1), w1);
                         if (lo_on) stsh(pbl + 2u * (r * kL1Pitch + e1), w1 >> 16);
                     }
@@ -495,6 +550,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             // next tile's raw bytes (its buffer was last read converting tile it-1, before the
             // raw barrier of this tile)
             if (fast && t + ncl < p.total_tiles) raw_issue(t + ncl, (it + 1) & 1);
+            if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_RAWISS);
             // ---- A tiles, one stage per 64-column K chunk
             for (int c = 0; c < p.kchunks; ++c) {
                 const int kc = c * 64;
@@ -665,7 +721,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         uint32_t pend_dcol = 0, xsq_phase = 0;
         int pend_it = 0;
         bool gamma_ready = false;
-        auto issue_norm = [&]() {
+        auto issue_norm = [&](uint64_t* done_bar) {
             if (!gamma_ready) { mbar_wait(gamma_bar, 0); gamma_ready = true; }
             tc_fence_after();
             constexpr int G = 16 * (GC > 0 ? GC : 1);
@@ -681,19 +737,33 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     mma_ts(ncol, ahi, bd, kk != 0);
                     mma_ts(ncol, alo, bd, 1u);
                 }
-                commit(norm_bar);
+                commit(done_bar);
             }
             __syncwarp();
             if (lane == 0) LIC_TRACE(pend_it, T_NORM_ISSUE);
             pend = 0;
         };
         int xsq_seen = 0;              // tiles whose x^2 the MMA warp has consumed
+        // two-group epilogue: tiles whose main MMAs are committed / whose norm MMAs are issued
+        // (in tile order; tile n uses accumulator buffer n & 1, the (n >> 1)-th phase of its barriers)
+        int g2_committed = 0, g2_nn = 0;
         auto poll_norm = [&]() {       // cheap volatile smem read; the mbarrier wait then completes at once
+            if constexpr (GC == 2) {
+                if (g2) {
+                    while (g2_nn < g2_committed && mbar_test(&xsq2_bar[g2_nn & 1], (uint32_t)(g2_nn >> 1) & 1u)) {
+                        pend_dcol = (uint32_t)((g2_nn & 1) * p.acc_stride);
+                        pend_it = g2_nn;
+                        issue_norm(&norm2_bar[g2_nn & 1]);
+                        ++g2_nn;
+                    }
+                    return;
+                }
+            }
             if (kGdn && pend && *reinterpret_cast<volatile uint32_t*>(xsq_cnt) >= (uint32_t)(kEpiWarps * CG * (xsq_seen + 1))) {
                 mbar_wait(xsq_bar, xsq_phase);
                 xsq_phase ^= 1;
                 ++xsq_seen;
-                issue_norm();
+                issue_norm(norm_bar);
             }
         };
         // blocking waits of the MMA warp keep polling for a pending norm (GDN), so that the
@@ -715,7 +785,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             TileCoord tc = decode_tile(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
             const uint32_t use = (p.n_accbuf == 2) ? (uint32_t)(it >> 1) : (uint32_t)it;
-            if (kGdn && pend && p.n_accbuf == 1) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(); }
+            if (kGdn && !g2 && pend && p.n_accbuf == 1) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
             wait_poll(&tempty_bar[buf], (use & 1) ^ 1);
             tc_fence_after();
             if (lane == 0) LIC_TRACE(it, T_MMA_START);
@@ -830,15 +900,27 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 p.trace[(size_t)it * kTraceEv + T_W_B] = (unsigned long long)w_b;
             }
 
-            if (kGdn) {
+            if (g2) {
+                g2_committed = it + 1;
+                poll_norm();
+            } else if (kGdn) {
                 // the previous tile's norm must be issued before this one becomes pending
-                if (pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(); }
+                if (pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
                 pend = 1;
                 pend_it = it;
                 pend_dcol = (uint32_t)(buf * p.acc_stride);
             }
         }
-        if (kGdn && pend && leader) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(); }
+        if (g2 && leader) {
+            while (g2_nn < g2_committed) {
+                mbar_wait(&xsq2_bar[g2_nn & 1], (uint32_t)(g2_nn >> 1) & 1u);
+                pend_dcol = (uint32_t)((g2_nn & 1) * p.acc_stride);
+                pend_it = g2_nn;
+                issue_norm(&norm2_bar[g2_nn & 1]);
+                ++g2_nn;
+            }
+        }
+        if (kGdn && !g2 && pend && leader) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
     } else if (warp >= 4) {
         // ====================== epilogue ======================
         if (p.pdl) griddep_wait();                  // global writes only after the previous kernel
@@ -874,7 +956,192 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 bulk_commit();
             }
         };
-        for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
+        // ---- two-group GDN / IGDN epilogue (p.g2, BN = 128): group gr = (warp - 4) / 8
+        // takes this CTA's tiles it = gr, gr + 2, ... (accumulator buffer gr); warp (q, h) of the group
+        // owns pixels 32q .. 32q + 31 (TMEM lanes) x channels 64h .. 64h + 63.  P1: x = acc + b, the
+        // norm operand v = x^2 2^-2k (|x| 2^-k for 1DN; k per pixel, v_max in [2^13, 2^15)) as fp16
+        // hi / lo written over the accumulator, the signs of x kept as bits; the MMA warp issues the
+        // norm MMAs; P2: y from v and the norm alone -- x = sign sqrt(v) 2^k, so
+        // y = x / sqrt(n) = sign v rsqrt(v n) 2^k (GDN), sign (v n) rsqrt(v n) 2^k (IGDN), one MUFU
+        // op per value, and no register holds x across the norm round trip, during which the other
+        // group works.
+        if constexpr (GC == 2) if (g2) {
+            const int gr = (warp - 4) >> 3;
+            const int h = ((warp - 4) >> 2) & 1;
+            const int lead = 128 + gr * 256;                          // the group's first thread
+            const uint32_t bar_full = 2u + (uint32_t)gr, bar_norm = 13u + (uint32_t)gr;
+            const uint32_t bar_px = 5u + (uint32_t)(gr * 4 + q);      // the pixel's two channel halves
+            const float s255 = p.l1_int ? (1.0f / 255.0f) : 1.0f;
+            const uint32_t xe_a = s_xe + (uint32_t)(gr * 512) + 4u * (uint32_t)r;
+            const uint32_t rowa = smem_u32(smem) + p.off_ostage + (uint32_t)(warp - 4) * 4096u + (uint32_t)lane * 64u;
+            const uint32_t sw = ((uint32_t)lane >> 1) & 3u;           // 64B swizzle of this row
+            const int ty0 = (q * 32) >> p.wt_log2, tx0 = (q * 32) & (p.Wt - 1);
+            const uint32_t tcol0 = tmem_base + lane_off + (uint32_t)(gr * p.acc_stride) + (uint32_t)(h * 64);
+            const int c0 = h * 64;                                     // first channel of this thread (one N tile)
+            // |bias| bound of this thread's channels: max |x| <= max |acc| s255 + bmax (the exponent
+            // below is taken from this bound, so the accumulator is read once before the exchange)
+            float bmax = 0.0f;
+            for (int i = 0; i < 64; ++i) bmax = fmaxf(bmax, fabsf(s_bias[c0 + i]));
+            auto body = [&](auto onedn_c, auto fwd_c) {
+                constexpr bool kOneDN = decltype(onedn_c)::value, kFwd = decltype(fwd_c)::value;
+                int it = gr;
+                for (int t = cid + gr * ncl; t < p.total_tiles; t += 2 * ncl, it += 2) {
+                    const TileCoord tc = decode_tile(p, t, rank);
+                    const uint32_t par = (uint32_t)(it >> 1) & 1u;
+                    if (threadIdx.x == lead) mbar_wait(&tfull_bar[gr], par);
+                    named_bar_sync(bar_full, 256);
+                    tc_fence_after();
+                    if (threadIdx.x == lead) LIC_TRACE(it, T_EPI_START);
+                    // ---- P1.  Pass A: a bound on max |x| of the pixel (both channel halves);
+                    // pass B, 32 channels at a time: x = acc s255 + b, v, signs, v -> TMEM.
+                    uint32_t xr[32];
+                    float amax = 0.0f;
+#pragma unroll 1
+                    for (int s = 0; s < 2; ++s) {
+                        tmem_ld32_nw(tcol0 + 32 * s, xr);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(__uint_as_float(xr[i])));
+                    }
+                    const float xb = fmaf(amax, s255, bmax);
+                    stsb(xe_a + (uint32_t)h, __float_as_uint(xb) >> 23);        // biased exponent of the bound
+                    named_bar_sync(bar_px, 64);
+                    const uint32_t ew = ldsu(xe_a);
+                    const int E = (int)max(ew & 0xffu, (ew >> 8) & 0xffu) - 127;   // max |x| < 2^(E+1)
+                    // GDN: v = x^2 2^-2k, k = E - 6 -> v < 2^14; 1DN: v = |x| 2^-k, k = E - 13 -> v < 2^14
+                    const int k = kOneDN ? min(max(E - 13, -100), 100) : min(max(E - 6, -50), 50);
+                    const float sc_dn = __int_as_float((127 - k) << 23);          // 2^-k
+                    uint32_t sg0 = 0u, sg1 = 0u;                             // sign bits (bit 31 = channel 32s)
+#pragma unroll 1
+                    for (int s = 0; s < 2; ++s) {
+                        tmem_ld32_nw(tcol0 + 32 * s, xr);
+                        tmem_ld_wait();
+                        uint32_t hv[16], lv[16];
+                        uint32_t sgs = 0u;
+#pragma unroll
+                        for (int i4 = 0; i4 < 8; ++i4) {
+                            const float4 bb = lds4(s_bias + c0 + 32 * s + 4 * i4);
+                            const float bq[4] = {bb.x, bb.y, bb.z, bb.w};
+                            float v[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const float xv = fmaf(__uint_as_float(xr[4 * i4 + u]), s255, bq[u]);
+                                sgs = __funnelshift_l(__float_as_uint(xv), sgs, 1);   // (sgs << 1) | sign
+                                const float xs = xv * sc_dn;                  // x 2^-k (GDN), |x| 2^-k (1DN)
+                                v[u] = kOneDN ? fabsf(xs) : xs * xs;
+                            }
+                            split2(v[0], v[1], hv[2 * i4], lv[2 * i4]);
+                            split2(v[2], v[3], hv[2 * i4 + 1], lv[2 * i4 + 1]);
+                        }
+                        if (s) sg1 = sgs; else sg0 = sgs;
+                        // the G = 32 layout of the norm MMA: hi of channel 32s + j at column 32s + j/2, lo at 32s + 16 + j/2
+                        const uint32_t ts = tcol0 + 32u * (uint32_t)s;
+                        tmem_st8(ts, hv);
+                        tmem_st8(ts + 8, hv + 8);
+                        tmem_st8(ts + 16, lv);
+                        tmem_st8(ts + 24, lv + 8);
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (CG == 2) mbar_arrive_cluster(lbar(&xsq2_bar[gr]));
+                        else mbar_arrive(&xsq2_bar[gr]);
+                    }
+                    if (threadIdx.x == lead) LIC_TRACE(it, T_EPI_XSQ);
+                    // ---- wait for the norm MMAs of this tile
+                    if (threadIdx.x == lead) mbar_wait(&norm2_bar[gr], par);
+                    named_bar_sync(bar_norm, 256);
+                    tc_fence_after();
+                    if (threadIdx.x == lead) LIC_TRACE(it, T_EPI_NORM);
+                    // n = beta + c 2^(2k) (GDN) / beta + c 2^k (1DN), c the contraction of v
+                    const float sc_up = kOneDN ? __int_as_float((127 + k) << 23) : __int_as_float((127 + 2 * k) << 23);
+                    const float sc_k = __int_as_float((127 + k) << 23);       // |x| = sqrt(v) 2^k (GDN), v 2^k (1DN)
+                    // ---- P2: 4 pieces of 16 channels; pieces 2s, 2s + 1 form staging round s (32 channels)
+#pragma unroll 1
+                    for (int pc = 0; pc < 4; ++pc) {
+                        const int j = pc & 1;
+                        if (j == 0) {
+                            if (lane == 0) bulk_wait_read0();              // this warp's slot is free again
+                            __syncwarp();
+                        }
+                        uint32_t vh[8], vl[8], nr[16];
+                        const uint32_t ts = tcol0 + 32u * (uint32_t)(pc >> 1) + 8u * (uint32_t)j;
+                        tmem_ld8_nw(ts, vh);
+                        tmem_ld8_nw(ts + 16, vl);
+                        tmem_ld16_nw(tcol0 + (uint32_t)p.BN + 16u * (uint32_t)pc, nr);
+                        tmem_ld_wait();
+                        if (pc == 3) {
+                            // every TMEM read of this tile is complete: release the buffer
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) {
+                                if constexpr (CG == 2) mbar_arrive_cluster(lbar(&tempty_bar[gr]));
+                                else mbar_arrive(&tempty_bar[gr]);
+                            }
+                        }
+                        const uint32_t sgp = ((pc >> 1) ? sg1 : sg0) << (16 * j);          // bit 31 = this piece's channel 0
+                        float y[16];
+#pragma unroll
+                        for (int i4 = 0; i4 < 4; ++i4) {
+                            const float4 be = lds4(s_beta + c0 + 16 * pc + 4 * i4);
+                            const float bv[4] = {be.x, be.y, be.z, be.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int i = 4 * i4 + u;
+                                const float v = (i & 1) ? join_h<1>(vh[i >> 1], vl[i >> 1]) : join_h<0>(vh[i >> 1], vl[i >> 1]);
+                                const float nn = fmaf(__uint_as_float(nr[i]), sc_up, bv[u]);
+                                float m;
+                                if constexpr (kOneDN) {
+                                    m = kFwd ? (v * sc_k) * rcp_ftz(nn) : (v * sc_k) * nn;    // |x| / n, |x| n
+                                } else {
+                                    const float tv = fmaf(v, nn, 1e-30f);                    // v = 0: y = 0
+                                    const float rs = rsqrt_ftz(tv);
+                                    m = (kFwd ? v * rs : tv * rs) * sc_k;     // |x| / sqrt(n), |x| sqrt(n)
+                                }
+                                y[i] = __uint_as_float(__float_as_uint(m) ^ ((sgp << i) & 0x80000000u));
+                            }
+                        }
+                        if (p.out_f32) {
+                            const int gy = tc.gy0 + (r >> p.wt_log2), gx = tc.gx0 + (r & (p.Wt - 1));
+                            if (gy < p.Hg && gx < p.Wg) {
+                                const size_t HWo = (size_t)p.Hout * p.Wout;
+                                const size_t chw0 = (size_t)tc.b * p.Cout * HWo + (size_t)gy * p.Wout + gx;
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(c0 + 16 * pc + i) * HWo] = y[i];
+                            }
+                        }
+                        guard16(y, ovf);
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk) {
+                            uint4 hq, lq;
+                            const float* v8 = y + 8 * kk;
+                            split2(v8[0], v8[1], hq.x, lq.x); split2(v8[2], v8[3], hq.y, lq.y);
+                            split2(v8[4], v8[5], hq.z, lq.z); split2(v8[6], v8[7], hq.w, lq.w);
+                            const uint32_t o = ((((uint32_t)(2 * j + kk)) ^ sw) & 3u) << 4;
+                            stsu4(rowa + o, hq);
+                            stsu4(rowa + 2048u + o, lq);
+                        }
+                        if (j == 1) {
+                            fence_proxy_async_smem();
+                            __syncwarp();
+                            if (lane == 0) {
+                                if (threadIdx.x == lead) LIC_TRACE(it, pc == 3 ? T_EPI_ACQ : T_EPI_P2);
+                                tma_store_5d(&mapOH, smem + p.off_ostage + (uint32_t)(warp - 4) * 4096u,
+                                             tc.nt * p.BN + c0 + 32 * (pc >> 1), tc.gx0 + tx0, tc.gy0 + ty0, tc.b, 0);
+                                bulk_commit();
+                                if (threadIdx.x == lead) LIC_TRACE(it, pc == 3 ? T_EPI_END : T_EPI_STAGED);
+                            }
+                        }
+                    }
+                }
+            };
+            using T_ = std::integral_constant<bool, true>;
+            using F_ = std::integral_constant<bool, false>;
+            if (p.onedn) { if (p.ep == EP_GDN) body(T_{}, T_{}); else body(T_{}, F_{}); }
+            else { if (p.ep == EP_GDN) body(F_{}, T_{}); else body(F_{}, F_{}); }
+        }
+        for (int t = g2 ? p.total_tiles : cid; t < p.total_tiles; t += ncl, ++it) {
             TileCoord tc = decode_tile(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
             const uint32_t use = (p.n_accbuf == 2) ? (uint32_t)(it >> 1) : (uint32_t)it;

@@ -106,7 +106,8 @@ struct ConvParams {
                                       // builders convert u8 -> f16 arithmetically (no LUT)
     uint32_t off_patch;               // split patch [2][hi, lo][19][112] fp16
     uint32_t off_lut;                 // u8 LUT [257] (hi | lo << 16; entry 256 = 0)
-    uint32_t off_raw;                 // raw u8 patch [2][19][112] (cp.async, u8 frames)
+    uint32_t off_raw;                 // raw u8 patch [2][19][112] in 2176-byte slots (cp.async or TMA, u8 frames)
+    int raw_tma;                      // the raw patch by one TMA box per tile (mapA = the u8 frame, 3W x H x B)
     // TMA-store epilogue: each epilogue warp stages 32 px x 16 ch (hi, lo: 1 KB each) in smem and
     // writes it with a bulk tensor store; out maps: conv (C, W, H, B), deconv phase view
     // (C, px, W/2, py, B*H/2) of the NHWC output, one map per plane
@@ -116,6 +117,10 @@ struct ConvParams {
     // rounds of wst_ch channels (32: 4 KB slots, 64-byte rows; 16: 2 KB) in wst_slots private
     // slots and stores them itself (out maps with a wst_ch-channel box); 0: quadrant blocks
     int wst_ch, wst_slots;
+    // two-group GDN / IGDN epilogue (BN = 128, per-warp 32-channel staging, double-buffered TMEM):
+    // two groups of 8 epilogue warps alternate tiles so one group's norm MMA round trip overlaps
+    // the other's arithmetic; y is computed from the norm operand and the signs (conv_umma.cu)
+    int g2;
     // gather mode (g_s L4, stride-2 transposed conv N -> 3): the 9 input offsets go into N instead
     // of K -- P[p][t][j] = A[p] . W_t[j] over a 16 x 8 input tile (one A read per pixel, N = 9 x 16),
     // then out[g][j] = sum_t P[g + off_t][t][j] gathered through shared memory for the 14 x 6

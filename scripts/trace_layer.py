@@ -36,7 +36,7 @@ c.trace(layer, True)
 step()
 t = c.trace_read().astype(np.int64)
 names = ["mma_s", "mma_e", "norm_i", "epi_s", "epi_x2", "epi_n", "epi_e", "prod_s"]
-bnames = ["b_patch", "b_c0_rdy", "b_c0_done", "b_c1_rdy", "b_c1_done", "mma_k0", "mma_kl", "peerB", "b_raw", "epi_p2", "epi_acq", "epi_stg", "w_halo", "w_b"]
+bnames = ["b_patch", "b_c0_rdy", "b_c0_done", "b_c1_rdy", "b_c1_done", "mma_k0", "mma_kl", "peerB", "b_raw", "epi_p2", "epi_acq", "epi_stg", "w_halo", "w_b", "b_rawiss"]
 n = int((t[:, 0] > 0).sum())
 t0 = t[0, 0]
 fused = True
