@@ -177,7 +177,7 @@ struct lic_codec {
     int a_hi_only_enabled = 1;     // g_s L1 skips the zero lo plane of the integer y-hat (env LIC_YHAT_HI=0: off)
     int raw_tma_enabled = 1;       // u8 frames: raw patches by TMA (env LIC_RAW_TMA=0: cp.async)
     int l1_stage_split = 1;        // u8 frames: hi-only A stages, twice as many (env LIC_L1_STAGES=0: off)
-    int g2_enabled = 1;            // two-group GDN epilogue for g_a L1 (env LIC_G2=0: off)
+    int g2_enabled = 1;            // two-group GDN epilogue: 1 g_a L1, 2 every BN = 128 GDN layer (env LIC_G2)
     int l1_int_enabled = 1;        // u8 frames: integer samples into g_a L1, one MMA pass (env LIC_L1_INT=0: off)
     int l1_conv_enabled = 1;       // ... converted arithmetically, 8 per item, no LUT (env LIC_L1_CONV=0: LUT)
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
@@ -656,7 +656,8 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     // two-group GDN epilogue (env LIC_G2=0: off): the fused g_a L1, whose tiles are short (K = 80)
     // and whose time is the GDN epilogue's
     P.g2 = 0;
-    if (gdn && P.BN == 128 && P.wst_ch == 32 && P.wst_slots == 1 && P.n_accbuf == 2 && gemm_l1 && c->g2_enabled)
+    if (gdn && P.BN == 128 && P.wst_ch == 32 && P.wst_slots == 1 && P.n_accbuf == 2 && P.tma_out &&
+        (gemm_l1 ? c->g2_enabled >= 1 : c->g2_enabled >= 2))
         P.g2 = 1;
     P.L = c->L;
     // tensor maps
@@ -954,7 +955,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_PDL")) c->pdl_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_GS4_GATHER")) c->gs4_gather = (e[0] != '0');
     if (const char* e = std::getenv("LIC_L1_INT")) c->l1_int_enabled = (e[0] != '0');
-    if (const char* e = std::getenv("LIC_G2")) c->g2_enabled = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_G2")) c->g2_enabled = atoi(e);      // 0 off, 1 g_a L1, 2 every BN = 128 GDN layer
     if (const char* e = std::getenv("LIC_L1_STAGES")) c->l1_stage_split = (e[0] != '0');
     if (const char* e = std::getenv("LIC_RAW_TMA")) c->raw_tma_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');

@@ -988,6 +988,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 for (int t = cid + gr * ncl; t < p.total_tiles; t += 2 * ncl, it += 2) {
                     const TileCoord tc = decode_tile(p, t, rank);
                     const uint32_t par = (uint32_t)(it >> 1) & 1u;
+                    const bool tma_ok = p.nphase == 1 || tc.gy0 + ty0 + 32 / (p.Wt < 32 ? p.Wt : 32) <= p.Hg;
                     if (threadIdx.x == lead) mbar_wait(&tfull_bar[gr], par);
                     named_bar_sync(bar_full, 256);
                     tc_fence_after();
@@ -1102,16 +1103,30 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                                 y[i] = __uint_as_float(__float_as_uint(m) ^ ((sgp << i) & 0x80000000u));
                             }
                         }
-                        if (p.out_f32) {
-                            const int gy = tc.gy0 + (r >> p.wt_log2), gx = tc.gx0 + (r & (p.Wt - 1));
-                            if (gy < p.Hg && gx < p.Wg) {
-                                const size_t HWo = (size_t)p.Hout * p.Wout;
-                                const size_t chw0 = (size_t)tc.b * p.Cout * HWo + (size_t)gy * p.Wout + gx;
+                        // output pixel (conv: the grid pixel; transposed conv: its sub-pixel phase)
+                        const int gy = tc.gy0 + (r >> p.wt_log2), gx = tc.gx0 + (r & (p.Wt - 1));
+                        const bool valid = gy < p.Hg && gx < p.Wg;
+                        const int oy = p.out_s * gy + (p.nphase == 4 ? (tc.ph >> 1) : 0);
+                        const int ox = p.out_s * gx + (p.nphase == 4 ? (tc.ph & 1) : 0);
+                        if (p.out_f32 && valid) {
+                            const size_t HWo = (size_t)p.Hout * p.Wout;
+                            const size_t chw0 = (size_t)tc.b * p.Cout * HWo + (size_t)oy * p.Wout + ox;
 #pragma unroll
-                                for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(c0 + 16 * pc + i) * HWo] = y[i];
-                            }
+                            for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(tc.nt * p.BN + c0 + 16 * pc + i) * HWo] = y[i];
                         }
                         guard16(y, ovf);
+                        if (!tma_ok) {
+                            // a transposed conv's tile crossing the grid's bottom edge: the phase view
+                            // would run into the next frame -- direct 16-byte stores
+                            if (valid) {
+                                __half* out = reinterpret_cast<__half*>(p.out_act);
+                                const size_t pix = ((size_t)tc.b * p.Hout + oy) * p.Wout + ox;
+                                const int cb = tc.nt * p.BN + c0 + 16 * pc;
+                                split_store8(out + pix * p.Cout + cb, out + p.act_plane + pix * p.Cout + cb, y);
+                                split_store8(out + pix * p.Cout + cb + 8, out + p.act_plane + pix * p.Cout + cb + 8, y + 8);
+                            }
+                            continue;
+                        }
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk) {
                             uint4 hq, lq;
@@ -1127,8 +1142,15 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             __syncwarp();
                             if (lane == 0) {
                                 if (threadIdx.x == lead) LIC_TRACE(it, pc == 3 ? T_EPI_ACQ : T_EPI_P2);
-                                tma_store_5d(&mapOH, smem + p.off_ostage + (uint32_t)(warp - 4) * 4096u,
-                                             tc.nt * p.BN + c0 + 32 * (pc >> 1), tc.gx0 + tx0, tc.gy0 + ty0, tc.b, 0);
+                                const uint8_t* hs = smem + p.off_ostage + (uint32_t)(warp - 4) * 4096u;
+                                const int cb = tc.nt * p.BN + c0 + 32 * (pc >> 1);
+                                if (p.nphase == 1) {
+                                    tma_store_5d(&mapOH, hs, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b, 0);
+                                } else {
+                                    const int ph = tc.ph;
+                                    const CUtensorMap* om = ph == 0 ? &mapOH : ph == 1 ? &mapOL : ph == 2 ? &mapO2 : &mapO3;
+                                    tma_store_4d(om, hs, cb, tc.gx0 + tx0, tc.b * p.Hg + tc.gy0 + ty0, 0);
+                                }
                                 bulk_commit();
                                 if (threadIdx.x == lead) LIC_TRACE(it, pc == 3 ? T_EPI_END : T_EPI_STAGED);
                             }
