@@ -596,6 +596,8 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.off_gamma = stages * P.stage_bytes;
     }
     if (P.sub4 && !P.halo) return fail(c, LIC_EINVAL, "parity-halo conv does not fit shared memory");
+    for (int i = 0; i < kMaxTaps; ++i)
+        P.tapoff[i] = P.halo ? (uint32_t)(((P.tap_dy[i] + 1) * P.halo_w + P.tap_dx[i] + 1) * 8) : 0u;
     if (!P.tsx) { P.tsx = P.Wt; P.tsy = P.Ht; }
     P.tiles_x = (P.Wg + P.tsx - 1) / P.tsx;
     P.tiles_y = (P.Hg + P.tsy - 1) / P.tsy;

@@ -791,7 +791,64 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (lane == 0) LIC_TRACE(it, T_MMA_START);
             const uint32_t d = tmem_base + (uint32_t)(buf * p.acc_stride);
             long long w_halo = 0, w_b = 0;          // trace only: cycles waiting for operands
-            if (p.halo) {
+            // halo mode, streamed weights, 2 or 3 taps per stage, no trace: the lean issue loop --
+            // tap window offsets from the kernel parameters (uniform registers), the stage count
+            // compile-time, no per-stage parameter tests
+            auto halo_fast = [&](auto tps_c, auto lo_c) {
+                constexpr int TPS = decltype(tps_c)::value;
+                constexpr bool LO = decltype(lo_c)::value;
+                const uint32_t sbo = (uint32_t)p.halo_w * 128;
+                const uint32_t hstride = (uint32_t)p.split * p.halo_plane_bytes;
+                const uint64_t lo16 = p.halo_plane_bytes >> 4;
+                const uint64_t bstep16 = b_bytes >> 4;
+                const uint32_t halo0 = smem_u32(smem + p.off_halo), stage0 = smem_u32(smem);
+                const int ngr = p.sub4 ? 4 : 1;
+                for (int c = 0; c < p.kchunks; ++c)
+                    for (int gi = 0; gi < ngr; ++gi) {
+                        const int nt = p.sub4 ? p.ntaps[gi] : p.ntaps[tc.ph], t0 = p.sub4 ? p.tap0[gi] : p.tap0[tc.ph];
+                        wait_poll(&hfull_bar[hs], hphase);
+                        tc_fence_after();
+                        const uint64_t ahb = sdesc_sw128_sbo(halo0 + (uint32_t)hs * hstride, sbo);
+                        for (int ti = 0; ti < nt; ti += TPS) {
+                            const int ntp = min(TPS, nt - ti);
+                            wait_poll(&full_bar[stage], phase);
+                            tc_fence_after();
+                            const uint64_t bdb = sdesc_sw128(stage0 + (uint32_t)stage * p.stage_bytes);
+                            if (elect_one()) {
+                                const uint32_t acc0 = (c | gi | ti) != 0;
+#pragma unroll
+                                for (int u = 0; u < TPS; ++u) {
+                                    if (u < ntp) {
+                                        const uint64_t ah = ahb + p.tapoff[t0 + ti + u];
+                                        const uint64_t bd = bdb + (uint64_t)u * bstep16;
+#pragma unroll
+                                        for (int kk = 0; kk < kBK / 16; ++kk) {
+                                            mma_ss(d, ah + 2 * kk, bd + 2 * kk, (u | kk) ? 1u : acc0);
+                                            if constexpr (LO) mma_ss(d, ah + lo16 + 2 * kk, bd + 2 * kk, 1u);
+                                        }
+                                    }
+                                }
+                                commit(&empty_bar[stage]);
+                            }
+                            __syncwarp();
+                            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                            poll_norm();
+                        }
+                        if (elect_one()) commit(&hempty_bar[hs]);
+                        __syncwarp();
+                        if (++hs == p.halo_slots) { hs = 0; hphase ^= 1; }
+                    }
+            };
+            const bool fast_halo = p.halo && !p.wres && !p.trace && (p.tps == 2 || p.tps == 3);
+            if (fast_halo) {
+                using I2 = std::integral_constant<int, 2>;
+                using I3 = std::integral_constant<int, 3>;
+                using BT = std::integral_constant<bool, true>;
+                using BF = std::integral_constant<bool, false>;
+                const bool lo_mma = p.split == 2 && !p.a_hi_only;
+                if (p.tps == 2) { if (lo_mma) halo_fast(I2{}, BT{}); else halo_fast(I2{}, BF{}); }
+                else { if (lo_mma) halo_fast(I3{}, BT{}); else halo_fast(I3{}, BF{}); }
+            } else if (p.halo) {
                 const uint32_t sbo = (uint32_t)p.halo_w * 128;
                 const bool lo_mma = p.split == 2 && !p.a_hi_only;
                 for (int c = 0; c < p.kchunks; ++c)

@@ -41,6 +41,8 @@ struct ConvParams {
     int out_s;                        // output pixel = out_s * g + phase offset
     int ntaps[4], tap0[4];
     int tap_dy[kMaxTaps], tap_dx[kMaxTaps], tap_w[kMaxTaps];
+    uint32_t tapoff[kMaxTaps];        // halo mode: tap t's window start in the halo, 16-byte descriptor units
+                                      // ((dy + 1) * halo_w + dx + 1) * 8 -- host-computed (uniform operands)
     int split;                        // 2: activations are fp16 hi + lo planes; 1: hi only
     int cg;                           // 1: one CTA per tile; 2: CTA pair (cta_group::2, M = 256)
     int total_tiles;
