@@ -1690,20 +1690,24 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     case EP_SIGMA: {
                         if (!valid) break;
                         uint8_t* idx = reinterpret_cast<uint8_t*>(p.out_sym);
+                        const uint32_t tab = smem_u32(s_tab);
+                        if (p.out_f32) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = fmaxf(v[j], 0.0f);
+                        }
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            if (j >= nj) continue;
-                            float s = fmaxf(v[j], 0.0f);
-                            if (p.out_f32) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = s;
-                            s = fmaxf(s, 0.11f);
-                            // #{ j in [0, 62] : table_j < s }: binary search over the sorted table
-                            int lo_i = 0, hi_i = 63;
+                            // sigma' = max(relu(x), 0.11); index = #{j in [0, 62] : table_j < sigma'} by a
+                            // branch-free lower bound over the sorted table (steps 32 .. 1; the probed
+                            // position never passes 62) -- compact code: these layers run 1-2 tiles per
+                            // CTA, so their epilogue executes from a cold instruction cache
+                            const float s = fmaxf(fmaxf(v[j], 0.0f), 0.11f);
+                            int lo = 0;
 #pragma unroll
-                            for (int step = 0; step < 6; ++step) {
-                                const int mid = (lo_i + hi_i) >> 1;
-                                if (s_tab[mid] < s) lo_i = mid + 1; else hi_i = mid;
-                            }
-                            idx[chw0 + (size_t)(cb + j) * HWo] = (uint8_t)lo_i;
+                            for (int step = 32; step > 0; step >>= 1)
+                                lo = (ldsf(tab + 4u * (uint32_t)(lo + step - 1)) < s) ? lo + step : lo;
+                            if (j < nj) idx[chw0 + (size_t)(cb + j) * HWo] = (uint8_t)lo;
                         }
                         break;
                     }
