@@ -746,18 +746,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         int xsq_seen = 0;              // tiles whose x^2 the MMA warp has consumed
         // two-group epilogue: tiles whose main MMAs are committed / whose norm MMAs are issued
         // (in tile order; tile n uses accumulator buffer n & 1, the (n >> 1)-th phase of its barriers)
-        int g2_committed = 0, g2_nn = 0;
+        int g2_committed = 0;
+        (void)g2_committed;
         auto poll_norm = [&]() {       // cheap volatile smem read; the mbarrier wait then completes at once
             if constexpr (GC == 2) {
-                if (g2) {
-                    while (g2_nn < g2_committed && mbar_test(&xsq2_bar[g2_nn & 1], (uint32_t)(g2_nn >> 1) & 1u)) {
-                        pend_dcol = (uint32_t)((g2_nn & 1) * p.acc_stride);
-                        pend_it = g2_nn;
-                        issue_norm(&norm2_bar[g2_nn & 1]);
-                        ++g2_nn;
-                    }
-                    return;
-                }
+                if (g2) return;                              // the epilogue issues its own norm MMAs
             }
             if (kGdn && pend && *reinterpret_cast<volatile uint32_t*>(xsq_cnt) >= (uint32_t)(kEpiWarps * CG * (xsq_seen + 1))) {
                 mbar_wait(xsq_bar, xsq_phase);
@@ -770,6 +763,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         // norm of tile i is not held back while the warp waits for tile i+1's operands
         auto wait_poll = [&](uint64_t* bar, uint32_t par) {
             if constexpr (kGdn) {
+                if (g2) { mbar_wait(bar, par); return; }      // norms are issued by the epilogue (g2)
                 if (mbar_test(bar, par)) return;
                 const long long t0 = clock64();
                 while (!mbar_test(bar, par)) {
@@ -959,22 +953,12 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 
             if (g2) {
                 g2_committed = it + 1;
-                poll_norm();
             } else if (kGdn) {
                 // the previous tile's norm must be issued before this one becomes pending
                 if (pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
                 pend = 1;
                 pend_it = it;
                 pend_dcol = (uint32_t)(buf * p.acc_stride);
-            }
-        }
-        if (g2 && leader) {
-            while (g2_nn < g2_committed) {
-                mbar_wait(&xsq2_bar[g2_nn & 1], (uint32_t)(g2_nn >> 1) & 1u);
-                pend_dcol = (uint32_t)((g2_nn & 1) * p.acc_stride);
-                pend_it = g2_nn;
-                issue_norm(&norm2_bar[g2_nn & 1]);
-                ++g2_nn;
             }
         }
         if (kGdn && !g2 && pend && leader) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
@@ -1035,6 +1019,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const int ty0 = (q * 32) >> p.wt_log2, tx0 = (q * 32) & (p.Wt - 1);
             const uint32_t tcol0 = tmem_base + lane_off + (uint32_t)(gr * p.acc_stride) + (uint32_t)(h * 64);
             const int c0 = h * 64;                                     // first channel of this thread (one N tile)
+            bool gamma_ok = false;                                     // (the norm-issuing thread) gamma landed
             // |bias| bound of this thread's channels: max |x| <= max |acc| s255 + bmax (the exponent
             // below is taken from this bound, so the accumulator is read once before the exchange)
             float bmax = 0.0f;
@@ -1046,6 +1031,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     const TileCoord tc = decode_tile(p, t, rank);
                     const uint32_t par = (uint32_t)(it >> 1) & 1u;
                     const bool tma_ok = p.nphase == 1 || tc.gy0 + ty0 + 32 / (p.Wt < 32 ? p.Wt : 32) <= p.Hg;
+                    const bool slow = !tma_ok || p.out_f32 != nullptr;
                     if (threadIdx.x == lead) mbar_wait(&tfull_bar[gr], par);
                     named_bar_sync(bar_full, 256);
                     tc_fence_after();
@@ -1107,6 +1093,31 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         else mbar_arrive(&xsq2_bar[gr]);
                     }
                     if (threadIdx.x == lead) LIC_TRACE(it, T_EPI_XSQ);
+                    if (leader && threadIdx.x == lead) {
+                        // every warp of the group (both CTAs) has written v: issue norm = v . gamma^T
+                        // from here (a blocking wait: the MMA warp keeps issuing main loops meanwhile)
+                        if (!gamma_ok) { mbar_wait(gamma_bar, 0); gamma_ok = true; }
+                        mbar_wait(&xsq2_bar[gr], par);
+                        tc_fence_after();
+                        const uint32_t dcol = (uint32_t)(gr * p.acc_stride);
+                        const uint32_t ncol = tmem_base + dcol + (uint32_t)p.BN;
+                        const uint32_t gbase = smem_u32(smem + p.off_gamma);
+                        const uint32_t idesc_n = idesc_f16_f32(kBM * CG, (uint32_t)p.BN);
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {          // K = BN = 128 in steps of 16 (G = 32 layout)
+                            const int k0 = 16 * kk, gg = k0 / 32, o = k0 - gg * 32;
+                            const uint32_t ahi = tmem_base + dcol + gg * 32 + o / 2;
+                            const uint64_t bd = sdesc_sw128(gbase + (k0 / 64) * (uint32_t)((p.BN / CG) * kBK * 2)) + 2 * (kk & 3);
+                            if constexpr (CG == 2) {
+                                umma_f16_ts_cg2(ncol, ahi, bd, idesc_n, kk != 0);
+                                umma_f16_ts_cg2(ncol, ahi + 16, bd, idesc_n, 1u);
+                            } else {
+                                umma_f16_ts(ncol, ahi, bd, idesc_n, kk != 0);
+                                umma_f16_ts(ncol, ahi + 16, bd, idesc_n, 1u);
+                            }
+                        }
+                        if constexpr (CG == 2) umma_commit_pair(&norm2_bar[gr]); else umma_commit(&norm2_bar[gr]);
+                    }
                     // ---- wait for the norm MMAs of this tile
                     if (threadIdx.x == lead) mbar_wait(&norm2_bar[gr], par);
                     named_bar_sync(bar_norm, 256);
@@ -1160,30 +1171,32 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                                 y[i] = __uint_as_float(__float_as_uint(m) ^ ((sgp << i) & 0x80000000u));
                             }
                         }
-                        // output pixel (conv: the grid pixel; transposed conv: its sub-pixel phase)
-                        const int gy = tc.gy0 + (r >> p.wt_log2), gx = tc.gx0 + (r & (p.Wt - 1));
-                        const bool valid = gy < p.Hg && gx < p.Wg;
-                        const int oy = p.out_s * gy + (p.nphase == 4 ? (tc.ph >> 1) : 0);
-                        const int ox = p.out_s * gx + (p.nphase == 4 ? (tc.ph & 1) : 0);
-                        if (p.out_f32 && valid) {
-                            const size_t HWo = (size_t)p.Hout * p.Wout;
-                            const size_t chw0 = (size_t)tc.b * p.Cout * HWo + (size_t)oy * p.Wout + ox;
+                        if (slow) {
+                            // test-only f32 copy, and a transposed conv's tile crossing the grid's bottom
+                            // edge (the phase view would run into the next frame): direct stores
+                            const int gy = tc.gy0 + (r >> p.wt_log2), gx = tc.gx0 + (r & (p.Wt - 1));
+                            const bool valid = gy < p.Hg && gx < p.Wg;
+                            const int oy = p.out_s * gy + (p.nphase == 4 ? (tc.ph >> 1) : 0);
+                            const int ox = p.out_s * gx + (p.nphase == 4 ? (tc.ph & 1) : 0);
+                            const int cb = tc.nt * p.BN + c0 + 16 * pc;
+                            if (p.out_f32 && valid) {
+                                const size_t HWo = (size_t)p.Hout * p.Wout;
+                                const size_t chw0 = (size_t)tc.b * p.Cout * HWo + (size_t)oy * p.Wout + ox;
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(tc.nt * p.BN + c0 + 16 * pc + i) * HWo] = y[i];
+                                for (int i = 0; i < 16; ++i) p.out_f32[chw0 + (size_t)(cb + i) * HWo] = y[i];
+                            }
+                            if (!tma_ok) {
+                                guard16(y, ovf);
+                                if (valid) {
+                                    __half* out = reinterpret_cast<__half*>(p.out_act);
+                                    const size_t pix = ((size_t)tc.b * p.Hout + oy) * p.Wout + ox;
+                                    split_store8(out + pix * p.Cout + cb, out + p.act_plane + pix * p.Cout + cb, y);
+                                    split_store8(out + pix * p.Cout + cb + 8, out + p.act_plane + pix * p.Cout + cb + 8, y + 8);
+                                }
+                                continue;
+                            }
                         }
                         guard16(y, ovf);
-                        if (!tma_ok) {
-                            // a transposed conv's tile crossing the grid's bottom edge: the phase view
-                            // would run into the next frame -- direct 16-byte stores
-                            if (valid) {
-                                __half* out = reinterpret_cast<__half*>(p.out_act);
-                                const size_t pix = ((size_t)tc.b * p.Hout + oy) * p.Wout + ox;
-                                const int cb = tc.nt * p.BN + c0 + 16 * pc;
-                                split_store8(out + pix * p.Cout + cb, out + p.act_plane + pix * p.Cout + cb, y);
-                                split_store8(out + pix * p.Cout + cb + 8, out + p.act_plane + pix * p.Cout + cb + 8, y + 8);
-                            }
-                            continue;
-                        }
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk) {
                             uint4 hq, lq;
