@@ -177,7 +177,7 @@ struct lic_codec {
     int a_hi_only_enabled = 1;     // g_s L1 skips the zero lo plane of the integer y-hat (env LIC_YHAT_HI=0: off)
     int raw_tma_enabled = 1;       // u8 frames: raw patches by TMA (env LIC_RAW_TMA=0: cp.async)
     int l1_stage_split = 1;        // u8 frames: hi-only A stages, twice as many (env LIC_L1_STAGES=0: off)
-    int g2_enabled = 1;            // two-group GDN epilogue: 1 g_a L1, 2 every BN = 128 GDN layer (env LIC_G2)
+    int g2_enabled = 2;            // two-group GDN epilogue: 1 g_a L1 only, 2 every BN = 128 GDN layer (env LIC_G2)
     int l1_int_enabled = 1;        // u8 frames: integer samples into g_a L1, one MMA pass (env LIC_L1_INT=0: off)
     int l1_conv_enabled = 1;       // ... converted arithmetically, 8 per item, no LUT (env LIC_L1_CONV=0: LUT)
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
