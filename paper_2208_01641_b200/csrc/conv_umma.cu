@@ -763,11 +763,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         // norm of tile i is not held back while the warp waits for tile i+1's operands
         auto wait_poll = [&](uint64_t* bar, uint32_t par) {
             if constexpr (kGdn) {
-                if (g2) { mbar_wait(bar, par); return; }      // norms are issued by the epilogue (g2)
+                if (g2 && !p.mma_spin) { mbar_wait(bar, par); return; }   // norms issued by the epilogue (g2)
                 if (mbar_test(bar, par)) return;
                 const long long t0 = clock64();
                 while (!mbar_test(bar, par)) {
-                    poll_norm();
+                    if (!g2) poll_norm();
                     if (clock64() - t0 > (1ll << 35)) __trap();      // protocol bug: fail loudly
                 }
             } else {
@@ -800,12 +800,17 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 for (int c = 0; c < p.kchunks; ++c)
                     for (int gi = 0; gi < ngr; ++gi) {
                         const int nt = p.sub4 ? p.ntaps[gi] : p.ntaps[tc.ph], t0 = p.sub4 ? p.tap0[gi] : p.tap0[tc.ph];
+                        long long tw0 = p.trace ? clock64() : 0;
                         wait_poll(&hfull_bar[hs], hphase);
+                        if (p.trace) w_halo += clock64() - tw0;
                         tc_fence_after();
+                        if (lane == 0 && c == 0 && gi == 0) LIC_TRACE(it, T_MMA_K0);
                         const uint64_t ahb = sdesc_sw128_sbo(halo0 + (uint32_t)hs * hstride, sbo);
                         for (int ti = 0; ti < nt; ti += TPS) {
                             const int ntp = min(TPS, nt - ti);
+                            long long tw1 = p.trace ? clock64() : 0;
                             wait_poll(&full_bar[stage], phase);
+                            if (p.trace) w_b += clock64() - tw1;
                             tc_fence_after();
                             const uint64_t bdb = sdesc_sw128(stage0 + (uint32_t)stage * p.stage_bytes);
                             if (elect_one()) {
@@ -833,7 +838,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         if (++hs == p.halo_slots) { hs = 0; hphase ^= 1; }
                     }
             };
-            const bool fast_halo = p.halo && !p.wres && !p.trace && (p.tps == 2 || p.tps == 3);
+            const bool fast_halo = p.halo && !p.wres && (p.tps == 2 || p.tps == 3);
             if (fast_halo) {
                 using I2 = std::integral_constant<int, 2>;
                 using I3 = std::integral_constant<int, 3>;

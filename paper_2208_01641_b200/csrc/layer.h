@@ -123,6 +123,8 @@ struct ConvParams {
     // two groups of 8 epilogue warps alternate tiles so one group's norm MMA round trip overlaps
     // the other's arithmetic; y is computed from the norm operand and the signs (conv_umma.cu)
     int g2;
+    int mma_spin;                     // g2: the MMA warp polls its operand barriers (test_wait loop) instead
+                                      // of a suspending try_wait
     // gather mode (g_s L4, stride-2 transposed conv N -> 3): the 9 input offsets go into N instead
     // of K -- P[p][t][j] = A[p] . W_t[j] over a 16 x 8 input tile (one A read per pixel, N = 9 x 16),
     // then out[g][j] = sum_t P[g + off_t][t][j] gathered through shared memory for the 14 x 6
