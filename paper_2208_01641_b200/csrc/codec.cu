@@ -176,6 +176,7 @@ struct lic_codec {
     int s2halo_enabled = 1;        // 5x5/s2 convs in parity-sub-grid halo mode (env LIC_S2HALO=0: per-tap tiles)
     int a_hi_only_enabled = 1;     // g_s L1 skips the zero lo plane of the integer y-hat (env LIC_YHAT_HI=0: off)
     int raw_tma_enabled = 1;       // u8 frames: raw patches by TMA (env LIC_RAW_TMA=0: cp.async)
+    int g2_mma_norm = 0;           // g2 halo layers: norm MMAs issued by the MMA warp (env LIC_G2_MMANORM=1; measured no change)
     int mma_spin = 0;              // g2 halo layers: MMA warp spins on operand barriers (env LIC_MMA_SPIN=1)
     int l1_stage_split = 1;        // u8 frames: hi-only A stages, twice as many (env LIC_L1_STAGES=0: off)
     int g2_enabled = 2;            // two-group GDN epilogue: 1 g_a L1 only, 2 every BN = 128 GDN layer (env LIC_G2)
@@ -663,6 +664,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         (gemm_l1 ? c->g2_enabled >= 1 : c->g2_enabled >= 2))
         P.g2 = 1;
     P.mma_spin = (P.g2 && !gemm_l1 && c->mma_spin) ? 1 : 0;
+    P.g2_mma_norm = (P.g2 && !gemm_l1 && c->g2_mma_norm) ? 1 : 0;
     P.L = c->L;
     // tensor maps
     const int ntaps_w = (gemm_l1 || P.gather) ? 1 : (P.pack4 ? 9 : Ly.k * Ly.k);
@@ -963,6 +965,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_L1_STAGES")) c->l1_stage_split = (e[0] != '0');
     if (const char* e = std::getenv("LIC_RAW_TMA")) c->raw_tma_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_MMA_SPIN")) c->mma_spin = (e[0] == '1');
+    if (const char* e = std::getenv("LIC_G2_MMANORM")) c->g2_mma_norm = (e[0] != '0');
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');

@@ -746,11 +746,21 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         int xsq_seen = 0;              // tiles whose x^2 the MMA warp has consumed
         // two-group epilogue: tiles whose main MMAs are committed / whose norm MMAs are issued
         // (in tile order; tile n uses accumulator buffer n & 1, the (n >> 1)-th phase of its barriers)
-        int g2_committed = 0;
-        (void)g2_committed;
+        int g2_committed = 0, g2_nn = 0;
         auto poll_norm = [&]() {       // cheap volatile smem read; the mbarrier wait then completes at once
             if constexpr (GC == 2) {
-                if (g2) return;                              // the epilogue issues its own norm MMAs
+                if (g2) {
+                    // g2_mma_norm: the MMA warp inserts each tile's norm MMAs between its stages
+                    // (they queue behind at most one stage); otherwise the epilogue issues them
+                    while (p.g2_mma_norm && g2_nn < g2_committed &&
+                           mbar_test(&xsq2_bar[g2_nn & 1], (uint32_t)(g2_nn >> 1) & 1u)) {
+                        pend_dcol = (uint32_t)((g2_nn & 1) * p.acc_stride);
+                        pend_it = g2_nn;
+                        issue_norm(&norm2_bar[g2_nn & 1]);
+                        ++g2_nn;
+                    }
+                    return;
+                }
             }
             if (kGdn && pend && *reinterpret_cast<volatile uint32_t*>(xsq_cnt) >= (uint32_t)(kEpiWarps * CG * (xsq_seen + 1))) {
                 mbar_wait(xsq_bar, xsq_phase);
@@ -763,7 +773,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         // norm of tile i is not held back while the warp waits for tile i+1's operands
         auto wait_poll = [&](uint64_t* bar, uint32_t par) {
             if constexpr (kGdn) {
-                if (g2 && !p.mma_spin) { mbar_wait(bar, par); return; }   // norms issued by the epilogue (g2)
+                if (g2 && !p.mma_spin && !p.g2_mma_norm) { mbar_wait(bar, par); return; }   // norms issued by the epilogue (g2)
                 if (mbar_test(bar, par)) return;
                 const long long t0 = clock64();
                 while (!mbar_test(bar, par)) {
@@ -958,12 +968,22 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 
             if (g2) {
                 g2_committed = it + 1;
+                poll_norm();
             } else if (kGdn) {
                 // the previous tile's norm must be issued before this one becomes pending
                 if (pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
                 pend = 1;
                 pend_it = it;
                 pend_dcol = (uint32_t)(buf * p.acc_stride);
+            }
+        }
+        if (g2 && p.g2_mma_norm && leader) {
+            while (g2_nn < g2_committed) {
+                mbar_wait(&xsq2_bar[g2_nn & 1], (uint32_t)(g2_nn >> 1) & 1u);
+                pend_dcol = (uint32_t)((g2_nn & 1) * p.acc_stride);
+                pend_it = g2_nn;
+                issue_norm(&norm2_bar[g2_nn & 1]);
+                ++g2_nn;
             }
         }
         if (kGdn && !g2 && pend && leader) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
@@ -1098,7 +1118,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         else mbar_arrive(&xsq2_bar[gr]);
                     }
                     if (threadIdx.x == lead) LIC_TRACE(it, T_EPI_XSQ);
-                    if (leader && threadIdx.x == lead) {
+                    if (leader && threadIdx.x == lead && !p.g2_mma_norm) {
                         // every warp of the group (both CTAs) has written v: issue norm = v . gamma^T
                         // from here (a blocking wait: the MMA warp keeps issuing main loops meanwhile)
                         if (!gamma_ok) { mbar_wait(gamma_bar, 0); gamma_ok = true; }

@@ -123,6 +123,7 @@ struct ConvParams {
     // two groups of 8 epilogue warps alternate tiles so one group's norm MMA round trip overlaps
     // the other's arithmetic; y is computed from the norm operand and the signs (conv_umma.cu)
     int g2;
+    int g2_mma_norm;                  // g2: the MMA warp issues the norm MMAs between its stages (halo layers)
     int mma_spin;                     // g2: the MMA warp polls its operand barriers (test_wait loop) instead
                                       // of a suspending try_wait
     // gather mode (g_s L4, stride-2 transposed conv N -> 3): the 9 input offsets go into N instead

@@ -84,7 +84,7 @@ def test_raw_patch_tma_vs_cp_async(lic, data):
 
 def test_norm_issue_by_mma_warp_or_epilogue(lic, data):
     a = run(lic, data)
-    b = run(lic, data, LIC_G2_MMANORM=0)
+    b = run(lic, data, LIC_G2_MMANORM=1)
     for k in ("y", "z", "ys", "yi", "zs", "xh"):
         assert np.array_equal(a[k], b[k]), k
 
