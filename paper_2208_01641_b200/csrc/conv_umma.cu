@@ -1068,7 +1068,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll 1
                     for (int s = 0; s < 2; ++s) {
                         tmem_ld32_nw(tcol0 + 32 * s, xr);
-                        tmem_ld_wait();
+                        tmem_ld_wait_dep32(xr);
 #pragma unroll
                         for (int i = 0; i < 32; ++i) amax = fmaxf(amax, fabsf(__uint_as_float(xr[i])));
                     }
@@ -1084,7 +1084,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll 1
                     for (int s = 0; s < 2; ++s) {
                         tmem_ld32_nw(tcol0 + 32 * s, xr);
-                        tmem_ld_wait();
+                        tmem_ld_wait_dep32(xr);
                         uint32_t hv[16], lv[16];
                         uint32_t sgs = 0u;
 #pragma unroll
@@ -1164,7 +1164,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         tmem_ld8_nw(ts, vh);
                         tmem_ld8_nw(ts + 16, vl);
                         tmem_ld16_nw(tcol0 + (uint32_t)p.BN + 16u * (uint32_t)pc, nr);
-                        tmem_ld_wait();
+                        tmem_ld_wait_dep(vh, vl, nr);
                         if (pc == 3) {
                             // every TMEM read of this tile is complete: release the buffer
                             tc_fence_before();

@@ -167,6 +167,24 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                  :: "r"(smem_u32(bar)) : "memory");
 }
+// wait::ld that also "rewrites" the destination registers of the outstanding loads, so the compiler
+// cannot schedule a use of them above the wait (tcgen05.ld is asynchronous)
+#define LIC_R4(a, i) "+r"(a[i]), "+r"(a[i + 1]), "+r"(a[i + 2]), "+r"(a[i + 3])
+__device__ __forceinline__ void tmem_ld_wait_dep32(uint32_t* a) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : LIC_R4(a, 0), LIC_R4(a, 4), LIC_R4(a, 8), LIC_R4(a, 12), LIC_R4(a, 16), LIC_R4(a, 20),
+                   LIC_R4(a, 24), LIC_R4(a, 28) :: "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait_dep(uint32_t* a8, uint32_t* b8, uint32_t* c16) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : LIC_R4(a8, 0), LIC_R4(a8, 4), LIC_R4(b8, 0), LIC_R4(b8, 4), LIC_R4(c16, 0), LIC_R4(c16, 4),
+                   LIC_R4(c16, 8), LIC_R4(c16, 12) :: "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait_dep16(uint32_t* a) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : LIC_R4(a, 0), LIC_R4(a, 4), LIC_R4(a, 8), LIC_R4(a, 12) :: "memory");
+}
+#undef LIC_R4
 // 32 lanes x 32 consecutive 32-bit columns: thread t of the warp gets lane (base_lane + t)
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     uint32_t r[32];
@@ -179,7 +197,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
           "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    tmem_ld_wait_dep32(r);
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
@@ -191,7 +209,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
           "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    tmem_ld_wait_dep16(r);
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblic.so")
+# LIC_LIB: an alternative in-tree build of the same library (A/B experiments, scripts/ab_lib.sh)
+LIB_PATH = os.path.join(_HERE, os.environ.get("LIC_LIB", "liblic.so"))
 
 LIC_OK, LIC_EINVAL, LIC_ESHAPE, LIC_ECORRUPT, LIC_EDIGEST, LIC_ENOMEM, LIC_ECUDA, LIC_EFOREIGN, \
     LIC_ENOSPACE = range(9)
