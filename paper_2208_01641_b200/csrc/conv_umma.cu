@@ -224,7 +224,7 @@ enum TraceEv { T_MMA_START = 0, T_MMA_END = 1, T_NORM_ISSUE = 2, T_EPI_START = 3
                T_B_PATCH = 8, T_B_C0_READY = 9, T_B_C0_DONE = 10, T_B_C1_READY = 11, T_B_C1_DONE = 12,
                T_MMA_K0 = 13, T_MMA_KL = 14, T_PEER_B_DONE = 15, T_B_RAW = 16,
                T_EPI_P2 = 17, T_EPI_ACQ = 18, T_EPI_STAGED = 19,
-               T_W_HALO = 20, T_W_B = 21, T_B_RAWISS = 22 };
+               T_W_HALO = 20, T_W_B = 21, T_B_RAWISS = 22, T_CTA = 23 };
 #define LIC_TRACE(it, ev)                                                                         \
     do {                                                                                          \
         if (p.trace && blockIdx.x == 0 && (it) < kTraceTiles)                                     \
@@ -294,6 +294,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     // barrier address the TMA / epilogue arrivals target: the leader CTA's copy
     auto lbar = [&](uint64_t* b) -> uint32_t { return CG == 2 ? mapa_shared(smem_u32(b), 0) : smem_u32(b); };
 
+    // test-only: CTA entry and setup-done times of CTA 0 (tile slots 0 / 1 of event T_CTA)
+    const long long t_entry = p.trace ? clock64() : 0;
     if (threadIdx.x == 0) {
         // fused L1: the 3 builder warps of each CTA arrive on the leader's full barrier
         const uint32_t full_cnt = p.fuse_l1 ? 3u * CG : 1u;
@@ -319,15 +321,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         else tmem_alloc(tmem_slot, (uint32_t)p.tmem_cols);
     }
     if (warp >= 4) {
-        // per-channel epilogue constants, staged once per CTA
-        const int np = p.BN * p.n_ntiles;
-        for (int i = threadIdx.x - 128; i < np; i += 32 * kEpiWarps) {
-            const bool in = i < p.Cout;
-            s_bias[i] = in ? p.bias[i] : 0.0f;
-            s_beta[i] = (in && p.beta) ? p.beta[i] : 0.0f;
-            s_mu[i] = (in && p.mu) ? p.mu[i] : 0.0f;
-        }
-        for (int i = threadIdx.x - 128; i < 64; i += 32 * kEpiWarps) s_tab[i] = p.table ? p.table[i] : 0.0f;
+        // (the per-channel epilogue constants are staged by the epilogue warps after the setup
+        // barrier: their global-load latency stays off the path to the first TMA loads)
         // halo mode: tap t's window starts at halo row (dy+1)*(Wt+2) + dx+1, i.e. this many
         // 16-byte descriptor units past the halo slot
         for (int i = threadIdx.x - 128; i < kMaxTaps; i += 32 * kEpiWarps)
@@ -358,6 +353,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0 && p.trace && blockIdx.x == 0) p.trace[T_CTA] = (unsigned long long)t_entry;
+    if (threadIdx.x == 0) LIC_TRACE(1, T_CTA);
     if (p.pdl) griddep_launch();          // the next layer may start its prologue on SMs we free
 
     const uint32_t a_bytes = kBM * kBK * 2;          // 16 KB per activation plane
@@ -989,6 +986,19 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         if (kGdn && !g2 && pend && leader) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
     } else if (warp >= 4) {
         // ====================== epilogue ======================
+        {
+            // per-channel epilogue constants, staged once per CTA (visible to every epilogue warp
+            // after the named barrier; nobody else reads them)
+            const int np = p.BN * p.n_ntiles;
+            for (int i = threadIdx.x - 128; i < np; i += 32 * kEpiWarps) {
+                const bool in = i < p.Cout;
+                s_bias[i] = in ? p.bias[i] : 0.0f;
+                s_beta[i] = (in && p.beta) ? p.beta[i] : 0.0f;
+                s_mu[i] = (in && p.mu) ? p.mu[i] : 0.0f;
+            }
+            for (int i = threadIdx.x - 128; i < 64; i += 32 * kEpiWarps) s_tab[i] = p.table ? p.table[i] : 0.0f;
+            named_bar_sync(15, 32 * kEpiWarps);
+        }
         if (p.pdl) griddep_wait();                  // global writes only after the previous kernel
         const int q = warp & 3;                     // TMEM lane quadrant
         const int g = (warp - 4) >> 2;              // channel group (quarter)

@@ -36,7 +36,7 @@ c.trace(layer, True)
 step()
 t = c.trace_read().astype(np.int64)
 names = ["mma_s", "mma_e", "norm_i", "epi_s", "epi_x2", "epi_n", "epi_e", "prod_s"]
-bnames = ["b_patch", "b_c0_rdy", "b_c0_done", "b_c1_rdy", "b_c1_done", "mma_k0", "mma_kl", "peerB", "b_raw", "epi_p2", "epi_acq", "epi_stg", "w_halo", "w_b", "b_rawiss"]
+bnames = ["b_patch", "b_c0_rdy", "b_c0_done", "b_c1_rdy", "b_c1_done", "mma_k0", "mma_kl", "peerB", "b_raw", "epi_p2", "epi_acq", "epi_stg", "w_halo", "w_b", "b_rawiss", "cta"]
 n = int((t[:, 0] > 0).sum())
 t0 = t[0, 0]
 fused = True
@@ -47,6 +47,12 @@ for i in range(min(n, 40)):
     row = [(v if name.startswith("w_") else v - t0) if v else -1 for name, v in zip(cols, t[i, :len(cols)])]
     gap = t[i, 0] - t[i - 1, 1] if i else 0
     print(f"{i:4d} " + " ".join(f"{v:9d}" for v in row) + f"   {t[i,1]-t[i,0]:7d} {t[i,6]-t[i,3]:7d} {gap:7d}")
+# kernel-relative view: CTA entry (tile slot 0 of "cta"), setup done (slot 1), then tile 0's events
+ent, setup = int(t[0, 23]), int(t[1, 23])
+if ent:
+    print(f"CTA 0: setup {setup - ent} cycles after entry; tile 0 (from entry): producer {t[0,7]-ent}, "
+          f"MMA start {t[0,0]-ent}, first operands {t[0,13]-ent}, MMA end {t[0,1]-ent}, epilogue start {t[0,3]-ent}, "
+          f"epilogue end {t[0,6]-ent}; last tile epilogue end {t[n-1,6]-ent}")
 per_tile = (t[n - 1, 6] - t[0, 0]) / max(n, 1)
 print(f"mean cycles per tile (first MMA start -> last epilogue end): {per_tile:.0f}")
 print(f"mean MMA-busy per tile: {np.mean(t[:n,1]-t[:n,0]):.0f}, mean epilogue per tile: {np.mean(t[:n,6]-t[:n,3]):.0f}")
