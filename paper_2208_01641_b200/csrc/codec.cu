@@ -31,6 +31,10 @@ namespace lic {
 cudaError_t launch_conv_umma(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                              const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const ConvParams&, int,
                              cudaStream_t);
+cudaError_t launch_split_reduce(const float* part, int S, int B, int H, int W, int C, const float* bias,
+                                const float* mu, int ep, int L, __half* out_act, size_t act_plane, int split,
+                                int8_t* out_sym, float* out_f32, unsigned long long* sat_count,
+                                unsigned long long* range_count, cudaStream_t st);
 cudaError_t launch_sym_ingest(const int8_t*, const float*, int, int, int, int, __half*, size_t, int, cudaStream_t);
 cudaError_t launch_pack_chw(const float*, int, int, int, int, __half*, size_t, int, cudaStream_t);
 cudaError_t launch_sigma_index(const float*, size_t, const float*, uint8_t*, cudaStream_t);
@@ -159,6 +163,7 @@ struct lic_codec {
     int8_t* d_ysym = nullptr;
     uint8_t* d_yidx = nullptr;
     int8_t* d_zsym = nullptr;
+    float* d_part = nullptr;                 // split-K partial sums (workspace)
     float* d_dbg = nullptr;             // test-layer / debug scratch
     float* d_dbg_in = nullptr;          // test-layer input copy for the fused g_a L1
     size_t dbg_elems = 0;
@@ -176,6 +181,8 @@ struct lic_codec {
     int s2halo_enabled = 1;        // 5x5/s2 convs in parity-sub-grid halo mode (env LIC_S2HALO=0: per-tap tiles)
     int a_hi_only_enabled = 1;     // g_s L1 skips the zero lo plane of the integer y-hat (env LIC_YHAT_HI=0: off)
     int raw_tma_enabled = 1;       // u8 frames: raw patches by TMA (env LIC_RAW_TMA=0: cp.async)
+    int ksplit_enabled = 1;        // split-K for the few-tile h layers (env LIC_KSPLIT=0: off, =2/3/4: at most that many slices)
+    int ksplit_force = 0;
     int g2_mma_norm = 0;           // g2 halo layers: norm MMAs issued by the MMA warp (env LIC_G2_MMANORM=1; measured no change)
     int mma_spin = 0;              // g2 halo layers: MMA warp spins on operand barriers (env LIC_MMA_SPIN=1)
     int l1_stage_split = 1;        // u8 frames: hi-only A stages, twice as many (env LIC_L1_STAGES=0: off)
@@ -373,6 +380,7 @@ static void choose_tile(int Hg, int Wg, int* Wt, int* Ht) {
 // mbarrier area: full/empty[<= 8] + tfull/tempty[2] + norm + gamma + hfull/hempty[4] + xsq +
 // wres (34 x 8 B) + the TMEM base slot
 static constexpr uint32_t kBarBytes = 512;
+constexpr int kKsplitMax = 4;                // split-K slices of the few-tile h layers (run_layer)
 static constexpr int kGatherN = 144;     // g_s L4 gather mode: 9 input offsets x 16 packed outputs
 static_assert(kBarBytes >= (2 * 8 + 2 * 2 + 2 + 2 * 4 + 2) * 8 + 4, "barrier area too small");
 
@@ -665,6 +673,14 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.g2 = 1;
     P.mma_spin = (P.g2 && !gemm_l1 && c->mma_spin) ? 1 : 0;
     P.g2_mma_norm = (P.g2 && !gemm_l1 && c->g2_mma_norm) ? 1 : 0;
+    {
+        // split-K candidates: the h layers with a handful of tiles (h_a L2, L3, h_s L1), whose
+        // epilogue split_reduce_kernel implements (ReLU, z-quantise) and whose MMA loop is the
+        // lean halo loop (the only one that iterates a K slice)
+        const int lid = (int)(&Ly - c->layers);
+        P.ksplit_ok = (lid == HA2 || lid == HA3 || lid == HS1) && P.halo && !P.wres && (P.tps == 2 || P.tps == 3) &&
+                      P.cg == 2 && P.n_ntiles == 1 && (Ly.ep == EP_RELU || Ly.ep == EP_ZQUANT) && P.Cout % 8 == 0;
+    }
     P.L = c->L;
     // tensor maps
     const int ntaps_w = (gemm_l1 || P.gather) ? 1 : (P.pack4 ? 9 : Ly.k * Ly.k);
@@ -732,6 +748,25 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
     P.batch = batch;
     const int txs = (P.tiles_x + P.cg - 1) / P.cg;          // tiles (or CTA-pair tiles) along x
     P.total_tiles = batch * P.nphase * P.tiles_y * txs * P.n_ntiles;
+    // split-K: a layer with fewer (pair) tiles than a quarter of the SMs runs each
+    // tile as S K slices on S times as many CTAs; the slices' fp32 partial sums are added in
+    // slice order by split_reduce_kernel, which applies the layer's epilogue
+    int S = 1;
+    if (P.ksplit_ok && c->ksplit_enabled && c->d_part) {
+        S = std::min(kKsplitMax, (c->num_sms / P.cg) / std::max(1, P.total_tiles));
+        if (c->ksplit_force) S = std::min(S, c->ksplit_force);
+        if (S < 2) S = 1;
+    }
+    const ConvParams Pe = P;                                   // the layer's own epilogue fields
+    P.ksplit = S;
+    if (S > 1) {
+        P.total_tiles *= S;
+        P.ep = EP_PARTIAL;
+        P.part = c->d_part;
+        P.out_act = nullptr; P.out_sym = nullptr; P.out_f32 = nullptr;
+        P.sat_count = nullptr; P.range_count = nullptr;
+        P.tma_out = 0;
+    }
     const int grid = P.cg * std::min(P.total_tiles, c->num_sms / P.cg);
     const int lid = (int)(&Ly - c->layers);
     P.pdl = c->pdl_enabled;
@@ -753,6 +788,14 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
                         lid, grid, P.cg, P.smem_bytes, P.total_tiles, P.stages, P.halo, cudaGetErrorString(e));
     }
     ++c->launches;
+    if (S > 1) {
+        const cudaError_t e = launch_split_reduce(c->d_part, S, batch, Pe.Hout, Pe.Wout, Pe.Cout, Pe.bias, Pe.mu, Pe.ep,
+                                                  Pe.L, reinterpret_cast<__half*>(Pe.out_act), Pe.act_plane, Pe.split,
+                                                  reinterpret_cast<int8_t*>(Pe.out_sym), Pe.out_f32, Pe.sat_count,
+                                                  Pe.range_count, st);
+        if (e != cudaSuccess) return fail(c, LIC_ECUDA, "split-K reduce of layer %d: %s", lid, cudaGetErrorString(e));
+        ++c->launches;
+    }
     if (prof) {
         CK(cudaEventRecord(c->ev[2 * c->ev_used + 1], st));
         c->ev_layer[c->ev_used++] = lid;
@@ -818,7 +861,8 @@ extern "C" void lic_close(lic_codec* c) {
 // z-plane (z-hat), the host-frame staging buffer and the symbol / index staging planes.  One
 // block, carved in this order at 256-byte boundaries; owned by the library (lic_open) or by
 // the caller (lic_bind_workspace).
-struct WsLayout { size_t planeA, planeY, planeZ, off[8], total; };
+// (hyperprior codecs add the split-K partial sums of the h layers: fp32 [kKsplitMax][B][Hp/32][Wp/32][N])
+struct WsLayout { size_t planeA, planeY, planeZ, off[9], total; };
 static WsLayout ws_layout(const lic_codec* c, int B) {
     WsLayout L{};
     const int S = c->split, N = c->N, M = c->M;
@@ -826,11 +870,12 @@ static WsLayout ws_layout(const lic_codec* c, int B) {
     L.planeA = (size_t)B * (c->Hp / 2) * (c->Wp / 2) * N;
     L.planeY = (size_t)B * Hy * Wy * M;
     L.planeZ = (size_t)B * Hz * Wz * N;
-    const size_t sz[8] = {L.planeA * S * 2, L.planeA * S * 2, L.planeY * S * 2, L.planeZ * S * 2,
+    const size_t npart = c->kind == 1 ? (size_t)kKsplitMax * B * (c->Hp / 32) * (c->Wp / 32) * N * 4 : 0;
+    const size_t sz[9] = {L.planeA * S * 2, L.planeA * S * 2, L.planeY * S * 2, L.planeZ * S * 2,
                           (size_t)B * 3 * c->H * c->W * 4, (size_t)B * M * Hy * Wy, (size_t)B * M * Hy * Wy,
-                          (size_t)B * N * Hz * Wz};
+                          (size_t)B * N * Hz * Wz, npart};
     size_t o = 0;
-    for (int i = 0; i < 8; ++i) { L.off[i] = o; o += (sz[i] + 255) / 256 * 256; }
+    for (int i = 0; i < 9; ++i) { L.off[i] = o; o += (sz[i] + 255) / 256 * 256; }
     L.total = o;
     return L;
 }
@@ -845,6 +890,7 @@ static void ws_carve(lic_codec* c, uint8_t* base, int B) {
     c->d_ysym = (int8_t*)(base + L.off[5]);
     c->d_yidx = (uint8_t*)(base + L.off[6]);
     c->d_zsym = (int8_t*)(base + L.off[7]);
+    c->d_part = c->kind == 1 ? (float*)(base + L.off[8]) : nullptr;
 }
 static __half* ws_buf(const lic_codec* c, char id, size_t* plane) {
     switch (id) {
@@ -966,6 +1012,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_RAW_TMA")) c->raw_tma_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_MMA_SPIN")) c->mma_spin = (e[0] == '1');
     if (const char* e = std::getenv("LIC_G2_MMANORM")) c->g2_mma_norm = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_KSPLIT")) { c->ksplit_enabled = atoi(e) != 0; c->ksplit_force = atoi(e) > 1 ? atoi(e) : 0; }
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');

@@ -39,7 +39,7 @@ constexpr int kEpiWarps = 16;                 // 4 per TMEM lane quadrant
 constexpr int kEpiGroups = kEpiWarps / 4;     // channel groups (quarters of the N tile)
 constexpr int kThreads = 128 + 32 * kEpiWarps;
 
-struct TileCoord { int b, ph, gy0, gx0, nt; };
+struct TileCoord { int b, ph, gy0, gx0, nt, split; };
 
 // Tile order: sub-pixel phase fastest, then N tile, x, y, frame -- the 4 phase tiles (and
 // the N tiles) of one location run on neighbouring CTAs and share their input via L2.
@@ -52,6 +52,8 @@ __device__ __forceinline__ int fdiv(int n, uint32_t m, int s) {
 }
 __device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t, int rank) {
     TileCoord c;
+    c.split = 0;
+    if (p.ksplit > 1) { c.split = t % p.ksplit; t /= p.ksplit; }
     c.ph = t & (p.nphase - 1);  t >>= p.nph_log2;
     if (p.nphase == 4) c.ph = (c.ph + t) & 3;
     int q = fdiv(t, p.fd_nt_m, p.fd_nt_s);
@@ -64,6 +66,24 @@ __device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t, int
     c.gx0 = tx * p.tsx;
     c.gy0 = ty * p.tsy;
     return c;
+}
+
+// split-K: this tile's slice of the flattened (chunk, parity group, tap) sequence, and one
+// group's local tap range [lo, hi) within it (empty: the group is skipped by every role)
+struct KRange { int u0, u1, T; };
+__device__ __forceinline__ KRange k_range(const ConvParams& p, const TileCoord& tc) {
+    KRange k;
+    k.T = p.sub4 ? (p.ntaps[0] + p.ntaps[1] + p.ntaps[2] + p.ntaps[3]) : p.ntaps[tc.ph];
+    const int U = p.kchunks * k.T;
+    k.u0 = p.ksplit > 1 ? tc.split * U / p.ksplit : 0;
+    k.u1 = p.ksplit > 1 ? (tc.split + 1) * U / p.ksplit : U;
+    return k;
+}
+__device__ __forceinline__ void group_range(const ConvParams& p, const KRange& k, int c, int gi, int nt, int& lo,
+                                            int& hi) {
+    const int ub = c * k.T + (p.sub4 ? p.tap0[gi] : 0);
+    lo = max(0, k.u0 - ub);
+    hi = min(nt, k.u1 - ub);
 }
 
 __device__ __forceinline__ uint32_t h2_bits(float a, float b) {
@@ -635,11 +655,14 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 // chunk-outer, tap-inner weight tiles (halos come from warp 3); p.tps consecutive
                 // taps share a stage (one barrier wait per 8 * tps MMAs)
                 // (sub4: the 4 parity groups of each chunk in turn)
+                const KRange kr = k_range(p, tc);
                 for (int c = 0; c < p.kchunks; ++c)
                     for (int gi = 0; gi < (p.sub4 ? 4 : 1); ++gi) {
                         const int gnt = p.sub4 ? p.ntaps[gi] : nt, gt0 = p.sub4 ? p.tap0[gi] : t0;
-                        for (int ti = 0; ti < gnt; ti += p.tps) {
-                            const int ntp = min(p.tps, gnt - ti);
+                        int tlo, thi;
+                        group_range(p, kr, c, gi, gnt, tlo, thi);
+                        for (int ti = tlo; ti < thi; ti += p.tps) {
+                            const int ntp = min(p.tps, thi - ti);
                             mbar_wait(&empty_bar[stage], phase ^ 1);
                             if (elect_one()) {
                                 expect(&full_bar[stage], b_bytes * (uint32_t)ntp);
@@ -684,8 +707,14 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const uint32_t hbytes = (uint32_t)p.halo_w * (p.Ht + 2) * 128 * (hlo ? 2 : 1);
             for (int t = cid; t < p.total_tiles; t += ncl) {
                 TileCoord tc = decode_tile(p, t, rank);
+                const KRange kr = k_range(p, tc);
                 for (int c = 0; c < p.kchunks; ++c)
                   for (int gi = 0; gi < (p.sub4 ? 4 : 1); ++gi) {
+                    {
+                        int tlo, thi;
+                        group_range(p, kr, c, gi, p.sub4 ? p.ntaps[gi] : p.ntaps[tc.ph], tlo, thi);
+                        if (tlo >= thi) continue;                       // no tap of this K slice
+                    }
                     // sub4: parity sub-grid (py, px) = (gi >> 1, gi & 1), rows / columns gy0 - 1 ..
                     // of the sub-grid = input 2 * (gy0 - 1) + py .. in steps of 2 (the map's stride)
                     const int hx = p.sub4 ? 2 * (tc.gx0 - 1) + (gi & 1) : tc.gx0 - 1;
@@ -804,24 +833,29 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 const uint64_t bstep16 = b_bytes >> 4;
                 const uint32_t halo0 = smem_u32(smem + p.off_halo), stage0 = smem_u32(smem);
                 const int ngr = p.sub4 ? 4 : 1;
+                const KRange kr = k_range(p, tc);
+                bool first = true;                         // the K slice's first MMA overwrites the accumulator
                 for (int c = 0; c < p.kchunks; ++c)
                     for (int gi = 0; gi < ngr; ++gi) {
                         const int nt = p.sub4 ? p.ntaps[gi] : p.ntaps[tc.ph], t0 = p.sub4 ? p.tap0[gi] : p.tap0[tc.ph];
+                        int tlo, thi;
+                        group_range(p, kr, c, gi, nt, tlo, thi);
+                        if (tlo >= thi) continue;
                         long long tw0 = p.trace ? clock64() : 0;
                         wait_poll(&hfull_bar[hs], hphase);
                         if (p.trace) w_halo += clock64() - tw0;
                         tc_fence_after();
                         if (lane == 0 && c == 0 && gi == 0) LIC_TRACE(it, T_MMA_K0);
                         const uint64_t ahb = sdesc_sw128_sbo(halo0 + (uint32_t)hs * hstride, sbo);
-                        for (int ti = 0; ti < nt; ti += TPS) {
-                            const int ntp = min(TPS, nt - ti);
+                        for (int ti = tlo; ti < thi; ti += TPS) {
+                            const int ntp = min(TPS, thi - ti);
                             long long tw1 = p.trace ? clock64() : 0;
                             wait_poll(&full_bar[stage], phase);
                             if (p.trace) w_b += clock64() - tw1;
                             tc_fence_after();
                             const uint64_t bdb = sdesc_sw128(stage0 + (uint32_t)stage * p.stage_bytes);
                             if (elect_one()) {
-                                const uint32_t acc0 = (c | gi | ti) != 0;
+                                const uint32_t acc0 = first ? 0u : 1u;
 #pragma unroll
                                 for (int u = 0; u < TPS; ++u) {
                                     if (u < ntp) {
@@ -837,6 +871,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                                 commit(&empty_bar[stage]);
                             }
                             __syncwarp();
+                            first = false;
                             if (++stage == p.stages) { stage = 0; phase ^= 1; }
                             poll_norm();
                         }
@@ -1687,7 +1722,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     if (p.pack4) {
 #pragma unroll
                         for (int j = 0; j < 16; ++j) v[j] += s_bias[j & 3];
-                    } else {
+                    } else if (p.ep != EP_PARTIAL) {
 #pragma unroll
                         for (int i4 = 0; i4 < 4; ++i4) {
                             const float4 bb = lds4(s_bias + cb + 4 * i4);
@@ -1695,6 +1730,17 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         }
                     }
                     switch (p.ep) {
+                    case EP_PARTIAL: {
+                        if (valid) {
+                            float4* dst = reinterpret_cast<float4*>(
+                                p.part + ((((size_t)tc.split * p.batch + tc.b) * p.Hout + oy) * p.Wout + ox) * p.Cout + cb);
+                            dst[0] = make_float4(v[0], v[1], v[2], v[3]);          // raw accumulator (no bias)
+                            dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+                            dst[2] = make_float4(v[8], v[9], v[10], v[11]);
+                            dst[3] = make_float4(v[12], v[13], v[14], v[15]);
+                        }
+                        break;
+                    }
                     case EP_F32: {
                         if (valid) {
 #pragma unroll

@@ -21,6 +21,8 @@ enum EpKind : int {
     EP_ZQUANT = 5,  // s = clamp(round(z - mu)) -> int8 CHW; z-hat = s + mu -> hi/lo NHWC
     EP_SIGMA = 6,   // sigma = relu(x); idx = #{table_j < max(sigma, 0.11f)} -> uint8 CHW
     EP_FINAL = 7,   // clamp(x, 0, 1), crop -> f32 CHW and/or u8 HWC
+    EP_PARTIAL = 8, // split-K: the raw fp32 accumulator of one K slice -> part[split] NHWC (summed by
+                    // split_reduce_kernel, which applies the layer's own epilogue)
 };
 
 constexpr int kMaxTaps = 32;
@@ -123,6 +125,11 @@ struct ConvParams {
     // two groups of 8 epilogue warps alternate tiles so one group's norm MMA round trip overlaps
     // the other's arithmetic; y is computed from the norm operand and the signs (conv_umma.cu)
     int g2;
+    // split-K (few-tile h layers): tile t of the launch is (output tile t / ksplit, K slice t % ksplit);
+    // slice s runs the flattened (chunk, parity group, tap) range [s U / ksplit, (s + 1) U / ksplit)
+    int ksplit;
+    int ksplit_ok;                    // host: the layer may be split (run_layer picks ksplit from the batch)
+    float* part;                      // EP_PARTIAL: fp32 [ksplit][batch][Hout][Wout][Cout]
     int g2_mma_norm;                  // g2: the MMA warp issues the norm MMAs between its stages (halo layers)
     int mma_spin;                     // g2: the MMA warp polls its operand barriers (test_wait loop) instead
                                       // of a suspending try_wait
