@@ -183,7 +183,6 @@ struct lic_codec {
     int raw_tma_enabled = 1;       // u8 frames: raw patches by TMA (env LIC_RAW_TMA=0: cp.async)
     int ksplit_enabled = 1;        // split-K for the few-tile h layers (env LIC_KSPLIT=0: off, =2/3/4: at most that many slices)
     int ksplit_force = 0;
-    int g2_mma_norm = 0;           // g2 halo layers: norm MMAs issued by the MMA warp (env LIC_G2_MMANORM=1; measured no change)
     int mma_spin = 0;              // g2 halo layers: MMA warp spins on operand barriers (env LIC_MMA_SPIN=1)
     int l1_stage_split = 1;        // u8 frames: hi-only A stages, twice as many (env LIC_L1_STAGES=0: off)
     int g2_enabled = 2;            // two-group GDN epilogue: 1 g_a L1 only, 2 every BN = 128 GDN layer (env LIC_G2)
@@ -672,7 +671,6 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         (gemm_l1 ? c->g2_enabled >= 1 : c->g2_enabled >= 2))
         P.g2 = 1;
     P.mma_spin = (P.g2 && !gemm_l1 && c->mma_spin) ? 1 : 0;
-    P.g2_mma_norm = (P.g2 && !gemm_l1 && c->g2_mma_norm) ? 1 : 0;
     {
         // split-K candidates: the h layers with a handful of tiles (h_a L2, L3, h_s L1), whose
         // epilogue split_reduce_kernel implements (ReLU, z-quantise) and whose MMA loop is the
@@ -1011,7 +1009,6 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_L1_STAGES")) c->l1_stage_split = (e[0] != '0');
     if (const char* e = std::getenv("LIC_RAW_TMA")) c->raw_tma_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_MMA_SPIN")) c->mma_spin = (e[0] == '1');
-    if (const char* e = std::getenv("LIC_G2_MMANORM")) c->g2_mma_norm = (e[0] != '0');
     if (const char* e = std::getenv("LIC_KSPLIT")) { c->ksplit_enabled = atoi(e) != 0; c->ksplit_force = atoi(e) > 1 ? atoi(e) : 0; }
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');

@@ -50,10 +50,12 @@ struct TileCoord { int b, ph, gy0, gx0, nt, split; };
 __device__ __forceinline__ int fdiv(int n, uint32_t m, int s) {
     return (int)((__umulhi((uint32_t)n, m) + (uint32_t)n) >> s);
 }
+// SPLITK: the instantiation may run split-K layers (non-GDN only; run_layer never splits others)
+template <bool SPLITK = false>
 __device__ __forceinline__ TileCoord decode_tile(const ConvParams& p, int t, int rank) {
     TileCoord c;
     c.split = 0;
-    if (p.ksplit > 1) { c.split = t % p.ksplit; t /= p.ksplit; }
+    if (SPLITK && p.ksplit > 1) { c.split = t % p.ksplit; t /= p.ksplit; }
     c.ph = t & (p.nphase - 1);  t >>= p.nph_log2;
     if (p.nphase == 4) c.ph = (c.ph + t) & 3;
     int q = fdiv(t, p.fd_nt_m, p.fd_nt_s);
@@ -262,7 +264,9 @@ enum TraceEv { T_MMA_START = 0, T_MMA_END = 1, T_NORM_ISSUE = 2, T_EPI_START = 3
 // CG: 1 = one CTA per 128-pixel tile; 2 = CTA pair (cluster of 2, tcgen05 cta_group::2, M = 256):
 //     each CTA loads its own A (or halo) and half of B / gamma, the leader issues the MMAs and
 //     commits to both CTAs' barriers, the peer's epilogue arrives remotely on the leader's.
-template <int GC, int CG>
+// L1: the fused g_a L1 variant (frame builders, resident weights) -- a separate instantiation,
+// so neither variant carries the other's code or register allocation
+template <int GC, int CG, bool L1>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                  const __grid_constant__ CUtensorMap mapB,
@@ -304,6 +308,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     constexpr bool kGdn = GC > 0;
+    constexpr bool kL1 = L1;                // == p.fuse_l1 (the host dispatches on it)
+    constexpr bool kSplitK = GC == 0 && !L1; // split-K layers are ReLU / z-quantise layers
     // two-group GDN epilogue (BN = 128): epilogue warps 4-11 take the even tiles of this CTA,
     // 12-19 the odd ones, each warp 32 pixels x 64 channels; the groups' norm round trips overlap
     const bool g2 = GC == 2 && p.g2;
@@ -318,7 +324,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     const long long t_entry = p.trace ? clock64() : 0;
     if (threadIdx.x == 0) {
         // fused L1: the 3 builder warps of each CTA arrive on the leader's full barrier
-        const uint32_t full_cnt = p.fuse_l1 ? 3u * CG : 1u;
+        const uint32_t full_cnt = kL1 ? 3u * CG : 1u;
         for (int s = 0; s < p.stages; ++s) { mbar_init(&full_bar[s], full_cnt); mbar_init(&empty_bar[s], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull_bar[i], 1); mbar_init(&tempty_bar[i], epi_arrivals); }
         for (int i = 0; i < 2; ++i) { mbar_init(&xsq2_bar[i], epi_arrivals); mbar_init(&norm2_bar[i], 1); }
@@ -332,7 +338,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
-        if (!p.fuse_l1) tma_prefetch_desc(&mapA);
+        if (!kL1) tma_prefetch_desc(&mapA);
         tma_prefetch_desc(&mapB);
         if (kGdn) tma_prefetch_desc(&mapG);
     }
@@ -348,7 +354,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         for (int i = threadIdx.x - 128; i < kMaxTaps; i += 32 * kEpiWarps)
             s_tapoff[i] = (uint32_t)(((p.tap_dy[i] + 1) * p.halo_w + p.tap_dx[i] + 1) * 8);
     }
-    if (p.fuse_l1) {
+    if constexpr (kL1) {
         // zero the A stages (K columns >= 80 are never rewritten) and both patch buffers (the
         // row padding halves 105..111 are never rewritten); u8 -> (hi | lo << 16) of u8 / 255
         // (IEEE division, as the oracle), entry 256 = 0 for samples outside the frame
@@ -425,7 +431,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         // outside the frame, completing on rawfull_bar
         const bool raw_tma = fast && p.raw_tma;
         auto raw_issue = [&](int tt, int buf) {
-            const TileCoord tn = decode_tile(p, tt, rank);
+            const TileCoord tn = decode_tile<kSplitK>(p, tt, rank);
             if (raw_tma) {
                 if (bw == 0 && lane == 0) {
                     mbar_arrive_expect_tx(&rawfull_bar[buf], kL1RawBytes);
@@ -453,7 +459,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         uint32_t phase = 0;
         int it = 0;
         for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
-            const TileCoord tc = decode_tile(p, t, rank);
+            const TileCoord tc = decode_tile<kSplitK>(p, t, rank);
             const uint32_t pbh = patch_s + (uint32_t)((it & 1) * 2 * kL1PlaneBytes), pbl = pbh + kL1PlaneBytes;
             const int iy0 = 2 * tc.gy0 - 2 - p.fr_top, ix0 = 2 * tc.gx0 - 2 - p.fr_left;
             // ---- patch (double-buffered by tile parity; the named barrier of tile it+1 orders
@@ -614,8 +620,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         }
     };
 
-    if (warp == 2 && p.fuse_l1) {
-        build_l1(1);
+    if (kL1 && warp == 2) {
+        if constexpr (kL1) build_l1(1);
     } else if (warp == 0) {
         // ====================== TMA producer (weights; activations unless halo mode) ======================
         // warp-uniform loop; one elected lane issues (keeps coordinates in uniform registers)
@@ -647,8 +653,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         uint32_t phase = 0;
         int pit = 0;
         // (resident weights: only the gather mode still streams A tiles from here)
-        for (int t = cid; t < p.total_tiles && (!p.wres || p.gather); t += ncl, ++pit) {
-            TileCoord tc = decode_tile(p, t, rank);
+        for (int t = cid; !kL1 && t < p.total_tiles && (!p.wres || p.gather); t += ncl, ++pit) {
+            TileCoord tc = decode_tile<kSplitK>(p, t, rank);
             const int nt = p.ntaps[tc.ph], t0 = p.tap0[tc.ph];
             if (lane == 0) LIC_TRACE(pit, T_PROD_START);
             if (p.halo) {
@@ -695,18 +701,18 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 }
             }
         }
-        if (p.fuse_l1) build_l1(0);
+        if constexpr (kL1) build_l1(0);
     } else if (warp == 3) {
         // ====================== halo producer (halo mode) ======================
-        if (p.fuse_l1) build_l1(2);
-        if (p.halo) {
+        if constexpr (kL1) build_l1(2);
+        if (!kL1 && p.halo) {
             if (p.pdl) griddep_wait();
             int hs = 0;
             uint32_t hphase = 0;
             const bool hlo = p.split == 2 && !p.a_hi_only;      // load the lo plane
             const uint32_t hbytes = (uint32_t)p.halo_w * (p.Ht + 2) * 128 * (hlo ? 2 : 1);
             for (int t = cid; t < p.total_tiles; t += ncl) {
-                TileCoord tc = decode_tile(p, t, rank);
+                TileCoord tc = decode_tile<kSplitK>(p, t, rank);
                 const KRange kr = k_range(p, tc);
                 for (int c = 0; c < p.kchunks; ++c)
                   for (int gi = 0; gi < (p.sub4 ? 4 : 1); ++gi) {
@@ -772,21 +778,11 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         int xsq_seen = 0;              // tiles whose x^2 the MMA warp has consumed
         // two-group epilogue: tiles whose main MMAs are committed / whose norm MMAs are issued
         // (in tile order; tile n uses accumulator buffer n & 1, the (n >> 1)-th phase of its barriers)
-        int g2_committed = 0, g2_nn = 0;
+        int g2_committed = 0;
+        (void)g2_committed;
         auto poll_norm = [&]() {       // cheap volatile smem read; the mbarrier wait then completes at once
             if constexpr (GC == 2) {
-                if (g2) {
-                    // g2_mma_norm: the MMA warp inserts each tile's norm MMAs between its stages
-                    // (they queue behind at most one stage); otherwise the epilogue issues them
-                    while (p.g2_mma_norm && g2_nn < g2_committed &&
-                           mbar_test(&xsq2_bar[g2_nn & 1], (uint32_t)(g2_nn >> 1) & 1u)) {
-                        pend_dcol = (uint32_t)((g2_nn & 1) * p.acc_stride);
-                        pend_it = g2_nn;
-                        issue_norm(&norm2_bar[g2_nn & 1]);
-                        ++g2_nn;
-                    }
-                    return;
-                }
+                if (g2) return;                              // the epilogue issues its own norm MMAs
             }
             if (kGdn && pend && *reinterpret_cast<volatile uint32_t*>(xsq_cnt) >= (uint32_t)(kEpiWarps * CG * (xsq_seen + 1))) {
                 mbar_wait(xsq_bar, xsq_phase);
@@ -799,7 +795,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         // norm of tile i is not held back while the warp waits for tile i+1's operands
         auto wait_poll = [&](uint64_t* bar, uint32_t par) {
             if constexpr (kGdn) {
-                if (g2 && !p.mma_spin && !p.g2_mma_norm) { mbar_wait(bar, par); return; }   // norms issued by the epilogue (g2)
+                if (g2 && !p.mma_spin) { mbar_wait(bar, par); return; }   // norms issued by the epilogue (g2)
                 if (mbar_test(bar, par)) return;
                 const long long t0 = clock64();
                 while (!mbar_test(bar, par)) {
@@ -812,7 +808,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         };
         if (p.wres && leader) mbar_wait(wres_bar, 0);      // the peer's bytes land on the leader's barrier
         for (int t = cid; t < p.total_tiles && leader; t += ncl, ++it) {
-            TileCoord tc = decode_tile(p, t, rank);
+            TileCoord tc = decode_tile<kSplitK>(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
             const uint32_t use = (p.n_accbuf == 2) ? (uint32_t)(it >> 1) : (uint32_t)it;
             if (kGdn && !g2 && pend && p.n_accbuf == 1) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
@@ -824,23 +820,27 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             // halo mode, streamed weights, 2 or 3 taps per stage, no trace: the lean issue loop --
             // tap window offsets from the kernel parameters (uniform registers), the stage count
             // compile-time, no per-stage parameter tests
-            auto halo_fast = [&](auto tps_c, auto lo_c) {
+            auto halo_fast = [&](auto tps_c, auto lo_c, auto split_c) {
                 constexpr int TPS = decltype(tps_c)::value;
                 constexpr bool LO = decltype(lo_c)::value;
+                constexpr bool SPLIT = decltype(split_c)::value;   // a K slice (split-K layers)
                 const uint32_t sbo = (uint32_t)p.halo_w * 128;
                 const uint32_t hstride = (uint32_t)p.split * p.halo_plane_bytes;
                 const uint64_t lo16 = p.halo_plane_bytes >> 4;
                 const uint64_t bstep16 = b_bytes >> 4;
                 const uint32_t halo0 = smem_u32(smem + p.off_halo), stage0 = smem_u32(smem);
                 const int ngr = p.sub4 ? 4 : 1;
-                const KRange kr = k_range(p, tc);
+                KRange kr;
+                if constexpr (SPLIT) kr = k_range(p, tc);
                 bool first = true;                         // the K slice's first MMA overwrites the accumulator
                 for (int c = 0; c < p.kchunks; ++c)
                     for (int gi = 0; gi < ngr; ++gi) {
                         const int nt = p.sub4 ? p.ntaps[gi] : p.ntaps[tc.ph], t0 = p.sub4 ? p.tap0[gi] : p.tap0[tc.ph];
-                        int tlo, thi;
-                        group_range(p, kr, c, gi, nt, tlo, thi);
-                        if (tlo >= thi) continue;
+                        int tlo = 0, thi = nt;
+                        if constexpr (SPLIT) {
+                            group_range(p, kr, c, gi, nt, tlo, thi);
+                            if (tlo >= thi) continue;
+                        }
                         long long tw0 = p.trace ? clock64() : 0;
                         wait_poll(&hfull_bar[hs], hphase);
                         if (p.trace) w_halo += clock64() - tw0;
@@ -855,7 +855,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             tc_fence_after();
                             const uint64_t bdb = sdesc_sw128(stage0 + (uint32_t)stage * p.stage_bytes);
                             if (elect_one()) {
-                                const uint32_t acc0 = first ? 0u : 1u;
+                                const uint32_t acc0 = SPLIT ? (first ? 0u : 1u) : ((c | gi | ti) != 0);
 #pragma unroll
                                 for (int u = 0; u < TPS; ++u) {
                                     if (u < ntp) {
@@ -871,7 +871,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                                 commit(&empty_bar[stage]);
                             }
                             __syncwarp();
-                            first = false;
+                            if constexpr (SPLIT) first = false;
                             if (++stage == p.stages) { stage = 0; phase ^= 1; }
                             poll_norm();
                         }
@@ -880,16 +880,24 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         if (++hs == p.halo_slots) { hs = 0; hphase ^= 1; }
                     }
             };
-            const bool fast_halo = p.halo && !p.wres && (p.tps == 2 || p.tps == 3);
+            const bool fast_halo = !kL1 && p.halo && !p.wres && (p.tps == 2 || p.tps == 3);
+            if constexpr (kL1) {
+                // (fused L1: the plain K loop below)
+            }
             if (fast_halo) {
                 using I2 = std::integral_constant<int, 2>;
                 using I3 = std::integral_constant<int, 3>;
                 using BT = std::integral_constant<bool, true>;
                 using BF = std::integral_constant<bool, false>;
                 const bool lo_mma = p.split == 2 && !p.a_hi_only;
-                if (p.tps == 2) { if (lo_mma) halo_fast(I2{}, BT{}); else halo_fast(I2{}, BF{}); }
-                else { if (lo_mma) halo_fast(I3{}, BT{}); else halo_fast(I3{}, BF{}); }
-            } else if (p.halo) {
+                if (kSplitK && p.ksplit > 1) {
+                    if (p.tps == 2) { if (lo_mma) halo_fast(I2{}, BT{}, BT{}); else halo_fast(I2{}, BF{}, BT{}); }
+                    else { if (lo_mma) halo_fast(I3{}, BT{}, BT{}); else halo_fast(I3{}, BF{}, BT{}); }
+                } else {
+                    if (p.tps == 2) { if (lo_mma) halo_fast(I2{}, BT{}, BF{}); else halo_fast(I2{}, BF{}, BF{}); }
+                    else { if (lo_mma) halo_fast(I3{}, BT{}, BF{}); else halo_fast(I3{}, BF{}, BF{}); }
+                }
+            } else if (!kL1 && p.halo) {
                 const uint32_t sbo = (uint32_t)p.halo_w * 128;
                 const bool lo_mma = p.split == 2 && !p.a_hi_only;
                 for (int c = 0; c < p.kchunks; ++c)
@@ -1000,22 +1008,12 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
 
             if (g2) {
                 g2_committed = it + 1;
-                poll_norm();
             } else if (kGdn) {
                 // the previous tile's norm must be issued before this one becomes pending
                 if (pend) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
                 pend = 1;
                 pend_it = it;
                 pend_dcol = (uint32_t)(buf * p.acc_stride);
-            }
-        }
-        if (g2 && p.g2_mma_norm && leader) {
-            while (g2_nn < g2_committed) {
-                mbar_wait(&xsq2_bar[g2_nn & 1], (uint32_t)(g2_nn >> 1) & 1u);
-                pend_dcol = (uint32_t)((g2_nn & 1) * p.acc_stride);
-                pend_it = g2_nn;
-                issue_norm(&norm2_bar[g2_nn & 1]);
-                ++g2_nn;
             }
         }
         if (kGdn && !g2 && pend && leader) { mbar_wait(xsq_bar, xsq_phase); xsq_phase ^= 1; ++xsq_seen; issue_norm(norm_bar); }
@@ -1098,7 +1096,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 constexpr bool kOneDN = decltype(onedn_c)::value, kFwd = decltype(fwd_c)::value;
                 int it = gr;
                 for (int t = cid + gr * ncl; t < p.total_tiles; t += 2 * ncl, it += 2) {
-                    const TileCoord tc = decode_tile(p, t, rank);
+                    const TileCoord tc = decode_tile<kSplitK>(p, t, rank);
                     const uint32_t par = (uint32_t)(it >> 1) & 1u;
                     const bool tma_ok = p.nphase == 1 || tc.gy0 + ty0 + 32 / (p.Wt < 32 ? p.Wt : 32) <= p.Hg;
                     const bool slow = !tma_ok || p.out_f32 != nullptr;
@@ -1163,7 +1161,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         else mbar_arrive(&xsq2_bar[gr]);
                     }
                     if (threadIdx.x == lead) LIC_TRACE(it, T_EPI_XSQ);
-                    if (leader && threadIdx.x == lead && !p.g2_mma_norm) {
+                    if (leader && threadIdx.x == lead) {
                         // every warp of the group (both CTAs) has written v: issue norm = v . gamma^T
                         // from here (a blocking wait: the MMA warp keeps issuing main loops meanwhile)
                         if (!gamma_ok) { mbar_wait(gamma_bar, 0); gamma_ok = true; }
@@ -1304,7 +1302,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             else { if (p.ep == EP_GDN) body(F_{}, T_{}); else body(F_{}, F_{}); }
         }
         for (int t = g2 ? p.total_tiles : cid; t < p.total_tiles; t += ncl, ++it) {
-            TileCoord tc = decode_tile(p, t, rank);
+            TileCoord tc = decode_tile<kSplitK>(p, t, rank);
             const int buf = (p.n_accbuf == 2) ? (it & 1) : 0;
             const uint32_t use = (p.n_accbuf == 2) ? (uint32_t)(it >> 1) : (uint32_t)it;
             // one lane waits on the mbarrier, the other epilogue warps sleep in a hardware
@@ -1636,7 +1634,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         for (int j = 0; j < GC; ++j) direct16(x[j], g * G + j * 16);
                     }
                 }
-            } else if (p.gather) {
+            } else if (!kL1 && p.gather) {
                 // ---- gather mode (g_s L4): P[p][t][0..11] -> smem, then each output sums its 9
                 // neighbours' slices.  Column chunk t (16 wide) of the accumulator = offset t.
                 const uint32_t gp = smem_u32(smem + p.off_gp);
@@ -1862,13 +1860,13 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     }
 }
 
-template <int GC, int CG>
+template <int GC, int CG, bool L1>
 static cudaError_t launch_t(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
                             const CUtensorMap& mapOH, const CUtensorMap& mapOL, const CUtensorMap& mapO2,
                             const CUtensorMap& mapO3, const ConvParams& p, int grid, cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<GC, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<GC, CG, L1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return e;
         attr_set = true;
@@ -1894,27 +1892,24 @@ static cudaError_t launch_t(const CUtensorMap& mapA, const CUtensorMap& mapB, co
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, conv_umma_kernel<GC, CG>, mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p);
+    return cudaLaunchKernelEx(&cfg, conv_umma_kernel<GC, CG, L1>, mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p);
 }
 
 cudaError_t launch_conv_umma(const CUtensorMap& mapA, const CUtensorMap& mapB, const CUtensorMap& mapG,
                              const CUtensorMap& mapOH, const CUtensorMap& mapOL, const CUtensorMap& mapO2,
                              const CUtensorMap& mapO3, const ConvParams& p, int grid, cudaStream_t stream) {
     const bool gdn = (p.ep == EP_GDN || p.ep == EP_IGDN);
+#define LIC_LAUNCH(G, C, L) launch_t<G, C, L>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream)
+    if (!gdn) return p.fuse_l1 ? cudaErrorInvalidValue : (p.cg == 2 ? LIC_LAUNCH(0, 2, false) : LIC_LAUNCH(0, 1, false));
+    // GDN channel counts of the configs: N = 128, 192
+    if (p.BN != 128 && p.BN != 192) return cudaErrorInvalidValue;
     if (p.cg == 2) {
-        if (!gdn) return launch_t<0, 2>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
-        switch (p.BN) {
-        case 128: return launch_t<2, 2>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
-        case 192: return launch_t<3, 2>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
-        default: return cudaErrorInvalidValue;
-        }
+        if (p.BN == 128) return p.fuse_l1 ? LIC_LAUNCH(2, 2, true) : LIC_LAUNCH(2, 2, false);
+        return p.fuse_l1 ? LIC_LAUNCH(3, 2, true) : LIC_LAUNCH(3, 2, false);
     }
-    if (!gdn) return launch_t<0, 1>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
-    switch (p.BN) {      // GDN channel counts of the configs: N = 128, 192
-    case 128: return launch_t<2, 1>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
-    case 192: return launch_t<3, 1>(mapA, mapB, mapG, mapOH, mapOL, mapO2, mapO3, p, grid, stream);
-    default: return cudaErrorInvalidValue;
-    }
+    if (p.BN == 128) return p.fuse_l1 ? LIC_LAUNCH(2, 1, true) : LIC_LAUNCH(2, 1, false);
+    return p.fuse_l1 ? LIC_LAUNCH(3, 1, true) : LIC_LAUNCH(3, 1, false);
+#undef LIC_LAUNCH
 }
 
 }  // namespace lic

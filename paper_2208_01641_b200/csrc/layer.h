@@ -130,7 +130,6 @@ struct ConvParams {
     int ksplit;
     int ksplit_ok;                    // host: the layer may be split (run_layer picks ksplit from the batch)
     float* part;                      // EP_PARTIAL: fp32 [ksplit][batch][Hout][Wout][Cout]
-    int g2_mma_norm;                  // g2: the MMA warp issues the norm MMAs between its stages (halo layers)
     int mma_spin;                     // g2: the MMA warp polls its operand barriers (test_wait loop) instead
                                       // of a suspending try_wait
     // gather mode (g_s L4, stride-2 transposed conv N -> 3): the 9 input offsets go into N instead
