@@ -183,6 +183,7 @@ struct lic_codec {
     int raw_tma_enabled = 1;       // u8 frames: raw patches by TMA (env LIC_RAW_TMA=0: cp.async)
     int ksplit_enabled = 1;        // split-K for the few-tile h layers (env LIC_KSPLIT=0: off, =2/3/4: at most that many slices)
     int ksplit_force = 0;
+    int g2_192 = 1;                // two-group epilogue also for BN = 192 (chunked norm; env LIC_G2_192=0: off)
     int mma_spin = 0;              // g2 halo layers: MMA warp spins on operand barriers (env LIC_MMA_SPIN=1)
     int l1_stage_split = 1;        // u8 frames: hi-only A stages, twice as many (env LIC_L1_STAGES=0: off)
     int g2_enabled = 2;            // two-group GDN epilogue: 1 g_a L1 only, 2 every BN = 128 GDN layer (env LIC_G2)
@@ -650,26 +651,30 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     }
     if (P.smem_bytes < 120 * 1024) P.smem_bytes = 120 * 1024;     // one CTA per SM (TMEM)
     if (P.smem_bytes > budget) return fail(c, LIC_EINVAL, "layer plan exceeds shared memory (%u)", P.smem_bytes);
-    // TMEM plan: accumulator (+ GDN norm) per buffer, double-buffered when it fits
-    int per = std::max(32, P.BN) + (gdn ? P.BN : 0);
+    // two-group GDN epilogue (env LIC_G2: 0 off, 1 g_a L1 only, 2 every eligible GDN
+    // layer): BN = 128, or BN = 192 with the norm in three 64-column chunks; needs 64 KB of
+    // per-warp output staging (4 KB, 32-channel rounds)
+    P.g2 = 0;
+    if (gdn && (P.BN == 128 || (P.BN == 192 && c->g2_192)) && tma_out && P.ostage_slots == 2 && c->wstage_enabled &&
+        (gemm_l1 ? c->g2_enabled >= 1 : c->g2_enabled >= 2))
+        P.g2 = 1;
+    // TMEM plan: accumulator (+ GDN norm) per buffer, double-buffered when it fits (two-group
+    // BN = 192: 192 + one 64-column norm chunk)
+    int per = std::max(32, P.BN) + (gdn ? (P.g2 && P.BN == 192 ? 64 : P.BN) : 0);
     P.n_accbuf = (2 * per <= 512) ? 2 : 1;
     P.acc_stride = per;
     P.tmem_cols = pow2_cols(P.n_accbuf * per);
+    if (P.g2 && P.n_accbuf != 2) P.g2 = 0;
     // per-warp staging of the GDN / IGDN epilogue when 64 KB of staging fit: rounds of 32 channels
-    // (BN = 128: one round, one 4 KB slot per warp) or 16 (BN = 192: three rounds, two 2 KB slots)
+    // (BN = 128: one round, one 4 KB slot per warp; two-group: one round per 32-channel sub-block)
+    // or 16 (BN = 192 single group: three rounds, two 2 KB slots)
     P.wst_ch = 0;
     P.wst_slots = 0;
     if (gdn && tma_out && P.ostage_slots == 2 && c->wstage_enabled) {
         const int G = P.BN / 4;                                         // channels per epilogue warp
-        P.wst_ch = (G % 32 == 0) ? 32 : 16;
+        P.wst_ch = (G % 32 == 0 || P.g2) ? 32 : 16;
         P.wst_slots = P.wst_ch == 32 ? 1 : 2;
     }
-    // two-group GDN epilogue (env LIC_G2=0: off): the fused g_a L1, whose tiles are short (K = 80)
-    // and whose time is the GDN epilogue's
-    P.g2 = 0;
-    if (gdn && P.BN == 128 && P.wst_ch == 32 && P.wst_slots == 1 && P.n_accbuf == 2 && P.tma_out &&
-        (gemm_l1 ? c->g2_enabled >= 1 : c->g2_enabled >= 2))
-        P.g2 = 1;
     P.mma_spin = (P.g2 && !gemm_l1 && c->mma_spin) ? 1 : 0;
     {
         // split-K candidates: the h layers with a handful of tiles (h_a L2, L3, h_s L1), whose
@@ -1009,6 +1014,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_L1_STAGES")) c->l1_stage_split = (e[0] != '0');
     if (const char* e = std::getenv("LIC_RAW_TMA")) c->raw_tma_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_MMA_SPIN")) c->mma_spin = (e[0] == '1');
+    if (const char* e = std::getenv("LIC_G2_192")) c->g2_192 = (e[0] != '0');
     if (const char* e = std::getenv("LIC_KSPLIT")) { c->ksplit_enabled = atoi(e) != 0; c->ksplit_force = atoi(e) > 1 ? atoi(e) : 0; }
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');

@@ -312,7 +312,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
     constexpr bool kSplitK = GC == 0 && !L1; // split-K layers are ReLU / z-quantise layers
     // two-group GDN epilogue (BN = 128): epilogue warps 4-11 take the even tiles of this CTA,
     // 12-19 the odd ones, each warp 32 pixels x 64 channels; the groups' norm round trips overlap
-    const bool g2 = GC == 2 && p.g2;
+    const bool g2 = (GC == 2 || GC == 3) && p.g2;
     const uint32_t epi_arrivals = (g2 ? kEpiWarps / 2 : kEpiWarps) * CG;   // per tile
     const int rank = CG == 2 ? (int)cluster_ctarank() : 0;
     const bool leader = rank == 0;
@@ -781,9 +781,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         int g2_committed = 0;
         (void)g2_committed;
         auto poll_norm = [&]() {       // cheap volatile smem read; the mbarrier wait then completes at once
-            if constexpr (GC == 2) {
-                if (g2) return;                              // the epilogue issues its own norm MMAs
-            }
+            if (g2) return;                                  // the epilogue issues its own norm MMAs
             if (kGdn && pend && *reinterpret_cast<volatile uint32_t*>(xsq_cnt) >= (uint32_t)(kEpiWarps * CG * (xsq_seen + 1))) {
                 mbar_wait(xsq_bar, xsq_phase);
                 xsq_phase ^= 1;
@@ -1074,7 +1072,13 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         // y = x / sqrt(n) = sign v rsqrt(v n) 2^k (GDN), sign (v n) rsqrt(v n) 2^k (IGDN), one MUFU
         // op per value, and no register holds x across the norm round trip, during which the other
         // group works.
-        if constexpr (GC == 2) if (g2) {
+        if constexpr (GC == 2 || GC == 3) if (g2) {
+            // NSUB 32-channel sub-blocks per thread (BN = 64 NSUB); BN = 192: the norm is computed in
+            // three 64-column N chunks (chunk j = sub-block j of both channel halves: gamma rows 32j..
+            // of each CTA's half), so a buffer is 192 accumulator + 64 norm columns and two fit in TMEM
+            constexpr int NSUB = GC;
+            constexpr bool kChunked = NSUB == 3;
+            constexpr int CPT = 32 * NSUB;                            // channels per thread
             const int gr = (warp - 4) >> 3;
             const int h = ((warp - 4) >> 2) & 1;
             const int lead = 128 + gr * 256;                          // the group's first thread
@@ -1085,19 +1089,55 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const uint32_t rowa = smem_u32(smem) + p.off_ostage + (uint32_t)(warp - 4) * 4096u + (uint32_t)lane * 64u;
             const uint32_t sw = ((uint32_t)lane >> 1) & 3u;           // 64B swizzle of this row
             const int ty0 = (q * 32) >> p.wt_log2, tx0 = (q * 32) & (p.Wt - 1);
-            const uint32_t tcol0 = tmem_base + lane_off + (uint32_t)(gr * p.acc_stride) + (uint32_t)(h * 64);
-            const int c0 = h * 64;                                     // first channel of this thread (one N tile)
+            const uint32_t tbuf = tmem_base + lane_off + (uint32_t)(gr * p.acc_stride);
+            const uint32_t tcol0 = tbuf + (uint32_t)(h * CPT);
+            // this thread's norm columns: the whole norm region (NSUB = 2) or its 32 of a chunk's 64
+            const uint32_t tnorm = kChunked ? tbuf + (uint32_t)p.BN + (uint32_t)(32 * h) : tcol0 + (uint32_t)p.BN;
+            const int c0 = h * CPT;                                    // first channel of this thread (one N tile)
             bool gamma_ok = false;                                     // (the norm-issuing thread) gamma landed
             // |bias| bound of this thread's channels: max |x| <= max |acc| s255 + bmax (the exponent
             // below is taken from this bound, so the accumulator is read once before the exchange)
             float bmax = 0.0f;
-            for (int i = 0; i < 64; ++i) bmax = fmaxf(bmax, fabsf(s_bias[c0 + i]));
+            for (int i = 0; i < CPT; ++i) bmax = fmaxf(bmax, fabsf(s_bias[c0 + i]));
+            // norm MMAs of chunk j (all of them for NSUB = 2), issued by the leader's group-lead thread
+            auto issue_norm_g2 = [&](int j) {
+                const uint32_t dcol = (uint32_t)(gr * p.acc_stride);
+                const uint32_t ncol = tmem_base + dcol + (uint32_t)p.BN;
+                const uint32_t gbase = smem_u32(smem + p.off_gamma) + (kChunked ? (uint32_t)(j * 32 * 128) : 0u);
+                const uint32_t nn = kChunked ? 64u : (uint32_t)p.BN;
+                const uint32_t idesc_n = idesc_f16_f32(kBM * CG, nn);
+#pragma unroll
+                for (int kk = 0; kk < 4 * NSUB; ++kk) {   // K = BN in steps of 16 (G = 32 layout)
+                    const int k0 = 16 * kk, gg = k0 / 32, o = k0 - gg * 32;
+                    const uint32_t ahi = tmem_base + dcol + gg * 32 + o / 2;
+                    const uint64_t bd = sdesc_sw128(gbase + (k0 / 64) * (uint32_t)((p.BN / CG) * kBK * 2)) + 2 * (kk & 3);
+                    if constexpr (CG == 2) {
+                        umma_f16_ts_cg2(ncol, ahi, bd, idesc_n, kk != 0);
+                        umma_f16_ts_cg2(ncol, ahi + 16, bd, idesc_n, 1u);
+                    } else {
+                        umma_f16_ts(ncol, ahi, bd, idesc_n, kk != 0);
+                        umma_f16_ts(ncol, ahi + 16, bd, idesc_n, 1u);
+                    }
+                }
+                if constexpr (CG == 2) umma_commit_pair(&norm2_bar[gr]); else umma_commit(&norm2_bar[gr]);
+            };
+            auto arrive_group = [&]() {          // this warp is done with v / the norm chunk (leader's barrier)
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2) mbar_arrive_cluster(lbar(&xsq2_bar[gr]));
+                    else mbar_arrive(&xsq2_bar[gr]);
+                }
+            };
             auto body = [&](auto onedn_c, auto fwd_c) {
                 constexpr bool kOneDN = decltype(onedn_c)::value, kFwd = decltype(fwd_c)::value;
                 int it = gr;
                 for (int t = cid + gr * ncl; t < p.total_tiles; t += 2 * ncl, it += 2) {
                     const TileCoord tc = decode_tile<kSplitK>(p, t, rank);
                     const uint32_t par = (uint32_t)(it >> 1) & 1u;
+                    // barrier phases per tile: xsq2 / norm2 complete once per tile (NSUB = 2) or once
+                    // per norm chunk (3 per tile): phase number ph0 + j
+                    const uint32_t ph0 = kChunked ? 3u * (uint32_t)(it >> 1) : (uint32_t)(it >> 1);
                     const bool tma_ok = p.nphase == 1 || tc.gy0 + ty0 + 32 / (p.Wt < 32 ? p.Wt : 32) <= p.Hg;
                     const bool slow = !tma_ok || p.out_f32 != nullptr;
                     if (threadIdx.x == lead) mbar_wait(&tfull_bar[gr], par);
@@ -1109,7 +1149,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     uint32_t xr[32];
                     float amax = 0.0f;
 #pragma unroll 1
-                    for (int s = 0; s < 2; ++s) {
+                    for (int s = 0; s < NSUB; ++s) {
                         tmem_ld32_nw(tcol0 + 32 * s, xr);
                         tmem_ld_wait_dep32(xr);
 #pragma unroll
@@ -1123,9 +1163,9 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     // GDN: v = x^2 2^-2k, k = E - 6 -> v < 2^14; 1DN: v = |x| 2^-k, k = E - 13 -> v < 2^14
                     const int k = kOneDN ? min(max(E - 13, -100), 100) : min(max(E - 6, -50), 50);
                     const float sc_dn = __int_as_float((127 - k) << 23);          // 2^-k
-                    uint32_t sg0 = 0u, sg1 = 0u;                             // sign bits (bit 31 = channel 32s)
+                    uint32_t sg0 = 0u, sg1 = 0u, sg2 = 0u;                   // sign bits (bit 31 = channel 32s)
 #pragma unroll 1
-                    for (int s = 0; s < 2; ++s) {
+                    for (int s = 0; s < NSUB; ++s) {
                         tmem_ld32_nw(tcol0 + 32 * s, xr);
                         tmem_ld_wait_dep32(xr);
                         uint32_t hv[16], lv[16];
@@ -1145,7 +1185,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             split2(v[0], v[1], hv[2 * i4], lv[2 * i4]);
                             split2(v[2], v[3], hv[2 * i4 + 1], lv[2 * i4 + 1]);
                         }
-                        if (s) sg1 = sgs; else sg0 = sgs;
+                        if (s == 0) sg0 = sgs; else if (s == 1) sg1 = sgs; else sg2 = sgs;
                         // the G = 32 layout of the norm MMA: hi of channel 32s + j at column 32s + j/2, lo at 32s + 16 + j/2
                         const uint32_t ts = tcol0 + 32u * (uint32_t)s;
                         tmem_st8(ts, hv);
@@ -1154,50 +1194,33 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         tmem_st8(ts + 24, lv + 8);
                     }
                     tmem_st_wait();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if constexpr (CG == 2) mbar_arrive_cluster(lbar(&xsq2_bar[gr]));
-                        else mbar_arrive(&xsq2_bar[gr]);
-                    }
+                    arrive_group();
                     if (threadIdx.x == lead) LIC_TRACE(it, T_EPI_XSQ);
                     if (leader && threadIdx.x == lead) {
                         // every warp of the group (both CTAs) has written v: issue norm = v . gamma^T
                         // from here (a blocking wait: the MMA warp keeps issuing main loops meanwhile)
                         if (!gamma_ok) { mbar_wait(gamma_bar, 0); gamma_ok = true; }
-                        mbar_wait(&xsq2_bar[gr], par);
+                        mbar_wait(&xsq2_bar[gr], ph0 & 1u);
                         tc_fence_after();
-                        const uint32_t dcol = (uint32_t)(gr * p.acc_stride);
-                        const uint32_t ncol = tmem_base + dcol + (uint32_t)p.BN;
-                        const uint32_t gbase = smem_u32(smem + p.off_gamma);
-                        const uint32_t idesc_n = idesc_f16_f32(kBM * CG, (uint32_t)p.BN);
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) {          // K = BN = 128 in steps of 16 (G = 32 layout)
-                            const int k0 = 16 * kk, gg = k0 / 32, o = k0 - gg * 32;
-                            const uint32_t ahi = tmem_base + dcol + gg * 32 + o / 2;
-                            const uint64_t bd = sdesc_sw128(gbase + (k0 / 64) * (uint32_t)((p.BN / CG) * kBK * 2)) + 2 * (kk & 3);
-                            if constexpr (CG == 2) {
-                                umma_f16_ts_cg2(ncol, ahi, bd, idesc_n, kk != 0);
-                                umma_f16_ts_cg2(ncol, ahi + 16, bd, idesc_n, 1u);
-                            } else {
-                                umma_f16_ts(ncol, ahi, bd, idesc_n, kk != 0);
-                                umma_f16_ts(ncol, ahi + 16, bd, idesc_n, 1u);
-                            }
-                        }
-                        if constexpr (CG == 2) umma_commit_pair(&norm2_bar[gr]); else umma_commit(&norm2_bar[gr]);
+                        issue_norm_g2(0);
                     }
-                    // ---- wait for the norm MMAs of this tile
-                    if (threadIdx.x == lead) mbar_wait(&norm2_bar[gr], par);
-                    named_bar_sync(bar_norm, 256);
-                    tc_fence_after();
+                    // ---- wait for the norm MMAs of this tile (NSUB = 3: of chunk 0; later chunks in P2)
+                    auto wait_norm = [&](int j) {
+                        if (threadIdx.x == lead) mbar_wait(&norm2_bar[gr], (ph0 + (uint32_t)j) & 1u);
+                        named_bar_sync(bar_norm, 256);
+                        tc_fence_after();
+                    };
+                    wait_norm(0);
                     if (threadIdx.x == lead) LIC_TRACE(it, T_EPI_NORM);
                     // n = beta + c 2^(2k) (GDN) / beta + c 2^k (1DN), c the contraction of v
                     const float sc_up = kOneDN ? __int_as_float((127 + k) << 23) : __int_as_float((127 + 2 * k) << 23);
                     const float sc_k = __int_as_float((127 + k) << 23);       // |x| = sqrt(v) 2^k (GDN), v 2^k (1DN)
-                    // ---- P2: 4 pieces of 16 channels; pieces 2s, 2s + 1 form staging round s (32 channels)
+                    // ---- P2: 2 NSUB pieces of 16 channels; pieces 2s, 2s + 1 form staging round s (32
+                    // channels) -- and, chunked, norm chunk s
 #pragma unroll 1
-                    for (int pc = 0; pc < 4; ++pc) {
+                    for (int pc = 0; pc < 2 * NSUB; ++pc) {
                         const int j = pc & 1;
+                        if (kChunked && j == 0 && pc > 0) wait_norm(pc >> 1);
                         if (j == 0) {
                             if (lane == 0) bulk_wait_read0();              // this warp's slot is free again
                             __syncwarp();
@@ -1206,9 +1229,19 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         const uint32_t ts = tcol0 + 32u * (uint32_t)(pc >> 1) + 8u * (uint32_t)j;
                         tmem_ld8_nw(ts, vh);
                         tmem_ld8_nw(ts + 16, vl);
-                        tmem_ld16_nw(tcol0 + (uint32_t)p.BN + 16u * (uint32_t)pc, nr);
+                        tmem_ld16_nw(kChunked ? tnorm + 16u * (uint32_t)j : tnorm + 16u * (uint32_t)pc, nr);
                         tmem_ld_wait_dep(vh, vl, nr);
-                        if (pc == 3) {
+                        if (kChunked && j == 1 && pc < 2 * NSUB - 1) {
+                            // this warp has read norm chunk s: the lead thread may overwrite the region
+                            // with chunk s + 1 once every warp of the group (both CTAs) has
+                            arrive_group();
+                            if (leader && threadIdx.x == lead) {
+                                mbar_wait(&xsq2_bar[gr], (ph0 + (uint32_t)(pc >> 1) + 1u) & 1u);
+                                tc_fence_after();
+                                issue_norm_g2((pc >> 1) + 1);
+                            }
+                        }
+                        if (pc == 2 * NSUB - 1) {
                             // every TMEM read of this tile is complete: release the buffer
                             tc_fence_before();
                             __syncwarp();
@@ -1217,7 +1250,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                                 else mbar_arrive(&tempty_bar[gr]);
                             }
                         }
-                        const uint32_t sgp = ((pc >> 1) ? sg1 : sg0) << (16 * j);          // bit 31 = this piece's channel 0
+                        const uint32_t sgw = (pc >> 1) == 0 ? sg0 : (pc >> 1) == 1 ? sg1 : sg2;
+                        const uint32_t sgp = sgw << (16 * j);          // bit 31 = this piece's channel 0
                         float y[16];
 #pragma unroll
                         for (int i4 = 0; i4 < 4; ++i4) {
@@ -1279,7 +1313,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             fence_proxy_async_smem();
                             __syncwarp();
                             if (lane == 0) {
-                                if (threadIdx.x == lead) LIC_TRACE(it, pc == 3 ? T_EPI_ACQ : T_EPI_P2);
+                                if (threadIdx.x == lead) LIC_TRACE(it, pc == 2 * NSUB - 1 ? T_EPI_ACQ : T_EPI_P2);
                                 const uint8_t* hs = smem + p.off_ostage + (uint32_t)(warp - 4) * 4096u;
                                 const int cb = tc.nt * p.BN + c0 + 32 * (pc >> 1);
                                 if (p.nphase == 1) {
@@ -1290,7 +1324,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                                     tma_store_4d(om, hs, cb, tc.gx0 + tx0, tc.b * p.Hg + tc.gy0 + ty0, 0);
                                 }
                                 bulk_commit();
-                                if (threadIdx.x == lead) LIC_TRACE(it, pc == 3 ? T_EPI_END : T_EPI_STAGED);
+                                if (threadIdx.x == lead) LIC_TRACE(it, pc == 2 * NSUB - 1 ? T_EPI_END : T_EPI_STAGED);
                             }
                         }
                     }

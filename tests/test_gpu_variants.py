@@ -94,3 +94,34 @@ def test_gdn_epilogue_variants_vs_oracle(lic, data, g2):
         ref = O.decode_frame(p["y_sym"], w, True, crop, H, W)
         ex = check_float(r["xh"][f], ref, what=f"G2={g2} x-hat")
         print(f"G2={g2} frame {f}: y max-abs {ey:.2e}, x-hat max-abs {ex:.2e}")
+
+
+@pytest.mark.parametrize("g2_192", [0, 1])
+def test_n192_two_group_chunked_norm_vs_oracle(lic, g2_192):
+    """N = 192 codec (C4 / C5 shapes): the two-group epilogue with the norm in three 64-column
+    chunks (LIC_G2_192=1) and the single-group one both meet the oracle bars."""
+    spec = ModelSpec(kind=1, N=192, M=320)
+    Hh, Ww = 128, 192
+    w = generate_weights(spec, seed=0)
+    fr = synth_frames_u8(1, Hh, Ww, seed=23)
+    x = u8_to_f32_chw(fr)
+    xp, crop = O.pad_chw(x[0], hyper=True)
+    pl = O.encode_planes(xp, w, True, 32)
+    with env(LIC_G2_192=g2_192):
+        c = lic.Codec(write_licw(spec, w), Hh, Ww, max_batch=1)
+    try:
+        ys = np.empty((1,) + c.y_shape, np.int8)
+        yi = np.empty((1,) + c.y_shape, np.uint8)
+        zs = np.empty((1,) + c.z_shape, np.int8)
+        c.set_debug(True)
+        c.encode(np.ascontiguousarray(fr), ys, yi, zs, u8=True)
+        y, _, _ = c.debug_latents(1)
+        ey = check_float(y[0], pl["y"], what=f"N=192 G2_192={g2_192} y")
+        check_symbols(ys[0], pl["y_sym"], pl["y"], what="N=192 y_sym")
+        xh = np.empty((1, 3, Hh, Ww), np.float32)
+        c.decode(pl["y_sym"][None], xh)
+        ref = O.decode_frame(pl["y_sym"], w, True, crop, Hh, Ww)
+        ex = check_float(xh[0], ref, what=f"N=192 G2_192={g2_192} x-hat")
+        print(f"N=192 G2_192={g2_192}: y max-abs {ey:.2e}, x-hat max-abs {ex:.2e}")
+    finally:
+        c.close()
