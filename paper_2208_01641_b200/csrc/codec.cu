@@ -183,6 +183,7 @@ struct lic_codec {
     int raw_tma_enabled = 1;       // u8 frames: raw patches by TMA (env LIC_RAW_TMA=0: cp.async)
     int ksplit_enabled = 1;        // split-K for the few-tile h layers (env LIC_KSPLIT=0: off, =2/3/4: at most that many slices)
     int ksplit_force = 0;
+    int g2_slot16 = 1;             // two-group epilogue also with 32 KB of staging (16-channel rounds; env LIC_G2_SLOT16=0: off)
     int g2_192 = 1;                // two-group epilogue also for BN = 192 (chunked norm; env LIC_G2_192=0: off)
     int mma_spin = 0;              // g2 halo layers: MMA warp spins on operand barriers (env LIC_MMA_SPIN=1)
     int l1_stage_split = 1;        // u8 frames: hi-only A stages, twice as many (env LIC_L1_STAGES=0: off)
@@ -655,8 +656,8 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     // layer): BN = 128, or BN = 192 with the norm in three 64-column chunks; needs 64 KB of
     // per-warp output staging (4 KB, 32-channel rounds)
     P.g2 = 0;
-    if (gdn && (P.BN == 128 || (P.BN == 192 && c->g2_192)) && tma_out && P.ostage_slots == 2 && c->wstage_enabled &&
-        (gemm_l1 ? c->g2_enabled >= 1 : c->g2_enabled >= 2))
+    if (gdn && (P.BN == 128 || (P.BN == 192 && c->g2_192)) && tma_out && c->wstage_enabled &&
+        (P.ostage_slots == 2 || c->g2_slot16) && (gemm_l1 ? c->g2_enabled >= 1 : c->g2_enabled >= 2))
         P.g2 = 1;
     // TMEM plan: accumulator (+ GDN norm) per buffer, double-buffered when it fits (two-group
     // BN = 192: 192 + one 64-column norm chunk)
@@ -674,6 +675,10 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         const int G = P.BN / 4;                                         // channels per epilogue warp
         P.wst_ch = (G % 32 == 0 || P.g2) ? 32 : 16;
         P.wst_slots = P.wst_ch == 32 ? 1 : 2;
+    } else if (P.g2) {
+        // two-group epilogue with 32 KB of staging: one 2 KB slot per warp, 16-channel rounds
+        P.wst_ch = 16;
+        P.wst_slots = 1;
     }
     P.mma_spin = (P.g2 && !gemm_l1 && c->mma_spin) ? 1 : 0;
     {
@@ -1015,6 +1020,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_RAW_TMA")) c->raw_tma_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_MMA_SPIN")) c->mma_spin = (e[0] == '1');
     if (const char* e = std::getenv("LIC_G2_192")) c->g2_192 = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_G2_SLOT16")) c->g2_slot16 = (e[0] != '0');
     if (const char* e = std::getenv("LIC_KSPLIT")) { c->ksplit_enabled = atoi(e) != 0; c->ksplit_force = atoi(e) > 1 ? atoi(e) : 0; }
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');

@@ -1086,8 +1086,14 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const uint32_t bar_px = 5u + (uint32_t)(gr * 4 + q);      // the pixel's two channel halves
             const float s255 = p.l1_int ? (1.0f / 255.0f) : 1.0f;
             const uint32_t xe_a = s_xe + (uint32_t)(gr * 512) + 4u * (uint32_t)r;
-            const uint32_t rowa = smem_u32(smem) + p.off_ostage + (uint32_t)(warp - 4) * 4096u + (uint32_t)lane * 64u;
-            const uint32_t sw = ((uint32_t)lane >> 1) & 3u;           // 64B swizzle of this row
+            // per-warp output staging slot: rounds of wst = 32 (4 KB slots, 64-byte rows, 64B swizzle)
+            // or 16 channels (2 KB slots, 32-byte rows, 32B swizzle: layers with 32 KB of staging)
+            const bool w32 = p.wst_ch == 32;
+            const uint32_t rows_b = w32 ? 64u : 32u, slot_b = 32u * rows_b * 2u, lo_off = 32u * rows_b;
+            const uint32_t sw_mask = rows_b / 16u - 1u;
+            const uint32_t slot_off = p.off_ostage + (uint32_t)(warp - 4) * slot_b;
+            const uint32_t rowa = smem_u32(smem) + slot_off + (uint32_t)lane * rows_b;
+            const uint32_t sw = (((uint32_t)lane * rows_b) >> 7) & sw_mask;     // swizzle of this row
             const int ty0 = (q * 32) >> p.wt_log2, tx0 = (q * 32) & (p.Wt - 1);
             const uint32_t tbuf = tmem_base + lane_off + (uint32_t)(gr * p.acc_stride);
             const uint32_t tcol0 = tbuf + (uint32_t)(h * CPT);
@@ -1221,7 +1227,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     for (int pc = 0; pc < 2 * NSUB; ++pc) {
                         const int j = pc & 1;
                         if (kChunked && j == 0 && pc > 0) wait_norm(pc >> 1);
-                        if (j == 0) {
+                        if (j == 0 || !w32) {
                             if (lane == 0) bulk_wait_read0();              // this warp's slot is free again
                             __syncwarp();
                         }
@@ -1305,17 +1311,17 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             const float* v8 = y + 8 * kk;
                             split2(v8[0], v8[1], hq.x, lq.x); split2(v8[2], v8[3], hq.y, lq.y);
                             split2(v8[4], v8[5], hq.z, lq.z); split2(v8[6], v8[7], hq.w, lq.w);
-                            const uint32_t o = ((((uint32_t)(2 * j + kk)) ^ sw) & 3u) << 4;
+                            const uint32_t o = ((((uint32_t)((w32 ? 2 * j : 0) + kk)) ^ sw) & sw_mask) << 4;
                             stsu4(rowa + o, hq);
-                            stsu4(rowa + 2048u + o, lq);
+                            stsu4(rowa + lo_off + o, lq);
                         }
-                        if (j == 1) {
+                        if (j == 1 || !w32) {
                             fence_proxy_async_smem();
                             __syncwarp();
                             if (lane == 0) {
                                 if (threadIdx.x == lead) LIC_TRACE(it, pc == 2 * NSUB - 1 ? T_EPI_ACQ : T_EPI_P2);
-                                const uint8_t* hs = smem + p.off_ostage + (uint32_t)(warp - 4) * 4096u;
-                                const int cb = tc.nt * p.BN + c0 + 32 * (pc >> 1);
+                                const uint8_t* hs = smem + slot_off;
+                                const int cb = tc.nt * p.BN + c0 + (w32 ? 32 * (pc >> 1) : 16 * pc);
                                 if (p.nphase == 1) {
                                     tma_store_5d(&mapOH, hs, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b, 0);
                                 } else {
