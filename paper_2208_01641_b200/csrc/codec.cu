@@ -1025,7 +1025,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
-    if (const char* e = std::getenv("LIC_SMALL_BN")) c->small_bn = atoi(e) == 64 || atoi(e) == 128 ? atoi(e) : 0;
+    if (const char* e = std::getenv("LIC_SMALL_BN")) c->small_bn = atoi(e) == 64 || atoi(e) == 96 || atoi(e) == 128 ? atoi(e) : 0;
     if (const char* e = std::getenv("LIC_NO_WRES")) c->wres_enabled = (e[0] != '1');
     if (const char* e = std::getenv("LIC_WSTAGE")) c->wstage_enabled = (e[0] != '0');
     c->max_batch = (int)max_batch;
