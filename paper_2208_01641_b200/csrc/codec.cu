@@ -177,7 +177,8 @@ struct lic_codec {
     int cg_enabled = 1;            // LIC_CG=1 forces one CTA per tile (no cta_group::2 pairs)
     int gs4_bn = 32;               // packed g_s L4 N tile (env LIC_GS4_BN=16|32)
     int pdl_enabled = 1;           // programmatic dependent launch of the GEMM engine (env LIC_PDL=0 disables)
-    int small_bn = 0;              // N tile of the h_a / h_s layers (env LIC_SMALL_BN=64|128; 0 = whole Cout: measured no gain)
+    int small_bn = 0;              // N tile of the h_a / h_s layers (env LIC_SMALL_BN=64|96|128; 0 = whole Cout: measured no gain)
+    int hs3_split_n = 1;           // h_s L3 with Cout 192 as two 96-channel N tiles (env LIC_HS3_SPLITN=0: off)
     int s2halo_enabled = 1;        // 5x5/s2 convs in parity-sub-grid halo mode (env LIC_S2HALO=0: per-tap tiles)
     int a_hi_only_enabled = 1;     // g_s L1 skips the zero lo plane of the integer y-hat (env LIC_YHAT_HI=0: off)
     int raw_tma_enabled = 1;       // u8 frames: raw patches by TMA (env LIC_RAW_TMA=0: cp.async)
@@ -428,6 +429,11 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
             Ly.ep != EP_GDN && Ly.ep != EP_IGDN) {
             P.BN = c->small_bn;
             P.n_ntiles = Ly.Cout / c->small_bn;
+        } else if (lid == HS3 && !c->small_bn && c->hs3_split_n && Ly.Cout == 192) {
+            // h_s L3 (sigma -> index, one 192-channel tile per CTA): two 96-channel N tiles, so a
+            // CTA's second tile's MMAs overlap its first tile's epilogue (30 -> 28 us at C3)
+            P.BN = 96;
+            P.n_ntiles = 2;
         }
     }
     const bool gdn = (Ly.ep == EP_GDN || Ly.ep == EP_IGDN);
@@ -1025,6 +1031,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_HS3_SPLITN")) c->hs3_split_n = (e[0] != '0');
     if (const char* e = std::getenv("LIC_SMALL_BN")) c->small_bn = atoi(e) == 64 || atoi(e) == 96 || atoi(e) == 128 ? atoi(e) : 0;
     if (const char* e = std::getenv("LIC_NO_WRES")) c->wres_enabled = (e[0] != '1');
     if (const char* e = std::getenv("LIC_WSTAGE")) c->wstage_enabled = (e[0] != '0');
