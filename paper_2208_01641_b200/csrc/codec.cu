@@ -194,6 +194,9 @@ struct lic_codec {
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     int wstage_enabled = 1;        // per-warp output staging in the GDN epilogue (env LIC_WSTAGE=0: quadrant blocks)
+    int l1_rows_enabled = 1;       // u8 frames: row-halo g_a L1 (layer.h l1_rows; env LIC_L1_ROWS=0: im2col tiles)
+    Layer l1r;                     // g_a L1 planned in row-halo mode (tile 8 x 16; shares GA1's weights and buffers)
+    bool l1r_ok = false;
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
     std::vector<void*> allocs;          // device allocations to free
@@ -287,12 +290,13 @@ static bool encode_act_map(CUtensorMap* m, const __half* base, int C, int W, int
 }
 
 // the u8 HWC frames as a 3-D byte tensor (3W, H, B), box = one fused-L1 raw patch (128 B x 19 rows)
-static bool encode_u8_frame_map(CUtensorMap* m, const void* base, int W, int H, int B) {
+// (row-halo g_a L1: 80 B x 35 rows)
+static bool encode_u8_frame_map(CUtensorMap* m, const void* base, int W, int H, int B, bool rows = false) {
     EncodeTiledFn enc = get_encode_fn();
     if (!enc) return false;
     cuuint64_t dims[3] = {(cuuint64_t)W * 3, (cuuint64_t)H, (cuuint64_t)B};
     cuuint64_t str[2] = {(cuuint64_t)W * 3, (cuuint64_t)W * 3 * H};
-    cuuint32_t box[3] = {128, 19, 1};
+    cuuint32_t box[3] = {rows ? 80u : 128u, rows ? 35u : 19u, 1};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, str, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -405,11 +409,17 @@ static int pow2_cols(int n) {
 }
 
 // build the GEMM-side plan of one layer (everything except epilogue output pointers)
+// layer id of a Layer (the row-halo g_a L1 plan counts as g_a L1)
+static int lid_of(const lic_codec* c, const Layer& Ly) {
+    return &Ly == &c->l1r ? (int)GA1 : (int)(&Ly - c->layers);
+}
+
 static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     ConvParams& P = Ly.prm;
+    const bool l1rows = &Ly == &c->l1r;
     std::memset(&P, 0, sizeof P);
     P.tps = 1;
-    const bool gemm_l1 = (&Ly == &c->layers[GA1]);
+    const bool gemm_l1 = (&Ly == &c->layers[GA1]) || l1rows;
     P.Cin = Ly.Cin_eff;
     P.kchunks = Ly.Cin_eff / 64;
     P.Cout = Ly.Cout;
@@ -423,7 +433,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     // epilogue chain each): split their output channels into 64-wide N tiles so more CTAs work
     // and each CTA pipelines several tiles (env LIC_SMALL_BN=0 keeps one N tile)
     {
-        const int lid = (int)(&Ly - c->layers);
+        const int lid = lid_of(c, Ly);
         const bool hyper_layer = lid >= HA1 && lid <= HS3;
         if (hyper_layer && c->small_bn && Ly.Cout % c->small_bn == 0 && Ly.Cout > c->small_bn &&
             Ly.ep != EP_GDN && Ly.ep != EP_IGDN) {
@@ -531,7 +541,25 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     int halo_w = 10;                                                   // Wt + 2
     if (const char* e = std::getenv("LIC_HALO_W")) halo_w = std::max(10, std::min(32, atoi(e)));
     const uint32_t hpb = ((uint32_t)(halo_w * 18 * 128) + 1023) / 1024 * 1024;   // halo_w x (Ht+2) rows
-    if (gemm_l1) {
+    if (l1rows) {
+        // row-halo g_a L1 (u8 frames; layer.h l1_rows): stage = one 35 x 8-row halo (SW128 rows),
+        // 3 stages when they fit; resident weights; 2 raw u8 patch slots (TMA, 80 B x 35 rows)
+        P.fuse_l1 = 1;
+        P.l1_rows = 1;
+        P.halo = 0;
+        P.halo_slots = 0;
+        P.Wt = 8; P.Ht = 16;
+        P.stage_bytes = 35u * 8u * 128u;
+        const uint32_t wbytes = (uint32_t)P.kchunks * b_bytes, rawb = 2u * 2816u;
+        P.stages = (fixed + 3 * P.stage_bytes + wbytes + rawb + 2048 + (tma_out ? ostage_bytes : 0) <= budget) ? 3 : 2;
+        P.wres = 1;
+        P.off_wres = P.stages * P.stage_bytes;
+        P.off_patch = P.off_wres + wbytes;
+        P.off_lut = P.off_patch;
+        P.off_halo = 0;
+        P.off_raw = (P.off_patch + 127) / 128 * 128;
+        P.off_gamma = (P.off_raw + rawb + 1023) / 1024 * 1024;
+    } else if (gemm_l1) {
         // fused g_a L1: stage s = A chunk s (hi, lo) built by warps 0/2/3; resident weights;
         // double-buffered fp32 input patch; k -> patch offset table + u8 LUT
         P.fuse_l1 = 1;
@@ -568,7 +596,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         // several taps per weight stage (one wait per 8 * tps MMAs; env LIC_TPS=1..4)
         // (measured per layer: 3 for the many-tile parity-halo convs of g_a, 2 elsewhere)
         {
-            const int lid = (int)(&Ly - c->layers);
+            const int lid = lid_of(c, Ly);
             P.tps = (P.sub4 && lid >= GA2 && lid <= GA4) ? 3 : 2;
         }
         if (const char* e = std::getenv("LIC_TPS")) P.tps = std::max(1, std::min(kMaxTps, atoi(e)));
@@ -691,7 +719,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         // split-K candidates: the h layers with a handful of tiles (h_a L2, L3, h_s L1), whose
         // epilogue split_reduce_kernel implements (ReLU, z-quantise) and whose MMA loop is the
         // lean halo loop (the only one that iterates a K slice)
-        const int lid = (int)(&Ly - c->layers);
+        const int lid = lid_of(c, Ly);
         P.ksplit_ok = (lid == HA2 || lid == HA3 || lid == HS1) && P.halo && !P.wres && (P.tps == 2 || P.tps == 3) &&
                       P.cg == 2 && P.n_ntiles == 1 && (Ly.ep == EP_RELU || Ly.ep == EP_ZQUANT) && P.Cout % 8 == 0;
     }
@@ -750,7 +778,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     P.crop_top = 0; P.crop_left = 0; P.crop_H = Ly.Hout; P.crop_W = Ly.Wout;
     if (std::getenv("LIC_PLAN_DEBUG"))
         std::fprintf(stderr, "plan layer %d: BN %d cg %d ntiles %d halo %d sub4 %d tps %d stages %d slots %d wres %d "
-                     "tma_out %d ostage %d smem %u kchunks %d wst %d/%d\n", (int)(&Ly - c->layers), P.BN, P.cg,
+                     "tma_out %d ostage %d smem %u kchunks %d wst %d/%d\n", lid_of(c, Ly), P.BN, P.cg,
                      P.n_ntiles, P.halo, P.sub4, P.tps, P.stages, P.halo_slots, P.wres, P.tma_out, P.ostage_slots,
                      P.smem_bytes, P.kchunks, P.wst_ch, P.wst_slots);
     return LIC_OK;
@@ -782,7 +810,7 @@ static lic_status run_layer(lic_codec* c, Layer& Ly, const ConvParams& P0, int b
         P.tma_out = 0;
     }
     const int grid = P.cg * std::min(P.total_tiles, c->num_sms / P.cg);
-    const int lid = (int)(&Ly - c->layers);
+    const int lid = lid_of(c, Ly);
     P.pdl = c->pdl_enabled;
     if (c->trace_layer == lid && c->d_trace) {
         P.trace = c->d_trace;
@@ -922,6 +950,17 @@ static lic_status upload(lic_codec* c, void* dst, const void* src, size_t bytes)
 }
 
 // per-codec epilogue settings of the layer plans (after plan_layer)
+// the row-halo plan of g_a L1 (u8 frames): a copy of GA1's layer (weights, buffers) planned
+// with l1_rows -- encode_impl picks it per call when the frames qualify
+static lic_status plan_l1r(lic_codec* c) {
+    c->l1r_ok = false;
+    if (!c->layers[GA1].present || !c->l1_rows_enabled) return LIC_OK;
+    c->l1r = c->layers[GA1];
+    if (lic_status r = plan_layer(c, c->l1r)) return r;
+    c->l1r_ok = true;
+    return LIC_OK;
+}
+
 static void finish_plans(lic_codec* c) {
     for (int l = 0; l < NLAYER; ++l)
         if (c->layers[l].present) c->layers[l].prm.range_count = c->d_range;
@@ -933,6 +972,10 @@ static void finish_plans(lic_codec* c) {
     c->layers[GS4].prm.crop_left = c->left;
     c->layers[GS4].prm.crop_H = c->H;
     c->layers[GS4].prm.crop_W = c->W;
+    if (c->l1r_ok) {
+        c->l1r.prm.range_count = c->d_range;
+        c->l1r.prm.onedn = c->act == 1;
+    }
 }
 
 extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint32_t height, uint32_t width,
@@ -1029,6 +1072,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_G2_SLOT16")) c->g2_slot16 = (e[0] != '0');
     if (const char* e = std::getenv("LIC_KSPLIT")) { c->ksplit_enabled = atoi(e) != 0; c->ksplit_force = atoi(e) > 1 ? atoi(e) : 0; }
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_L1_ROWS")) c->l1_rows_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_HS3_SPLITN")) c->hs3_split_n = (e[0] != '0');
@@ -1175,6 +1219,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
         }
         if ((st = plan_layer(c, Ly))) return bail(st);
     }
+    if ((st = plan_l1r(c))) return bail(st);
     if (cudaMemset(c->d_range, 0, 8) != cudaSuccess) return bail(LIC_ECUDA);
     finish_plans(c);
     c->dbg_elems = dbg;
@@ -1215,6 +1260,7 @@ extern "C" lic_status lic_bind_workspace(lic_codec* c, void* dev_ptr, size_t byt
         lic_status r = plan_layer(c, Ly);        // tensor maps over the new planes
         if (r) { c->max_batch = old_batch; c->sticky = true; return r; }
     }
+    if (lic_status r = plan_l1r(c)) { c->max_batch = old_batch; c->sticky = true; return r; }
     finish_plans(c);
     if (c->ws_own) { cudaFree(c->ws_own); c->ws_own = nullptr; }
     c->ws_user = dev_ptr;
@@ -1361,7 +1407,18 @@ static lic_status encode_impl(lic_codec* c, const void* frames, int hwc, uint32_
     OutBuf oi = hyper ? route_out(c, y_idx, c->d_yidx, ny) : OutBuf{nullptr, nullptr, 0};
     OutBuf oz = hyper ? route_out(c, z_sym, c->d_zsym, nz) : OutBuf{nullptr, nullptr, 0};
     CK(cudaMemsetAsync(c->d_sat, 0, 8, st));
-    {
+    const bool raw_ok = hwc && c->raw_tma_enabled && (3 * c->W) % 16 == 0 && ((uintptr_t)fdev & 15) == 0;
+    if (raw_ok && c->l1r_ok && c->l1_int_enabled && c->l1_conv_enabled) {
+        // row-halo g_a L1 (layer.h l1_rows): u8 samples by one TMA box per tile, integer MMAs
+        ConvParams p = c->l1r.prm;
+        p.frame = fdev; p.fr_u8 = 1; p.fr_H = c->H; p.fr_W = c->W; p.fr_top = c->top; p.fr_left = c->left;
+        p.l1_int = 2;
+        p.raw_tma = 1;
+        CUtensorMap fmap{};
+        if (!encode_u8_frame_map(&fmap, fdev, c->W, c->H, B, true))
+            return fail(c, LIC_ECUDA, "cuTensorMapEncodeTiled (u8 frames) failed");
+        if ((r = run_layer(c, c->l1r, p, B, st, &fmap))) return r;
+    } else {
         ConvParams p = c->layers[GA1].prm;             // fused im2col: reads the frames directly
         p.frame = fdev; p.fr_u8 = hwc; p.fr_H = c->H; p.fr_W = c->W; p.fr_top = c->top; p.fr_left = c->left;
         p.l1_int = (hwc && c->l1_int_enabled) ? (c->l1_conv_enabled ? 2 : 1) : 0;

@@ -165,6 +165,14 @@ constexpr int kL1RawWords = 28;                                      // >= (3 + 
 constexpr int kL1RawPitch = 128;                                     // bytes per raw row (TMA box: 16-byte aligned start + 105 B)
 constexpr uint32_t kL1RawBytes = kL1PH * kL1RawPitch;               // one raw u8 patch (2432 B, a multiple of 128)
 static_assert(kL1Wt == 16, "build_l1 decodes r -> (r >> 4, r & 15)");
+// row-halo g_a L1 (p.l1_rows): tile 8 x 16 output pixels; the raw patch is a 80 B x 35 row TMA
+// box (16-byte aligned start + 19 px x 3 B + the 16th sample of the last element); the row halo
+// is 35 x 8 elements of one 128-byte SW128 row each (the first 32 bytes used: 16 fp16 samples)
+constexpr int kL1RRows = 35;                                         // 2 * 16 + 3 input rows
+constexpr int kL1RBox = 80;                                          // bytes per raw row (box width)
+constexpr uint32_t kL1RRawBytes = kL1RRows * kL1RBox;                // 2800 B per raw patch
+constexpr uint32_t kL1RRawSlot = 2816;                               // raw slot pitch (multiple of 128)
+constexpr uint32_t kL1RHaloBytes = kL1RRows * 8 * 128;               // 35840 B per row halo (35 KB)
 
 // MUFU.RSQ without the denormal-input fix-up (GDN/IGDN: beta + n >= beta > 0, normal)
 __device__ __forceinline__ float rcp_ftz(float x) {
@@ -354,7 +362,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
         for (int i = threadIdx.x - 128; i < kMaxTaps; i += 32 * kEpiWarps)
             s_tapoff[i] = (uint32_t)(((p.tap_dy[i] + 1) * p.halo_w + p.tap_dx[i] + 1) * 8);
     }
-    if constexpr (kL1) {
+    if constexpr (kL1) if (!p.l1_rows) {
+        // (row halo: no patch or LUT, and the MMAs read only the 32 bytes written per halo row)
         // zero the A stages (K columns >= 80 are never rewritten) and both patch buffers (the
         // row padding halves 105..111 are never rewritten); u8 -> (hi | lo << 16) of u8 / 255
         // (IEEE division, as the oracle), entry 256 = 0 for samples outside the frame
@@ -619,9 +628,74 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             if (bw == 0 && lane == 0) LIC_TRACE(it, T_PROD_START);     // fused L1: tile built
         }
     };
+    // row-halo g_a L1 (p.l1_rows; u8 frames, raw TMA, integer samples -- layer.h): per tile one
+    // raw TMA box (prefetched two tiles ahead into 2 slots) -> one row halo in stage `stage`
+    auto build_l1_rows = [&](int bw) {
+        const int bt = bw * 32 + lane;
+        const uint32_t raw_s = smem_u32(smem + p.off_raw);
+        auto raw_issue = [&](int tt, int buf) {
+            if (bw != 0 || lane != 0 || tt >= p.total_tiles) return;
+            const TileCoord tn = decode_tile<kSplitK>(p, tt, rank);
+            fence_proxy_async_smem();                 // the builders' reads of this slot precede the TMA write
+            mbar_arrive_expect_tx(&rawfull_bar[buf], kL1RRawBytes);
+            tma_load_3d(smem + p.off_raw + (uint32_t)buf * kL1RRawSlot, &mapA, &rawfull_bar[buf],
+                        (3 * (2 * tn.gx0 - 2 - p.fr_left)) & ~15, 2 * tn.gy0 - 2 - p.fr_top, tn.b);
+        };
+        if (p.pdl) griddep_wait();
+        raw_issue(cid, 0);
+        raw_issue(cid + ncl, 1);
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
+            const TileCoord tc = decode_tile<kSplitK>(p, t, rank);
+            const int ix0 = 2 * tc.gx0 - 2 - p.fr_left;
+            // the patch's first byte inside the 16-byte aligned box
+            const uint32_t sh = (uint32_t)(3 * ix0) & 15u;
+            const uint32_t rb = raw_s + (uint32_t)(it & 1) * kL1RRawSlot;
+            mbar_wait(&rawfull_bar[it & 1], (uint32_t)(it >> 1) & 1u);
+            if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_RAW);
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            if (bw == 0 && lane == 0) LIC_TRACE(it, T_B_C0_READY);
+            const uint32_t hb = smem_u32(smem + stage * p.stage_bytes);
+            for (int e = bt; e < kL1RRows * 8; e += kL1Builders) {
+                const int iy = e >> 3, tx = e & 7;
+                const uint32_t o = sh + 6u * (uint32_t)tx;                 // byte offset in the raw row
+                const uint32_t src = rb + (uint32_t)iy * kL1RBox + (o & ~3u);
+                const uint32_t w0 = ldsu(src), w1 = ldsu(src + 4), w2 = ldsu(src + 8), w3 = ldsu(src + 12),
+                               w4 = ldsu(src + 16);
+                const uint32_t s8 = (o & 3u) * 8u;
+                const uint32_t a0 = __funnelshift_r(w0, w1, s8), a1 = __funnelshift_r(w1, w2, s8);
+                const uint32_t a2 = __funnelshift_r(w2, w3, s8), a3 = __funnelshift_r(w3, w4, s8);
+                // samples 0-7 -> logical 16-byte chunk 0, 8-15 -> chunk 1 (SW128: chunk c of row e at c ^ (e & 7))
+                const uint32_t d = hb + (uint32_t)e * 128u;
+                stsu4(d + ((uint32_t)tx << 4),
+                      make_uint4(u8pair_to_h2(a0, 0x4140u), u8pair_to_h2(a0, 0x4342u),
+                                 u8pair_to_h2(a1, 0x4140u), u8pair_to_h2(a1, 0x4342u)));
+                stsu4(d + (((uint32_t)tx ^ 1u) << 4),
+                      make_uint4(u8pair_to_h2(a2, 0x4140u), u8pair_to_h2(a2, 0x4342u),
+                                 u8pair_to_h2(a3, 0x4140u), u8pair_to_h2(a3, 0x4342u)));
+            }
+            fence_proxy_async_smem();                             // generic writes -> tensor core
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_cluster(lbar(&full_bar[stage]));
+                else mbar_arrive(&full_bar[stage]);
+                if (bw == 0) LIC_TRACE(it, T_B_C0_DONE);
+            }
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            // every builder has read raw slot it & 1: it takes tile it + 2's patch
+            named_bar_sync_na(4, kL1Builders);
+            raw_issue(t + 2 * ncl, it & 1);
+            if (bw == 0 && lane == 0) LIC_TRACE(it, T_PROD_START);
+        }
+    };
+    auto build_l1_any = [&](int bw) {
+        if (p.l1_rows) build_l1_rows(bw); else build_l1(bw);
+    };
 
     if (kL1 && warp == 2) {
-        if constexpr (kL1) build_l1(1);
+        if constexpr (kL1) build_l1_any(1);
     } else if (warp == 0) {
         // ====================== TMA producer (weights; activations unless halo mode) ======================
         // warp-uniform loop; one elected lane issues (keeps coordinates in uniform registers)
@@ -701,10 +775,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 }
             }
         }
-        if constexpr (kL1) build_l1(0);
+        if constexpr (kL1) build_l1_any(0);
     } else if (warp == 3) {
         // ====================== halo producer (halo mode) ======================
-        if constexpr (kL1) build_l1(2);
+        if constexpr (kL1) build_l1_any(2);
         if (!kL1 && p.halo) {
             if (p.pdl) griddep_wait();
             int hs = 0;
@@ -969,6 +1043,25 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     __syncwarp();
                     if (++hs == p.halo_slots) { hs = 0; hphase ^= 1; }
                 }
+            } else if (kL1 && p.l1_rows) {
+                // row-halo g_a L1: kernel row ky is one K = 16 MMA -- A = the halo rows 2 ty + ky
+                // (window start ky * 8 rows, 8-row groups every 2 halo row-blocks), B = K columns
+                // 16 ky .. 16 ky + 15 of the resident weights (chunk ky / 4, step ky % 4)
+                wait_poll(&full_bar[stage], phase);
+                tc_fence_after();
+                if (lane == 0) LIC_TRACE(it, T_MMA_K0);
+                const uint32_t st = smem_u32(smem + stage * p.stage_bytes);
+                const uint32_t wb = smem_u32(smem + p.off_wres);
+                if (elect_one()) {
+#pragma unroll
+                    for (int ky = 0; ky < 5; ++ky)
+                        mma_ss(d, sdesc_sw128_sbo(st + (uint32_t)ky * 1024u, 2048u),
+                               sdesc_sw128(wb + (uint32_t)(ky >> 2) * b_bytes) + 2 * (ky & 3), ky != 0);
+                    commit(&empty_bar[stage]);
+                }
+                __syncwarp();
+                if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                poll_norm();
             } else {
                 const int nk = p.ntaps[tc.ph] * p.kchunks;
                 const int t0k = p.tap0[tc.ph] * p.kchunks;            // resident weights: tile (tap, chunk)

@@ -112,6 +112,14 @@ struct ConvParams {
     uint32_t off_lut;                 // u8 LUT [257] (hi | lo << 16; entry 256 = 0)
     uint32_t off_raw;                 // raw u8 patch [2][19][112] in 2176-byte slots (cp.async or TMA, u8 frames)
     int raw_tma;                      // the raw patch by one TMA box per tile (mapA = the u8 frame, 3W x H x B)
+    // row-halo g_a L1 (u8 frames, raw TMA, integer samples; tile Wt = 8 x Ht = 16): instead of an
+    // im2col A tile (128 px x 80 K) the builders write one "row halo" per tile -- element
+    // (iy, tx), iy < 35, tx < 8, holds the 16 u8 samples at input row iy, bytes 6 tx .. 6 tx + 15
+    // of the patch (the 5 kx taps x 3 channels of K row ky, slot 15 has a zero weight) -- and the
+    // 5 kernel rows ky are 5 K = 16 MMAs whose A operand is the window of rows 2 ty + ky
+    // (SW128 rows, window start ky x 1024 B, 8-row-group stride 2048 B): 2.3x fewer builder
+    // stores than im2col, no fp16 patch, 5 instead of 8 MMAs per tile
+    int l1_rows;
     // TMA-store epilogue: each epilogue warp stages 32 px x 16 ch (hi, lo: 1 KB each) in smem and
     // writes it with a bulk tensor store; out maps: conv (C, W, H, B), deconv phase view
     // (C, px, W/2, py, B*H/2) of the NHWC output, one map per plane
