@@ -194,6 +194,7 @@ struct lic_codec {
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     int wstage_enabled = 1;        // per-warp output staging in the GDN epilogue (env LIC_WSTAGE=0: quadrant blocks)
+    int g2_db16 = 0;               // two-group epilogue: double-buffered 16-channel staging (env LIC_G2_DB16=1 all, 2 g_a L1)
     int l1_rows_enabled = 1;       // u8 frames: row-halo g_a L1 (layer.h l1_rows; env LIC_L1_ROWS=0: im2col tiles)
     Layer l1r;                     // g_a L1 planned in row-halo mode (tile 8 x 16; shares GA1's weights and buffers)
     bool l1r_ok = false;
@@ -709,6 +710,9 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         const int G = P.BN / 4;                                         // channels per epilogue warp
         P.wst_ch = (G % 32 == 0 || P.g2) ? 32 : 16;
         P.wst_slots = P.wst_ch == 32 ? 1 : 2;
+        // two-group epilogue: 16-channel rounds in two alternating 2 KB slots per warp instead of one
+        // 4 KB 32-channel slot (env LIC_G2_DB16=1 every such layer, 2 g_a L1 only; measured: no change)
+        if (P.g2 && (c->g2_db16 == 1 || (c->g2_db16 == 2 && gemm_l1))) { P.wst_ch = 16; P.wst_slots = 2; }
     } else if (P.g2) {
         // two-group epilogue with 32 KB of staging: one 2 KB slot per warp, 16-channel rounds
         P.wst_ch = 16;
@@ -1073,6 +1077,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_KSPLIT")) { c->ksplit_enabled = atoi(e) != 0; c->ksplit_force = atoi(e) > 1 ? atoi(e) : 0; }
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_L1_ROWS")) c->l1_rows_enabled = (e[0] != '0');
+    if (const char* e = std::getenv("LIC_G2_DB16")) c->g2_db16 = atoi(e);
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_HS3_SPLITN")) c->hs3_split_n = (e[0] != '0');

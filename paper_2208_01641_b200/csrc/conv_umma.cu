@@ -1184,8 +1184,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
             const bool w32 = p.wst_ch == 32;
             const uint32_t rows_b = w32 ? 64u : 32u, slot_b = 32u * rows_b * 2u, lo_off = 32u * rows_b;
             const uint32_t sw_mask = rows_b / 16u - 1u;
-            const uint32_t slot_off = p.off_ostage + (uint32_t)(warp - 4) * slot_b;
-            const uint32_t rowa = smem_u32(smem) + slot_off + (uint32_t)lane * rows_b;
+            // 16-channel rounds in two alternating 2 KB slots per warp (p.wst_slots == 2): a slot is
+            // rewritten two rounds after its store was issued (wait_group.read 1, not 0)
+            const bool db16 = !w32 && p.wst_slots == 2;
+            const uint32_t slot_off0 = p.off_ostage + (uint32_t)(warp - 4) * slot_b * (db16 ? 2u : 1u);
             const uint32_t sw = (((uint32_t)lane * rows_b) >> 7) & sw_mask;     // swizzle of this row
             const int ty0 = (q * 32) >> p.wt_log2, tx0 = (q * 32) & (p.Wt - 1);
             const uint32_t tbuf = tmem_base + lane_off + (uint32_t)(gr * p.acc_stride);
@@ -1320,8 +1322,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     for (int pc = 0; pc < 2 * NSUB; ++pc) {
                         const int j = pc & 1;
                         if (kChunked && j == 0 && pc > 0) wait_norm(pc >> 1);
+                        const uint32_t slot_off = slot_off0 + (db16 ? (uint32_t)(pc & 1) * slot_b : 0u);
+                        const uint32_t rowa = smem_u32(smem) + slot_off + (uint32_t)lane * rows_b;
                         if (j == 0 || !w32) {
-                            if (lane == 0) bulk_wait_read0();              // this warp's slot is free again
+                            if (lane == 0) { if (db16) bulk_wait_read1(); else bulk_wait_read0(); }   // the slot is free again
                             __syncwarp();
                         }
                         uint32_t vh[8], vl[8], nr[16];
