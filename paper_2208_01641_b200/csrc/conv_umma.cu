@@ -1325,7 +1325,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                         const uint32_t slot_off = slot_off0 + (db16 ? (uint32_t)(pc & 1) * slot_b : 0u);
                         const uint32_t rowa = smem_u32(smem) + slot_off + (uint32_t)lane * rows_b;
                         if (j == 0 || !w32) {
-                            if (lane == 0) { if (db16) bulk_wait_read1(); else bulk_wait_read0(); }   // the slot is free again
+                            if (lane == 0 && !(p.dbg_nostore & 128)) { if (db16) bulk_wait_read1(); else bulk_wait_read0(); }   // the slot is free again
                             __syncwarp();
                         }
                         uint32_t vh[8], vl[8], nr[16];
@@ -1402,6 +1402,10 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             }
                         }
                         guard16(y, ovf);
+                        if (p.dbg_nostore & 64) {                   // experiment (traced layer): compute only
+                            if (lane == 0 && __float_as_uint(y[0] + y[15]) == 0x7fc00001u) p.out_f32[0] = y[1];
+                            continue;
+                        }
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk) {
                             uint4 hq, lq;
@@ -1419,7 +1423,8 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                                 if (threadIdx.x == lead) LIC_TRACE(it, pc == 2 * NSUB - 1 ? T_EPI_ACQ : T_EPI_P2);
                                 const uint8_t* hs = smem + slot_off;
                                 const int cb = tc.nt * p.BN + c0 + (w32 ? 32 * (pc >> 1) : 16 * pc);
-                                if (p.nphase == 1) {
+                                if (p.dbg_nostore & 32) {                   // experiment (traced layer): no TMA store
+                                } else if (p.nphase == 1) {
                                     tma_store_5d(&mapOH, hs, cb, tc.gx0 + tx0, tc.gy0 + ty0, tc.b, 0);
                                 } else {
                                     const int ph = tc.ph;
