@@ -140,6 +140,7 @@ struct Layer {
     __half* out_buf = nullptr;
     size_t out_plane = 0;
     char in_id = 0, out_id = 0;   // workspace buffer ('A', 'B', 'Y', 'Z'; 0 = none) -- re-bound by lic_bind_workspace
+    bool y_bounded = false;   // forward GDN / 1DN whose output provably stays in fp16 range (no guard)
     ConvParams prm{};
     CUtensorMap mapA{}, mapB{}, mapG{}, mapOH{}, mapOL{}, mapO2{}, mapO3{};
 };
@@ -194,6 +195,7 @@ struct lic_codec {
     int gs4_gather = 1;            // g_s L4 in gather mode (offsets in N; env LIC_GS4_GATHER=0: packed-phase halo mode)
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     int wstage_enabled = 1;        // per-warp output staging in the GDN epilogue (env LIC_WSTAGE=0: quadrant blocks)
+    int no_guard_enabled = 1;      // skip the range guard of provably bounded GDN outputs (env LIC_NO_GUARD=0: keep it)
     int g2_db16 = 0;               // two-group epilogue: double-buffered 16-channel staging (env LIC_G2_DB16=1 all, 2 g_a L1)
     int l1_rows_enabled = 1;       // u8 frames: row-halo g_a L1 (layer.h l1_rows; env LIC_L1_ROWS=0: im2col tiles)
     Layer l1r;                     // g_a L1 planned in row-halo mode (tile 8 x 16; shares GA1's weights and buffers)
@@ -728,6 +730,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
                       P.cg == 2 && P.n_ntiles == 1 && (Ly.ep == EP_RELU || Ly.ep == EP_ZQUANT) && P.Cout % 8 == 0;
     }
     P.L = c->L;
+    P.no_guard = (Ly.y_bounded && c->no_guard_enabled) ? 1 : 0;
     // tensor maps
     const int ntaps_w = (gemm_l1 || P.gather) ? 1 : (P.pack4 ? 9 : Ly.k * Ly.k);
     const int cout_pad = P.BN * P.n_ntiles;
@@ -1078,6 +1081,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_L1_ROWS")) c->l1_rows_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_G2_DB16")) c->g2_db16 = atoi(e);
+    if (const char* e = std::getenv("LIC_NO_GUARD")) c->no_guard_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_HS3_SPLITN")) c->hs3_split_n = (e[0] != '0');
@@ -1218,6 +1222,20 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
             const std::vector<float>& ga = blk[wn + ".gamma"];
             std::vector<__half> gh(ga.size());
             for (size_t i = 0; i < ga.size(); ++i) gh[i] = __float2half_rn(ga[i]);
+            // forward GDN / 1DN output bound (R16f): with gamma >= 0 and beta >= 0,
+            // n_i >= gamma_ii x_i^2 (GDN) / gamma_ii |x_i| (1DN), so |y_i| <= 1 / sqrt(gamma_ii) resp.
+            // 1 / gamma_ii -- below 60000 (fp16 range, rounding margin) the range guard cannot fire
+            if (d.ep == EP_GDN) {
+                const int n = Ly.Cout;
+                bool ok = true;
+                for (size_t i = 0; i < gh.size() && ok; ++i) ok = __half2float(gh[i]) >= 0.0f;
+                for (size_t i = 0; i < be.size() && ok; ++i) ok = be[i] >= 0.0f;
+                for (int i = 0; i < n && ok; ++i) {
+                    const double g = __half2float(gh[(size_t)i * n + i]);
+                    ok = c->act == 1 ? g >= 1.0 / 60000.0 : g >= 1.0 / (60000.0 * 60000.0);
+                }
+                Ly.y_bounded = ok;
+            }
             if ((st = dalloc(c, &Ly.beta, be.size() * 4)) || (st = upload(c, Ly.beta, be.data(), be.size() * 4)) ||
                 (st = dalloc(c, &Ly.gamma, gh.size() * 2)) || (st = upload(c, Ly.gamma, gh.data(), gh.size() * 2)))
                 return bail(st);

@@ -1401,7 +1401,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                                 continue;
                             }
                         }
-                        guard16(y, ovf);
+                        if (!p.no_guard) guard16(y, ovf);
                         if (p.dbg_nostore & 64) {                   // experiment (traced layer): compute only
                             if (lane == 0 && __float_as_uint(y[0] + y[15]) == 0x7fc00001u) p.out_f32[0] = y[1];
                             continue;

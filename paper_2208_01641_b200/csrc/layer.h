@@ -120,6 +120,8 @@ struct ConvParams {
     // (SW128 rows, window start ky x 1024 B, 8-row-group stride 2048 B): 2.3x fewer builder
     // stores than im2col, no fp16 patch, 5 instead of 8 MMAs per tile
     int l1_rows;
+    int no_guard;                     // forward GDN / 1DN with a provable |y| bound below the fp16 range
+                                      // (host check of gamma, beta; R16f): no range guard in P2
     // TMA-store epilogue: each epilogue warp stages 32 px x 16 ch (hi, lo: 1 KB each) in smem and
     // writes it with a bulk tensor store; out maps: conv (C, W, H, B), deconv phase view
     // (C, px, W/2, py, B*H/2) of the NHWC output, one map per plane
