@@ -1,10 +1,11 @@
 """Kernel-variant equivalence on the GPU (-m gpu): the experiment switches of DESIGN.md §7 that
 change how a layer is computed but not what it computes.
 
-- g_a L1's raw u8 patch by one TMA box per tile (3W % 16 == 0) or by 4-byte cp.async: the same
-  samples reach the same A tiles, so the latents are bit-identical; likewise 4 hi-only A stages
-  vs 2 split ones, and split-K h layers vs single-pass ones (up to summation order: compared
-  with the oracle bars).
+- g_a L1 on u8 frames as a row halo with five K = 16 MMAs (default, R16g) or as im2col
+  tiles whose raw u8 patch comes by one TMA box per tile (3W % 16 == 0) or by 4-byte cp.async:
+  the same products in the same K-step order, so the latents are bit-identical; likewise 4
+  hi-only A stages vs 2 split ones, and split-K h layers vs single-pass ones (up to summation
+  order: compared with the oracle bars).
 - the two-group GDN / IGDN epilogue (y from the norm operand and the signs, R16e) vs
   the single-group one (x kept in registers): different rounding, both within the oracle bars.
 """
@@ -75,12 +76,14 @@ def run(lic, data, **kv):
 
 
 def test_raw_patch_tma_vs_cp_async(lic, data):
-    a = run(lic, data)                                  # TMA boxes, 4 hi-only stages
-    b = run(lic, data, LIC_RAW_TMA=0)                   # 4-byte cp.async
-    c = run(lic, data, LIC_RAW_TMA=0, LIC_L1_STAGES=0)  # cp.async, 2 split stages
+    a = run(lic, data)                                  # row halo (R16g)
+    b = run(lic, data, LIC_RAW_TMA=0)                   # im2col, 4-byte cp.async
+    c = run(lic, data, LIC_RAW_TMA=0, LIC_L1_STAGES=0)  # im2col, cp.async, 2 split stages
+    d = run(lic, data, LIC_L1_ROWS=0)                   # im2col, TMA boxes, 4 hi-only stages
     for k in ("y", "z", "ys", "yi", "zs", "xh"):
         assert np.array_equal(a[k], b[k]), k
         assert np.array_equal(a[k], c[k]), k
+        assert np.array_equal(a[k], d[k]), k
 
 
 @pytest.mark.parametrize("g2", [0, 1, 2])
