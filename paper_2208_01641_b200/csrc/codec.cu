@@ -196,10 +196,13 @@ struct lic_codec {
     int wres_enabled = 1;          // env LIC_NO_WRES=1 streams the g_s L4 weights
     int wstage_enabled = 1;        // per-warp output staging in the GDN epilogue (env LIC_WSTAGE=0: quadrant blocks)
     int no_guard_enabled = 1;      // skip the range guard of provably bounded GDN outputs (env LIC_NO_GUARD=0: keep it)
+    int gs1_hi_plan = 1;           // hyperprior g_s L1: hi-only halo ring, deeper weight ring (env LIC_GS1_HI=0: off)
     int g2_db16 = 0;               // two-group epilogue: double-buffered 16-channel staging (env LIC_G2_DB16=1 all, 2 g_a L1)
     int l1_rows_enabled = 1;       // u8 frames: row-halo g_a L1 (layer.h l1_rows; env LIC_L1_ROWS=0: im2col tiles)
     Layer l1r;                     // g_a L1 planned in row-halo mode (tile 8 x 16; shares GA1's weights and buffers)
     bool l1r_ok = false;
+    Layer gs1h;                    // g_s L1 planned for a hi-only input (hyperprior decode; shares GS1's weights and buffers)
+    bool gs1h_ok = false;
     std::vector<float> h_sigma_y, h_sigma_z, h_table, h_mu_y, h_mu_z;
     std::vector<uint32_t> cdf_fact, cdf_z, cdf_gauss;
     std::vector<void*> allocs;          // device allocations to free
@@ -414,6 +417,7 @@ static int pow2_cols(int n) {
 // build the GEMM-side plan of one layer (everything except epilogue output pointers)
 // layer id of a Layer (the row-halo g_a L1 plan counts as g_a L1)
 static int lid_of(const lic_codec* c, const Layer& Ly) {
+    if (&Ly == &c->gs1h) return GS1;
     return &Ly == &c->l1r ? (int)GA1 : (int)(&Ly - c->layers);
 }
 
@@ -544,6 +548,12 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
     int halo_w = 10;                                                   // Wt + 2
     if (const char* e = std::getenv("LIC_HALO_W")) halo_w = std::max(10, std::min(32, atoi(e)));
     const uint32_t hpb = ((uint32_t)(halo_w * 18 * 128) + 1023) / 1024 * 1024;   // halo_w x (Ht+2) rows
+    // the hyperprior's g_s L1 on the decode path reads a hi-only input (R16c): one plane per halo slot,
+    // the freed shared memory goes to the weight ring (c->gs1h)
+    const bool hi_only_plan = &Ly == &c->gs1h;
+    const int hplanes = hi_only_plan ? 1 : P.split;
+    P.halo_planes = hplanes;
+    P.a_hi_only = hi_only_plan ? 1 : 0;
     if (l1rows) {
         // row-halo g_a L1 (u8 frames; layer.h l1_rows): stage = one 35 x 8-row halo (SW128 rows),
         // 3 stages when they fit; resident weights; 2 raw u8 patch slots (TMA, 80 B x 35 rows)
@@ -591,7 +601,7 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         P.off_gp = P.off_wres + P.kchunks * b_bytes;
         P.off_halo = 0;
         P.off_gamma = (P.off_gp + 9u * 128u * 48u + 1023) / 1024 * 1024;
-    } else if (stride1 && fixed + 2 * P.split * hpb + 2 * b_bytes <= budget && c->halo_enabled) {
+    } else if (stride1 && fixed + 2 * hplanes * hpb + 2 * b_bytes <= budget && c->halo_enabled) {
         P.halo = 1;
         P.Wt = 8; P.Ht = 16;
         P.halo_plane_bytes = hpb;
@@ -608,29 +618,29 @@ static lic_status plan_layer(lic_codec* c, Layer& Ly) {
         // its taps, while every tap needs a fresh weight tile, so smem goes to the weight ring)
         int slots = 2;
         if (const char* e = std::getenv("LIC_HALO_SLOTS")) slots = std::max(2, std::min(4, atoi(e)));
-        while (slots > 2 && fixed + slots * P.split * hpb + 3 * b_bytes > budget) --slots;
+        while (slots > 2 && fixed + slots * hplanes * hpb + 3 * b_bytes > budget) --slots;
         P.halo_slots = slots;
         // small weight sets (packed g_s L4: 9 taps x 2 chunks x 2 KB) stay resident
         const uint32_t wtot = (uint32_t)P.ntaps[0] * P.kchunks * b_bytes;
-        if (c->wres_enabled && P.nphase == 1 && fixed + slots * P.split * hpb + wtot <= budget && wtot <= 64 * 1024) {
+        if (c->wres_enabled && P.nphase == 1 && fixed + slots * hplanes * hpb + wtot <= budget && wtot <= 64 * 1024) {
             P.wres = 1;
             P.stages = 1;
             P.stage_bytes = 0;
             P.off_wres = 0;
             P.off_halo = (wtot + 1023) / 1024 * 1024;
         } else {
-            int stages = (int)((budget - fixed - slots * P.split * hpb) / P.stage_bytes);
+            int stages = (int)((budget - fixed - slots * hplanes * hpb) / P.stage_bytes);
             // keep a double-buffered weight ring: wide N tiles (M = 320 models, BN = 192) drop to
             // fewer taps per stage rather than to a single stage (measured: -10% frames/s at 1 stage)
             while (stages < 2 && P.tps > 1) {
                 --P.tps;
                 P.stage_bytes = b_bytes * (uint32_t)P.tps;
-                stages = (int)((budget - fixed - slots * P.split * hpb) / P.stage_bytes);
+                stages = (int)((budget - fixed - slots * hplanes * hpb) / P.stage_bytes);
             }
             P.stages = std::min(stages, 8);
             P.off_halo = P.stages * P.stage_bytes;
         }
-        P.off_gamma = P.off_halo + slots * P.split * hpb;
+        P.off_gamma = P.off_halo + slots * hplanes * hpb;
     } else {
         P.halo = 0;
         P.halo_slots = 0;
@@ -957,9 +967,16 @@ static lic_status upload(lic_codec* c, void* dst, const void* src, size_t bytes)
 }
 
 // per-codec epilogue settings of the layer plans (after plan_layer)
-// the row-halo plan of g_a L1 (u8 frames): a copy of GA1's layer (weights, buffers) planned
+// alternative plans picked per call: g_s L1 for a hi-only input (hyperprior decode) and the
+// row-halo plan of g_a L1 (u8 frames): copies of the layer (weights, buffers) planned
 // with l1_rows -- encode_impl picks it per call when the frames qualify
-static lic_status plan_l1r(lic_codec* c) {
+static lic_status plan_variants(lic_codec* c) {
+    c->gs1h_ok = false;
+    if (c->layers[GS1].present && c->kind == 1 && c->a_hi_only_enabled && c->gs1_hi_plan && c->layers[GS1].prm.halo) {
+        c->gs1h = c->layers[GS1];
+        if (lic_status r = plan_layer(c, c->gs1h)) return r;
+        c->gs1h_ok = c->gs1h.prm.halo == 1;
+    }
     c->l1r_ok = false;
     if (!c->layers[GA1].present || !c->l1_rows_enabled) return LIC_OK;
     c->l1r = c->layers[GA1];
@@ -982,6 +999,10 @@ static void finish_plans(lic_codec* c) {
     if (c->l1r_ok) {
         c->l1r.prm.range_count = c->d_range;
         c->l1r.prm.onedn = c->act == 1;
+    }
+    if (c->gs1h_ok) {
+        c->gs1h.prm.range_count = c->d_range;
+        c->gs1h.prm.onedn = c->act == 1;
     }
 }
 
@@ -1081,6 +1102,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
     if (const char* e = std::getenv("LIC_L1_CONV")) c->l1_conv_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_L1_ROWS")) c->l1_rows_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_G2_DB16")) c->g2_db16 = atoi(e);
+    if (const char* e = std::getenv("LIC_GS1_HI")) c->gs1_hi_plan = (e[0] != '0');
     if (const char* e = std::getenv("LIC_NO_GUARD")) c->no_guard_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_YHAT_HI")) c->a_hi_only_enabled = (e[0] != '0');
     if (const char* e = std::getenv("LIC_S2HALO")) c->s2halo_enabled = (e[0] != '0');
@@ -1242,7 +1264,7 @@ extern "C" lic_status lic_open(const uint8_t* licw, size_t len, int device, uint
         }
         if ((st = plan_layer(c, Ly))) return bail(st);
     }
-    if ((st = plan_l1r(c))) return bail(st);
+    if ((st = plan_variants(c))) return bail(st);
     if (cudaMemset(c->d_range, 0, 8) != cudaSuccess) return bail(LIC_ECUDA);
     finish_plans(c);
     c->dbg_elems = dbg;
@@ -1283,7 +1305,7 @@ extern "C" lic_status lic_bind_workspace(lic_codec* c, void* dev_ptr, size_t byt
         lic_status r = plan_layer(c, Ly);        // tensor maps over the new planes
         if (r) { c->max_batch = old_batch; c->sticky = true; return r; }
     }
-    if (lic_status r = plan_l1r(c)) { c->max_batch = old_batch; c->sticky = true; return r; }
+    if (lic_status r = plan_variants(c)) { c->max_batch = old_batch; c->sticky = true; return r; }
     finish_plans(c);
     if (c->ws_own) { cudaFree(c->ws_own); c->ws_own = nullptr; }
     c->ws_user = dev_ptr;
@@ -1537,9 +1559,10 @@ static lic_status decode_impl(lic_codec* c, const int8_t* y_sym, uint32_t batch,
     ++c->launches;
     {
         // hyperprior y-hat = the integer symbols: exact in fp16, its lo plane is zero
-        ConvParams p1 = c->layers[GS1].prm;
+        Layer& L1g = c->gs1h_ok ? c->gs1h : c->layers[GS1];
+        ConvParams p1 = L1g.prm;
         p1.a_hi_only = c->kind == 1 && c->a_hi_only_enabled;
-        if ((r = run_layer(c, c->layers[GS1], p1, B, st))) return r;
+        if ((r = run_layer(c, L1g, p1, B, st))) return r;
     }
     for (int id : {GS2, GS3})
         if ((r = run_layer(c, c->layers[id], c->layers[id].prm, B, st))) return r;

@@ -800,7 +800,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     const int hx = p.sub4 ? 2 * (tc.gx0 - 1) + (gi & 1) : tc.gx0 - 1;
                     const int hy = p.sub4 ? 2 * (tc.gy0 - 1) + (gi >> 1) : tc.gy0 - 1;
                     mbar_wait(&hempty_bar[hs], hphase ^ 1);
-                    uint8_t* hb = smem + p.off_halo + hs * (p.split * p.halo_plane_bytes);
+                    uint8_t* hb = smem + p.off_halo + hs * (p.halo_planes * p.halo_plane_bytes);
                     if (elect_one()) {
                         expect(&hfull_bar[hs], hbytes);
                         ld5(hb, &mapA, &hfull_bar[hs], c * kBK, hx, hy, tc.b, 0);
@@ -897,7 +897,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                 constexpr bool LO = decltype(lo_c)::value;
                 constexpr bool SPLIT = decltype(split_c)::value;   // a K slice (split-K layers)
                 const uint32_t sbo = (uint32_t)p.halo_w * 128;
-                const uint32_t hstride = (uint32_t)p.split * p.halo_plane_bytes;
+                const uint32_t hstride = (uint32_t)p.halo_planes * p.halo_plane_bytes;
                 const uint64_t lo16 = p.halo_plane_bytes >> 4;
                 const uint64_t bstep16 = b_bytes >> 4;
                 const uint32_t halo0 = smem_u32(smem + p.off_halo), stage0 = smem_u32(smem);
@@ -980,7 +980,7 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                     if (p.trace) w_halo += clock64() - tw0;
                     tc_fence_after();
                     if (lane == 0 && c == 0 && gi == 0) LIC_TRACE(it, T_MMA_K0);
-                    const uint32_t hb = smem_u32(smem + p.off_halo + hs * (p.split * p.halo_plane_bytes));
+                    const uint32_t hb = smem_u32(smem + p.off_halo + hs * (p.halo_planes * p.halo_plane_bytes));
                     // descriptors of the halo slot (hi, lo planes); a tap's window adds its row
                     // offset (s_tapoff: 16-byte units, no carry out of the 14-bit address field)
                     const uint64_t ahb = sdesc_sw128_sbo(hb, sbo);

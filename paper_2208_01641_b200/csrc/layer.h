@@ -65,6 +65,7 @@ struct ConvParams {
     int sub4;                         // halo mode for a 5x5/s2 conv: 4 parity sub-grid halos per chunk,
                                       // tap groups tap0[g] / ntaps[g] (g = py * 2 + px)
     uint32_t off_halo, halo_plane_bytes;
+    int halo_planes;                  // planes per halo ring slot: split, or 1 for a plan whose input is hi-only
     int wres;                         // all weight tiles resident in smem (loaded once per CTA)
     uint32_t off_wres;
     int tmem_cols, acc_stride, n_accbuf;
