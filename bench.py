@@ -281,7 +281,8 @@ def measure(args, name, rank, world, local, threads, full):
     cfg = CONFIGS[name]
     H, W = cfg["H"], cfg["W"]
     B = args.batch if (args.batch and name == args.config) else cfg["B"]
-    steps = args.steps if full else max(10, min(args.steps, 40))
+    # default run: >= 3000 frames; the driver passes --steps explicitly
+    steps = (args.steps or -(-3000 // B)) if full else max(10, min(args.steps or 40, 40))
     split = 2 if args.precision == "split" else 1
     spec = ModelSpec(kind=cfg["kind"], N=cfg["N"], M=cfg["M"], activation=1 if args.activation == "1dn" else 0)
     blob = write_licw(spec, generate_weights(spec, seed=0))
@@ -295,7 +296,10 @@ def measure(args, name, rank, world, local, threads, full):
     # the stream: local frame i of rank r is global frame t = r + G*i (frame t mod 8 of seed 1000)
     base = torch.from_numpy(synth_frames_u8(STREAM_T, H, W, seed=STREAM_SEED))
     nfr = steps * B
-    nloc = max(nfr, args.warmup * B)
+    # frames held on the device (and pinned on the host): at most ~2.8 GB of u8 frames; longer
+    # runs push the same buffer through again (one lic_pipeline_run call per pass, run_n)
+    nbuf = min(nfr, max(B, (int(2.8e9) // (H * W * 3)) // B * B))
+    nloc = max(nbuf, args.warmup * B)
     gidx = (rank + world * torch.arange(nloc)) % STREAM_T
     dev_in = base[gidx].cuda()                                  # frames resident in HBM
     dev_out = torch.empty_like(dev_in)
@@ -308,13 +312,30 @@ def measure(args, name, rank, world, local, threads, full):
         if world > 1:
             dist.barrier()
 
+    def run_n(p, src, dst, n):
+        """n frames through the pipeline, in passes over the nbuf frames on the device."""
+        agg, done = None, 0
+        while done < n:
+            k = min(nbuf, n - done)
+            s_ = p.run(src, dst, k)
+            if agg is None:
+                agg = dict(s_)
+            else:
+                for key in ("frames", "seconds", "y_bytes", "z_bytes", "symbol_mismatches", "gpu_busy_s",
+                            "coder_busy_s", "gpu_launches"):
+                    agg[key] += s_[key]
+                for key in ("latency_p95_ms", "latency_max_ms"):
+                    agg[key] = max(agg[key], s_[key])
+            done += k
+        return agg
+
     def timed(p, src, dst, n, clocks=None):
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if clocks:
             clocks.__enter__()
         ev0.record()
-        st = p.run(src, dst, n)
+        st = run_n(p, src, dst, n)
         ev1.record()
         torch.cuda.synchronize()
         if clocks:
@@ -415,7 +436,7 @@ def measure(args, name, rank, world, local, threads, full):
     fo = torch.empty((B, H, W, 3), dtype=torch.uint8, device="cuda")
 
     def gpu_step(i):
-        fr = dev_in[(i * B) % nfr:(i * B) % nfr + B]
+        fr = dev_in[(i * B) % nbuf:(i * B) % nbuf + B]
         codec.encode(fr, ys, yi, zs, stream=s, u8=True)
         if codec.hyper:
             codec.hyper_indexes(zs, yi2, stream=s)
@@ -458,7 +479,7 @@ def measure(args, name, rank, world, local, threads, full):
 
     # ---- 7. pipeline timeline (untimed): GPU idle while work was ready
     tp = lic.Pipeline(codec, inflight=args.inflight, timeline=True, **mk)
-    ntl = min(nfr, 48 * B)
+    ntl = min(nbuf, 48 * B)
     t_tl0 = time.perf_counter()
     tp.run(dev_in, dev_out, ntl)
     tl_ms = (time.perf_counter() - t_tl0) * 1e3
@@ -477,7 +498,7 @@ def measure(args, name, rank, world, local, threads, full):
 
     # ---- 9. serial reference (no overlap between stages)
     sp = lic.Pipeline(codec, inflight=1, serial=True, **mk)
-    nser = min(nfr, 16 * B)
+    nser = min(nbuf, 16 * B)
     t0 = time.perf_counter()
     sp.run(dev_in, dev_out, nser)
     serial_fps = nser / (time.perf_counter() - t0)
@@ -510,8 +531,9 @@ def measure(args, name, rank, world, local, threads, full):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=250)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=0,
+                    help="timed steps (batches); 0: >= 3000 frames (reference arm: 5 bounded samples)")
+    ap.add_argument("--warmup", type=int, default=8, help="untimed warm-up steps (8 x 4 frames >= SPEC.md:452's 30)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS),
                     help="BASELINE.json config (c3: the headline 720p hyperprior stream)")
@@ -631,7 +653,7 @@ def run_reference(args, rank, world):
         return
     cfg = CONFIGS[args.config]
     H, W = cfg["H"], cfg["W"]
-    steps, warm = args.steps, args.warmup
+    steps, warm = args.steps or 5, args.warmup
     # each step: a bounded sample (one 1280x64 strip = 1/12 of a padded 720p frame)
     from lic_synth import ModelSpec, generate_weights, synth_frame_u8
     from oracle import oracle as O
