@@ -53,10 +53,10 @@ def test_partial_batches_are_per_frame_identical(lic, kind):
     c.close()
 
 
-@pytest.mark.parametrize("kind,H,W", [(1, 8, 8), (0, 8, 8), (1, 2, 2), (0, 16, 16)])
+@pytest.mark.parametrize("kind,H,W", [(1, 8, 8), (0, 8, 8), (1, 2, 2), (0, 16, 16), (1, 16, 48)])
 def test_smallest_geometries(lic, kind, H, W):
     """Frames that pad to a single 64 x 64 (hyper: y 4 x 4, z 1 x 1) or 16 x 16 (factorized:
-    y 1 x 1) block: encode, indexes and decode against the oracle."""
+    y 1 x 1) block (W = 16, 48: rows of 3W bytes a multiple of 16 -- the row-halo g_a L1): encode, indexes and decode against the oracle."""
     spec = ModelSpec(kind=kind, N=128, M=192)
     w = generate_weights(spec, seed=0)
     hyper = kind == 1
