@@ -967,9 +967,9 @@ static lic_status upload(lic_codec* c, void* dst, const void* src, size_t bytes)
 }
 
 // per-codec epilogue settings of the layer plans (after plan_layer)
-// alternative plans picked per call: g_s L1 for a hi-only input (hyperprior decode) and the
-// row-halo plan of g_a L1 (u8 frames): copies of the layer (weights, buffers) planned
-// with l1_rows -- encode_impl picks it per call when the frames qualify
+// alternative plans of two layers, copies of the layer (weights, buffers) planned differently and
+// picked per call: g_s L1 with a hi-only halo ring (the hyperprior's integer y-hat, decode_impl)
+// and g_a L1 in row-halo mode (l1_rows; encode_impl, when the frames are u8 with 16-byte rows)
 static lic_status plan_variants(lic_codec* c) {
     c->gs1h_ok = false;
     if (c->layers[GS1].present && c->kind == 1 && c->a_hi_only_enabled && c->gs1_hi_plan && c->layers[GS1].prm.halo) {
