@@ -12,6 +12,7 @@
 #include <cstdint>
 
 #include "layer.h"
+#include "sigma_index.cuh"
 
 namespace lic {
 
@@ -56,15 +57,9 @@ __global__ void pack_chw_kernel(const float* __restrict__ in, int B, int C, int 
 // sigma -> index, the same arithmetic as the h_s L3 epilogue (EP_SIGMA in conv_umma.cu)
 __global__ void sigma_index_kernel(const float* __restrict__ sigma, size_t n, const float* __restrict__ table,
                                    uint8_t* __restrict__ idx) {
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const float s = fmaxf(sigma[i], 0.11f);
-        int lo = 0, hi = 63;
-        while (lo < hi) {
-            int mid = (lo + hi) >> 1;
-            if (table[mid] < s) lo = mid + 1; else hi = mid;
-        }
-        idx[i] = (uint8_t)lo;
-    }
+    const auto ltab = [&](int j) { return __ldg(table + j); };
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        idx[i] = (uint8_t)sigma_to_index(sigma[i], ltab);
 }
 
 static inline int grid_for(size_t n, int threads) {

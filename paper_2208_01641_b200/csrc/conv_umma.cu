@@ -32,6 +32,7 @@
 
 #include "layer.h"
 #include "ptx.cuh"
+#include "sigma_index.cuh"
 
 namespace lic {
 
@@ -1930,17 +1931,12 @@ conv_umma_kernel(const __grid_constant__ CUtensorMap mapA,
                             for (int j = 0; j < 16; ++j)
                                 if (j < nj) p.out_f32[chw0 + (size_t)(cb + j) * HWo] = fmaxf(v[j], 0.0f);
                         }
+                        // sigma' = max(relu(x), 0.11); index = #{j in [0, 62] : table_j < sigma'}
+                        // (sigma_index.cuh, the function lic_test_sigma_to_index checks exactly)
+                        const auto ltab = [&](int i) { return ldsf(tab + 4u * (uint32_t)i); };
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            // sigma' = max(relu(x), 0.11); index = #{j in [0, 62] : table_j < sigma'} by a
-                            // branch-free lower bound over the sorted table (steps 32 .. 1; the probed
-                            // position never passes 62) -- compact code: these layers run 1-2 tiles per
-                            // CTA, so their epilogue executes from a cold instruction cache
-                            const float s = fmaxf(fmaxf(v[j], 0.0f), 0.11f);
-                            int lo = 0;
-#pragma unroll
-                            for (int step = 32; step > 0; step >>= 1)
-                                lo = (ldsf(tab + 4u * (uint32_t)(lo + step - 1)) < s) ? lo + step : lo;
+                            const int lo = sigma_to_index(fmaxf(v[j], 0.0f), ltab);
                             if (j < nj) idx[chw0 + (size_t)(cb + j) * HWo] = (uint8_t)lo;
                         }
                         break;

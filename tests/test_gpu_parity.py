@@ -169,6 +169,18 @@ def test_sigma_to_index_exact(codec, hyper, lic):
     sig = np.concatenate([hyper["ref"][0]["hs3"].ravel(), tab, np.nextafter(tab, 0), np.nextafter(tab, 1e9),
                           np.array([0, 0.05, 0.11, 1e9], np.float32)]).astype(np.float32)
     assert np.array_equal(codec.test_sigma_to_index(sig), O.scale_index(sig, tab))
+    # the kernel arithmetic (sigma_index.cuh, also the h_s L3 epilogue) against the plain count: a log-uniform sweep
+    # over 1e-3 .. 1e4 and the 4 fp32 neighbours on each side of every table entry
+    rng = np.random.default_rng(7)
+    sweep = np.exp(rng.uniform(np.log(1e-3), np.log(1e4), 1 << 20)).astype(np.float32)
+    near = [tab.astype(np.float32)]
+    for d in (0, 1e9):
+        t = tab.astype(np.float32)
+        for _ in range(4):
+            t = np.nextafter(t, np.float32(d)).astype(np.float32)
+            near.append(t)
+    sig2 = np.concatenate([sweep] + near).astype(np.float32)
+    assert np.array_equal(codec.test_sigma_to_index(sig2), O.scale_index(sig2, tab))
 
 
 def test_bitstreams_bit_exact(codec, hyper, lic):
