@@ -5,8 +5,9 @@
 import sys
 
 lines = open(sys.argv[1]).read().splitlines()
-hdr = lines[1].split()
-rows = [l.split() for l in lines[2:] if l.strip() and l.split()[0].isdigit()]
+h0 = next(i for i, l in enumerate(lines) if l.split()[:1] == ["tile"])      # (skips plan-debug lines)
+hdr = lines[h0].split()
+rows = [l.split() for l in lines[h0 + 1:] if l.strip() and l.split()[0].isdigit()]
 ix = {h: i for i, h in enumerate(hdr)}
 rows = rows[4:-2] if len(rows) > 8 else rows
 acc = {}
