@@ -152,7 +152,7 @@ def test_decode_saturated_symbols_counted_and_finite(lic, w):
 # ---------------------------------------------------------------- workspace
 def test_bound_workspace_bit_identical(lic, w):
     import torch
-    H, W, B = 136, 200, 2
+    H, W, B = 136, 208, 2          # 3W % 16 == 0: the rebound row-halo g_a L1 and hi-only g_s L1 plans run
     c = lic.Codec(write_licw(HYPER, w), H, W, max_batch=B)
     fr = synth_frames_u8(B, H, W, seed=21)
 
